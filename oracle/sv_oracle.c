@@ -1,0 +1,365 @@
+/*
+ * sv_oracle.c -- plain, slow, obviously-correct CPU oracle for the Grover
+ * state-vector hot path (arxiv quant-ph/9804039, Obenland & Despain,
+ * "A Parallel Quantum Computer Simulator").
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py (cpu_baseline leg and --impl reference) may load this library.
+ * It shares no code, header, table or constant generator with the CUDA path
+ * under paper_quant_ph_9804039_b200/csrc/; neither side includes the other.
+ *
+ * Arithmetic: complex double (C99 _Complex), plain loops, no SIMD intrinsics,
+ * no blocking, no fusion.  Sums use long double with Kahan compensation.
+ *
+ * Citation keys: P:NNNN = line of /root/reference/PAPER.md (the paper's
+ * PostScript text), S:NNN = line of SPEC.md; "G<k>" = a reading listed in
+ * DESIGN.md section "Readings" (the paper is silent on Grover's iteration:
+ * it only cites [Grov96] in section 1.5).
+ *
+ * Index convention ("The bit value of a state corresponds to the
+ * index of that state in the vector"; Fig. 3, P:3144-3380 pairs (a0,a1) and
+ * (a2,a3) for the low bit): qubit q is bit q of the amplitude index.
+ */
+#include <complex.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef double complex cplx;
+
+/* ------------------------------------------------------------------------ */
+/* Seeded generators (G6, G8).  Implemented here independently of the CUDA  */
+/* library, which has its own implementation; tests check they agree.      */
+/* ------------------------------------------------------------------------ */
+
+#define OR_TAG_MARK 0x4D41524B00000000ULL /* "MARK" */
+#define OR_TAG_INIT 0x494E495400000000ULL /* "INIT" */
+
+/* SplitMix64 step: state += golden gamma, then the 64-bit finaliser. */
+uint64_t or_splitmix64_next(uint64_t *state)
+{
+    uint64_t z;
+    *state = *state + 0x9E3779B97F4A7C15ULL;
+    z = *state;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+/* Counter hash: one SplitMix64 output from state x (G8). */
+uint64_t or_hash64(uint64_t x)
+{
+    uint64_t s = x;
+    return or_splitmix64_next(&s);
+}
+
+/* Keyed bijection pi_seed on n-bit integers (G6):
+ *   x <- (x*k1 + k2) mod 2^n ; x ^= x >> s ; x <- (x*k3) mod 2^n ; x ^= x >> s
+ * with s = ceil(n/2), k1 and k3 odd, (k1,k2,k3) = first three SplitMix64
+ * outputs from state seed ^ TAG_MARK. */
+static void or_perm_keys(int n, uint64_t seed, uint64_t k[3])
+{
+    uint64_t st = seed ^ OR_TAG_MARK;
+    (void)n;
+    k[0] = or_splitmix64_next(&st) | 1ULL;
+    k[1] = or_splitmix64_next(&st);
+    k[2] = or_splitmix64_next(&st) | 1ULL;
+}
+
+uint64_t or_perm(int n, uint64_t seed, uint64_t x)
+{
+    uint64_t k[3];
+    uint64_t mask = (n >= 64) ? ~0ULL : ((1ULL << n) - 1ULL);
+    int s = (n + 1) / 2;
+    or_perm_keys(n, seed, k);
+    x = (x * k[0] + k[1]) & mask;
+    x ^= x >> s;
+    x = (x * k[2]) & mask;
+    x ^= x >> s;
+    return x;
+}
+
+static int cmp_u64(const void *a, const void *b)
+{
+    uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+    return (x > y) - (x < y);
+}
+
+/* Marked set M = sort{ pi_seed(j) : 0 <= j < m }  (G6 / G7).  Returns 0, or
+ * -1 if m > 2^n. */
+int or_marked_from_seed(int n, uint64_t m, uint64_t seed, uint64_t *out)
+{
+    uint64_t N = 1ULL << n, j;
+    if (m > N) return -1;
+    for (j = 0; j < m; ++j) out[j] = or_perm(n, seed, j);
+    qsort(out, (size_t)m, sizeof(uint64_t), cmp_u64);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Initial states                                                           */
+/* ------------------------------------------------------------------------ */
+
+/* |s> = H^{(x)n}|0>: every amplitude 2^{-n/2} (Fig. 1(b), P:2284-2286 is the
+ * n = 1 case: amplitudes 1/sqrt2, probabilities 1/2). */
+void or_init_uniform(int n, cplx *a)
+{
+    uint64_t N = 1ULL << n, i;
+    double v = ldexp(1.0, -n);          /* 2^{-n} */
+    v = sqrt(v);                         /* 2^{-n/2}, exact for even n */
+    for (i = 0; i < N; ++i) a[i] = v;
+}
+
+/* |0...0> (Fig. 1(a)). */
+void or_init_zero_state(int n, cplx *a)
+{
+    uint64_t N = 1ULL << n, i;
+    for (i = 0; i < N; ++i) a[i] = 0.0;
+    a[0] = 1.0;
+}
+
+/* Unnormalised complex Gaussian draw for amplitude i (G8):
+ *   u_j = ((hash64(key ^ (2i+j)) >> 11) + 0.5) * 2^-53,  j = 0, 1
+ *   r = sqrt(-2 ln u_0), phi = 2 pi u_1, z = r cos(phi) + i r sin(phi). */
+void or_gauss_draw(uint64_t key, uint64_t i, double *re, double *im)
+{
+    uint64_t h0 = or_hash64(key ^ (2ULL * i));
+    uint64_t h1 = or_hash64(key ^ (2ULL * i + 1ULL));
+    double u0 = ((double)(h0 >> 11) + 0.5) * 0x1.0p-53;
+    double u1 = ((double)(h1 >> 11) + 0.5) * 0x1.0p-53;
+    double r = sqrt(-2.0 * log(u0));
+    double phi = 6.283185307179586 * u1;
+    *re = r * cos(phi);
+    *im = r * sin(phi);
+}
+
+uint64_t or_gauss_key(uint64_t seed) { return or_hash64(seed ^ OR_TAG_INIT); }
+
+/* Seeded complex Gaussian start normalised to ||a||_2 = 1 (G8).  If
+ * round_to_c64 != 0 the normalised amplitudes are rounded to float (the
+ * c64 dtype) and the oracle continues in double from the rounded values
+ * (G12). */
+void or_init_gaussian(int n, uint64_t seed, int round_to_c64, cplx *a)
+{
+    uint64_t N = 1ULL << n, i, key = or_gauss_key(seed);
+    long double s = 0.0L, c = 0.0L;
+    double scale;
+    for (i = 0; i < N; ++i) {
+        double re, im;
+        long double y, t;
+        or_gauss_draw(key, i, &re, &im);
+        a[i] = CMPLX(re, im);
+        y = (long double)(re * re + im * im) - c;   /* Kahan */
+        t = s + y;
+        c = (t - s) - y;
+        s = t;
+    }
+    scale = 1.0 / sqrt((double)s);
+    for (i = 0; i < N; ++i) {
+        double re = creal(a[i]) * scale, im = cimag(a[i]) * scale;
+        if (round_to_c64) { re = (double)(float)re; im = (double)(float)im; }
+        a[i] = CMPLX(re, im);
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* The operations of one Grover iteration                                   */
+/* ------------------------------------------------------------------------ */
+
+/* Phase oracle O = I - 2 sum_m |m><m| (G3): negate every listed amplitude. */
+void or_oracle_flip(cplx *a, const uint64_t *marked, uint64_t m)
+{
+    uint64_t j;
+    for (j = 0; j < m; ++j) a[marked[j]] = -a[marked[j]];
+}
+
+/* One general 2x2 transformation [w x; y z] on qubit q: "a 2x2 transformation
+ * on a vector of size V, is a sequence of V/2 independent 2x2
+ * transformations ... the simulator splits the state space so that the bit
+ * value of the states in the vector differ only in the position of that bit"
+ * (section 2.1; Fig. 3). */
+void or_apply_2x2(int n, cplx *a, int q, cplx w, cplx x, cplx y, cplx z)
+{
+    uint64_t N = 1ULL << n, bit = 1ULL << q, i;
+    for (i = 0; i < N; ++i) {
+        if (i & bit) continue;              /* i has bit q = 0; partner i|bit */
+        {
+            cplx a0 = a[i], a1 = a[i | bit];
+            a[i] = w * a0 + x * a1;
+            a[i | bit] = y * a0 + z * a1;
+        }
+    }
+}
+
+/* Unnormalised Walsh-Hadamard transform W = (sqrt2 H)^{(x)n}: for q = 0..n-1
+ * apply Fig. 3's 2x2 with w = x = y = 1, z = -1, i.e. (x,y) -> (x+y, x-y). */
+void or_wht(int n, cplx *a)
+{
+    int q;
+    for (q = 0; q < n; ++q) or_apply_2x2(n, a, q, 1.0, 1.0, 1.0, -1.0);
+}
+
+/* F0 = 2|0><0| - I (G2), with the single exact 2^{-n} normalisation of the
+ * two unnormalised transforms folded in (G5). */
+void or_f0_scaled(int n, cplx *a)
+{
+    uint64_t N = 1ULL << n, i;
+    double s = ldexp(1.0, -n);
+    a[0] = a[0] * s;
+    for (i = 1; i < N; ++i) a[i] = -a[i] * s;
+}
+
+/* WHT diffusion D = H^n F0 H^n = 2|s><s| - I (north star). */
+void or_diffuse_wht(int n, cplx *a)
+{
+    or_wht(n, a);
+    or_f0_scaled(n, a);
+    or_wht(n, a);
+}
+
+/* Mean diffusion (inversion about the mean): mu = (1/N) sum_i a_i, then
+ * a_i <- 2 mu - a_i (north star).  The global sum is the paper's
+ * "accumulate and redistribute a sum" (Eq. 3). */
+cplx or_sum(int n, const cplx *a)
+{
+    uint64_t N = 1ULL << n, i;
+    long double sr = 0.0L, si = 0.0L, cr = 0.0L, ci = 0.0L;
+    for (i = 0; i < N; ++i) {
+        long double yr = (long double)creal(a[i]) - cr, yi = (long double)cimag(a[i]) - ci;
+        long double tr = sr + yr, ti = si + yi;
+        cr = (tr - sr) - yr; ci = (ti - si) - yi;
+        sr = tr; si = ti;
+    }
+    return CMPLX((double)sr, (double)si);
+}
+
+void or_diffuse_mean(int n, cplx *a)
+{
+    uint64_t N = 1ULL << n, i;
+    cplx mu = or_sum(n, a) * ldexp(1.0, -n);
+    for (i = 0; i < N; ++i) a[i] = 2.0 * mu - a[i];
+}
+
+/* k Grover iterations a <- (D O)^k a.  diffusion: 0 = WHT, 1 = mean. */
+void or_iterate(int n, cplx *a, const uint64_t *marked, uint64_t m, int k,
+                int diffusion)
+{
+    int it;
+    for (it = 0; it < k; ++it) {
+        or_oracle_flip(a, marked, m);
+        if (diffusion == 0) or_diffuse_wht(n, a);
+        else or_diffuse_mean(n, a);
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* Readouts                                                                 */
+/* ------------------------------------------------------------------------ */
+
+/* "The probability of each state is defined as the square of this complex
+ * amplitude". */
+void or_probabilities(int n, const cplx *a, double *p)
+{
+    uint64_t N = 1ULL << n, i;
+    for (i = 0; i < N; ++i) p[i] = creal(a[i]) * creal(a[i]) + cimag(a[i]) * cimag(a[i]);
+}
+
+double or_marked_mass(const cplx *a, const uint64_t *marked, uint64_t m)
+{
+    long double s = 0.0L;
+    uint64_t j;
+    for (j = 0; j < m; ++j) {
+        cplx v = a[marked[j]];
+        s += (long double)(creal(v) * creal(v) + cimag(v) * cimag(v));
+    }
+    return (double)s;
+}
+
+double or_norm_sq(int n, const cplx *a)
+{
+    uint64_t N = 1ULL << n, i;
+    long double s = 0.0L;
+    for (i = 0; i < N; ++i) s += (long double)(creal(a[i]) * creal(a[i]) + cimag(a[i]) * cimag(a[i]));
+    return (double)s;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Brute force: the gate as a 2^n x 2^n matrix (section 1.3)   */
+/* ------------------------------------------------------------------------ */
+
+/* K = H (x) H (x) ... (x) H (n factors), H = 2^{-1/2} [[1,1],[1,-1]], built
+ * by repeated Kronecker products: K_{m+1}[(r1,r0),(c1,c0)] = H[r1][c1] K_m[r0][c0].
+ * Row-major, dim 2^n.  Only for n <= 8. */
+int or_dense_hadamard(int n, double *K)
+{
+    static const double h = 0.70710678118654752440;
+    const double H[2][2] = {{h, h}, {h, -h}};
+    int m;
+    uint64_t dim = 1;
+    if (n < 0 || n > 8) return -1;
+    K[0] = 1.0;
+    for (m = 0; m < n; ++m) {
+        uint64_t nd = dim * 2, r, c;
+        double *tmp = (double *)malloc(sizeof(double) * nd * nd);
+        for (r = 0; r < nd; ++r)
+            for (c = 0; c < nd; ++c)
+                tmp[r * nd + c] = H[r / dim][c / dim] * K[(r % dim) * dim + (c % dim)];
+        memcpy(K, tmp, sizeof(double) * nd * nd);
+        free(tmp);
+        dim = nd;
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Emulated sharding (section 3.1; Fig. 8)         */
+/* ------------------------------------------------------------------------ */
+
+/* The owner of a state is the concatenation of the parallel bits, MSB first
+ * (P:4102-4103): with P = 2^g shards the parallel bits are the top g
+ * bits, so shard r holds global indices [r N_l, (r+1) N_l), N_l = 2^{n-g}.
+ *
+ * The reorganisation (Fig. 8) that makes the top-g local bits the new
+ * parallel bits: block (r, j) = elements of shard r whose top-g local bits
+ * equal j; if the owner does not change (j == r) "do nothing", otherwise it
+ * is sent to shard j and stored there as block r.  Applied twice it is the
+ * identity.  shards[r] points to N_l amplitudes; tmp is scratch of N_l. */
+void or_reorganize(int n, int g, cplx **shards, cplx *tmp_all)
+{
+    uint64_t P = 1ULL << g, Nl = 1ULL << (n - g), B = Nl / P, r, j, i;
+    /* tmp_all holds P * N_l amplitudes: new shard j = concat_r old(r, j). */
+    for (r = 0; r < P; ++r)
+        for (j = 0; j < P; ++j)
+            for (i = 0; i < B; ++i)
+                tmp_all[j * Nl + r * B + i] = shards[r][j * B + i];
+    for (j = 0; j < P; ++j)
+        for (i = 0; i < Nl; ++i) shards[j][i] = tmp_all[j * Nl + i];
+}
+
+/* Unnormalised WHT over P = 2^g shards: local bits on every shard, one
+ * reorganisation, the (new) top-g local bits, reorganise back.  Requires
+ * 2g <= n.  Must equal or_wht on the concatenated vector. */
+int or_wht_sharded(int n, int g, cplx *a_global)
+{
+    uint64_t P = 1ULL << g, Nl, r;
+    int nl = n - g, q;
+    cplx **sh;
+    cplx *tmp;
+    if (g < 0 || 2 * g > n) return -1;
+    Nl = 1ULL << nl;
+    sh = (cplx **)malloc(sizeof(cplx *) * P);
+    tmp = (cplx *)malloc(sizeof(cplx) * P * Nl);
+    for (r = 0; r < P; ++r) sh[r] = a_global + r * Nl;
+    for (r = 0; r < P; ++r)
+        for (q = 0; q < nl; ++q) or_apply_2x2(nl, sh[r], q, 1.0, 1.0, 1.0, -1.0);
+    if (g > 0) {
+        or_reorganize(n, g, sh, tmp);
+        for (r = 0; r < P; ++r)
+            for (q = nl - g; q < nl; ++q) or_apply_2x2(nl, sh[r], q, 1.0, 1.0, 1.0, -1.0);
+        or_reorganize(n, g, sh, tmp);
+    }
+    free(tmp);
+    free(sh);
+    return 0;
+}
