@@ -1,0 +1,287 @@
+#!/usr/bin/env python
+"""Benchmark of the Grover state-vector hot path on B200 (arxiv quant-ph/9804039).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c4]
+
+Workload (BASELINE.json): config c4 -- n = 32 qubits, complex64 (32 GiB state),
+uniform start, M = 256 marked indices from the seeded generator, 16 Grover
+iterations with the WHT diffusion; sharded over the N GPUs by the top log2 N
+qubits (strong scaling: the state is fixed).  One step = re-initialise the
+state + 16 iterations (all 2 x 32 butterfly stages, F0, O per iteration, plus
+the qubit-swap exchanges when N > 1).  Metric: Grover amplitude-updates/s =
+N_amp * k / t (G13), whole job.
+
+Prints ONE JSON line (rank 0).  The state (32 GiB) is far larger than the
+126 MB L2, so no L2 flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (n, dtype, M, k, diffusion, seed, init, description)
+    "c3": (28, "c64", 1, 64, "wht", 3, "uniform", "c3: n=28 complex64 (2 GiB), M=1, 64 WHT iterations"),
+    "c4": (32, "c64", 256, 16, "wht", 4, "uniform",
+           "c4: n=32 complex64 (32 GiB) sharded by top qubits, M=256 seeded, 16 WHT iterations"),
+    "c5w": (34, "c64", 1024, 8, "wht", 5, "gaussian", "c5: n=34 complex64 (128 GiB), Gaussian start, M=1024, 8 WHT"),
+    "c5m": (34, "c64", 1024, 8, "mean", 5, "gaussian", "c5: n=34 complex64 (128 GiB), Gaussian start, M=1024, 8 mean"),
+}
+METRIC = "grover_amp_updates_per_s"
+UNIT = "amplitude-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(config: str, world: int):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(f"{config}_P{world}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while running."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.lines: list[str] = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.device), "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=5)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline_sample(n: int, m: int, k: int, seed: int):
+    """The oracle as it stands (plain C, one thread) on a bounded sample of the
+    workload: same recipe at n qubits (uniform start, seeded marked set, WHT)."""
+    from oracle import oracle as orc
+
+    marked = orc.marked_from_seed(n, m, seed)
+    a = orc.init_uniform(n)
+    t0 = time.perf_counter()
+    orc.iterate(a, marked, k, orc.WHT)
+    dt = time.perf_counter() - t0
+    return (1 << n) * k / dt, dt
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (the tier's reference arm), rank 0 only."""
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    n_full, _, M, k_full, diff, seed, _, desc = CONFIGS[args.config]
+    n_s, k_s = 24, 1  # bounded sample per step: one WHT iteration at n=24 (~1-2 s)
+    m_s = max(1, M >> (n_full - n_s))
+    from oracle import oracle as orc
+
+    orc.build()
+    marked = orc.marked_from_seed(n_s, m_s, seed)
+    times = []
+    for i in range(args.warmup + args.steps):
+        a = orc.init_uniform(n_s)
+        t0 = time.perf_counter()
+        orc.iterate(a, marked, k_s, orc.WHT if diff == "wht" else orc.MEAN)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    t = sum(times)
+    value = (1 << n_s) * k_s * args.steps / t
+    sample = f"oracle (plain C, 1 thread) n={n_s}, M={m_s}, k={k_s} {diff} iteration per step"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": desc, "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_quant_ph_9804039_b200 as sv
+    from paper_quant_ph_9804039_b200 import dist as svd
+
+    rank, world, local = svd.init_process_group("nccl")
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    n, dts, M, k, diff, seed, init, desc = CONFIGS[args.config]
+    dtype = sv.SV_C64 if dts == "c64" else sv.SV_C128
+    dflag = sv.SV_DIFFUSE_WHT if diff == "wht" else sv.SV_DIFFUSE_MEAN
+    ikind = sv.SV_INIT_UNIFORM if init == "uniform" else sv.SV_INIT_GAUSSIAN
+    stream = torch.cuda.current_stream()
+    ctx = svd.sharded_init(n, seed, dtype, ikind, stream=stream.cuda_stream)
+    marked = sv.sv_marked_from_seed(n, M, seed)
+    sv.sv_set_marked(ctx, marked)
+
+    def step():
+        sv.sv_reset(ctx, seed, ikind)
+        sv.sv_iterate(ctx, k, dflag)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+
+    # ---- device-timed region: inputs resident, CUDA events on the launching stream
+    sv.sv_profile(ctx, True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t_ms = svd.max_over_ranks(ev0.elapsed_time(ev1))
+    prof = {sv.KERNEL_KIND_NAMES[i]: sv.sv_profile_read(ctx, i) for i in range(sv.SV_K_COUNT)}
+    sv.sv_profile(ctx, False)
+    N_amp = 1 << n
+    value = N_amp * k * args.steps / (t_ms / 1e3)
+
+    # roofline of the dominant kernel: the WHT tile pass (or the mean pass)
+    kname = "wht_tile" if diff == "wht" else "mean"
+    launches, kms = prof[kname]
+    local_bytes = (N_amp // world) * (8 if dtype == sv.SV_C64 else 16)
+    algo_bytes = 2 * local_bytes  # one read + one write of the local state per pass
+    avg_s = (kms / 1e3) / max(launches, 1)
+    peak, peak_src = measured_peaks()
+    achieved = algo_bytes / avg_s / 1e9
+    total_kernel_ms = sum(v[1] for name, v in prof.items() if name not in ("exchange", "allreduce"))
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": ncu_traffic(args.config, world), "kernel": f"{kname} (wht_tile_kernel)",
+                "algorithmic_bytes_per_launch": algo_bytes, "launches": launches, "avg_launch_ms": 1e3 * avg_s,
+                "share_of_step": kms / max(t_ms, 1e-9), "peak_source": peak_src}
+    gpu_launches = int(sum(v[0] for name, v in prof.items() if name not in ("exchange", "allreduce")))
+
+    # ---- end to end through the C ABI: pinned host inputs in, host scalar out
+    pinned = torch.empty(M, dtype=torch.int64, pin_memory=True)
+    pinned.numpy()[:] = marked.view(np.int64)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        host_marked = pinned.numpy().view(np.uint64)
+        sv.sv_set_marked(ctx, host_marked)          # H2D copy of the step's input
+        sv.sv_reset(ctx, seed, ikind)
+        sv.sv_iterate(ctx, k, dflag)
+        p_success = sv.sv_measure_marked_mass(ctx)  # D2H read of the step's result
+    e2e_s = svd.max_over_ranks(time.perf_counter() - t0)
+    e2e = {"value": N_amp * k * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(M * 8),
+           "d2h_bytes_per_step": 8, "p_success": p_success}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_s, k_s = 26, 2
+        m_s = max(1, M >> (n - n_s))
+        v, dt = cpu_baseline_sample(n_s, m_s, k_s, seed)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"plain C oracle, 1 thread, n={n_s} M={m_s} k={k_s} WHT iterations ({dt:.1f} s)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": desc, "n": n, "dtype": dts, "M": M, "k": k, "diffusion": diff,
+                           "parallelism": f"state sharded by top log2({world}) qubits" if world > 1 else "1 GPU",
+                           "l2": "inputs larger than L2 (state %d GiB >> 126 MB)" % ((N_amp * 8) >> 30)},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+                "clocks": clocks.summary(),
+                "phases_ms": {nm: v[1] for nm, v in prof.items() if v[0]},
+                "p_success": p_success}
+        print(json.dumps(line), flush=True)
+    sv.sv_free(ctx)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

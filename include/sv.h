@@ -1,0 +1,230 @@
+/*
+ * sv.h -- C ABI of the B200-native Grover state-vector hot path
+ * (arxiv quant-ph/9804039, Obenland & Despain, "A Parallel Quantum Computer
+ * Simulator", HPC'98).
+ *
+ * Implemented by paper_quant_ph_9804039_b200/libsv.so (hand-written CUDA for
+ * sm_100a + NCCL).  C99, extern "C", plain pointers and sizes; no torch types.
+ *
+ * Citations: P:NNNN is a line of the paper text (reference PAPER.md);
+ * S:NNN a line of the reference SPEC.md; G<k> a reading in DESIGN.md
+ * ("Readings").  The paper cites quantum search only in section 1.5
+ * (P:2946-2965); the iteration a <- D O a is fixed by the north star (G1).
+ *
+ * Conventions used by every call
+ *  - Amplitude store (section 1.2): a dense vector of N = 2^n
+ *    complex amplitudes; "the bit value of a state corresponds to the index of
+ *    that state in the vector": qubit q is bit q of the index (G4).
+ *    Layout is interleaved complex: SV_C64 = {float re, im} (8 B),
+ *    SV_C128 = {double re, im} (16 B) -- torch.complex64/complex128 compatible.
+ *  - Sharding (section 3.1): with P = 2^g ranks the "parallel
+ *    bits" are the top g qubits, concatenated MSB first into the rank
+ *    (P:4102-4103): rank r owns global indices [r*N/P, (r+1)*N/P).
+ *    local index = global index - r*N/P.  Between calls the layout is always
+ *    this natural one (internal qubit swaps are undone before a call returns).
+ *  - Status: every sv_status call returns SV_OK (0) or a negative code and
+ *    sets a thread-local message readable with sv_last_error().  After
+ *    SV_ECUDA / SV_ENCCL the context must be freed.
+ *  - Streams: all device work of a context is enqueued on one stream (the
+ *    caller's, if given in sv_dist.stream, else a stream the context creates).
+ *    Calls returning host data synchronise that stream; others are
+ *    asynchronous.  A context is single-writer: no concurrent
+ *    calls on the same sv_ctx.
+ *  - Ownership: the library owns every device buffer it allocates; input
+ *    arrays are copied before the call returns; output buffers belong to the
+ *    caller.
+ */
+#ifndef SV_H
+#define SV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SV_OK = 0,
+    SV_EINVAL = -1,  /* invalid argument (range, ordering, power-of-two, size) */
+    SV_ENOMEM = -2,  /* device or host allocation failed                       */
+    SV_ECUDA = -3,   /* CUDA runtime error (message has cudaGetErrorString)    */
+    SV_ENCCL = -4,   /* NCCL error (message has ncclGetErrorString)            */
+    SV_ESTATE = -5,  /* call not valid in the context's state                  */
+    SV_ETOOBIG = -6  /* host gather above the 2^26-entry guard     */
+} sv_status;
+
+typedef enum { SV_C64 = 0, SV_C128 = 1 } sv_dtype;
+
+typedef enum {
+    SV_INIT_UNIFORM = 0,    /* |s> = H^n|0>: every amplitude 2^{-n/2} (Fig. 1(b)) */
+    SV_INIT_GAUSSIAN = 1,   /* seeded complex Gaussian, normalised to ||a||_2 = 1 (G8)          */
+    SV_INIT_ZERO_STATE = 2  /* |0...0> (Fig. 1(a))                                      */
+} sv_init_kind;
+
+typedef enum {
+    SV_DIFFUSE_WHT = 0,   /* D = H^n F0 H^n, F0 = 2|0><0| - I (G2): 2 x n butterfly stages   */
+    SV_DIFFUSE_MEAN = 1   /* D a = 2 mean(a) - a: global sum (Eq. 3) + update   */
+} sv_diffusion;
+
+typedef struct sv_ctx sv_ctx; /* opaque; one per process (= per GPU rank) */
+
+/* Multi-GPU description (section 3.1).  world = P = 2^g >= 1.
+ *  - nccl_id != NULL: real rank `rank` of a P-rank job; nccl_id points to the
+ *    128-byte ncclUniqueId produced by sv_nccl_unique_id() on rank 0 and
+ *    broadcast by the caller (e.g. torch.distributed).  One GPU per rank.
+ *  - nccl_id == NULL and world > 1: single-process emulation of all P ranks on
+ *    one device (the state is held as P shards in rank order; qubit swaps are
+ *    device-local copies).  For tests of the sharded schedule on one GPU.
+ *  - device: CUDA device ordinal; stream: a cudaStream_t or NULL. */
+typedef struct {
+    int rank;
+    int world;
+    const void *nccl_id;
+    int device;
+    void *stream;
+} sv_dist;
+
+/* Create a context holding an n-qubit state and initialise it.
+ *   n: 1..40; seed: drives SV_INIT_GAUSSIAN (G8) -- other kinds ignore it;
+ *   dist: NULL = one GPU (device 0 / current device), own stream.
+ * Device memory: the local shard (2^{n-g} amplitudes) plus, when P > 1, one
+ * receive buffer of the same size for the out-of-place qubit swap.
+ * Errors: SV_EINVAL (n out of range, world not a power of two, shard too small
+ * for the WHT tiles: n - 2g < 13 for c64 / 12 for c128 when P > 1),
+ * SV_ENOMEM, SV_ECUDA, SV_ENCCL.  *out is NULL on error. */
+sv_status sv_init(sv_ctx **out, int n, uint64_t seed, sv_dtype dtype, sv_init_kind init,
+                  const sv_dist *dist);
+
+/* Re-initialise the existing state (no reallocation); the marked set is kept. */
+sv_status sv_reset(sv_ctx *ctx, uint64_t seed, sv_init_kind init);
+
+/* Set the marked set used by sv_iterate without applying O.
+ *   marked: m GLOBAL indices, strictly increasing, each < 2^n (host memory,
+ *   copied).  0 <= m <= 2^n; m = 0 means O = I (G17).
+ * Errors: SV_EINVAL (index out of range, not strictly increasing -- duplicates
+ * are errors, not double flips). */
+sv_status sv_set_marked(sv_ctx *ctx, const uint64_t *marked, uint64_t m);
+
+/* Set the marked set (as sv_set_marked) and apply the phase oracle
+ * O = I - 2 sum_m |m><m| once (G3: phase pi on the marked states). */
+sv_status sv_apply_oracle(sv_ctx *ctx, const uint64_t *marked, uint64_t m);
+
+/* Apply the diffusion D once (no oracle). */
+sv_status sv_diffuse(sv_ctx *ctx, sv_diffusion diffusion);
+
+/* Apply k Grover iterations a <- (D O)^k a with the context's marked set.
+ * WHT: each iteration runs both n-stage transforms (the paper's "sequence of
+ * V/2 independent 2x2 transformations" per qubit, with w = x = y
+ * = 1, z = -1; Fig. 3) around F0 and the exact 2^{-n} scale (G5), fused into
+ * multi-stage HBM passes; P > 1 adds one qubit-swap exchange per transform
+ * (the paper's reorganisation, Fig. 8).  MEAN: one fused
+ * flip + invert-about-mean pass per iteration plus (P > 1) one 2-double
+ * allreduce (Eq. 3's accumulate-and-redistribute).
+ * Errors: SV_EINVAL (k < 0), SV_ESTATE (no marked set was ever given). */
+sv_status sv_iterate(sv_ctx *ctx, int k, sv_diffusion diffusion);
+
+/* p_i = re^2 + im^2 in fp64 ("the probability of each state is defined as the
+ * square of this complex amplitude") for the context's resident
+ * indices (local shard; whole state in emulation), in local index order.
+ *   out: len doubles (len must equal the resident length); out_on_device: 1 =
+ *   device pointer, 0 = host pointer (host path guarded at 2^26 entries,
+ *   SV_ETOOBIG above). */
+sv_status sv_probabilities(sv_ctx *ctx, double *out, uint64_t len, int out_on_device);
+
+/* out (host) = sum over the marked set of |a_m|^2, fp64, allreduced over
+ * ranks (identical on every rank).  SV_ESTATE if no marked set. */
+sv_status sv_measure_marked_mass(sv_ctx *ctx, double *out);
+
+/* Copy `count` resident amplitudes starting at resident offset `offset` to
+ * host memory, dtype-native (8 or 16 bytes each).  SV_EINVAL if out of range. */
+sv_status sv_get_amplitudes(sv_ctx *ctx, void *host_out, uint64_t offset, uint64_t count);
+
+/* Overwrite `count` resident amplitudes from host memory (dtype-native).
+ * Used to start from an arbitrary (test-generated) state. */
+sv_status sv_set_amplitudes(sv_ctx *ctx, const void *host_in, uint64_t offset, uint64_t count);
+
+/* The seeded marked set of G6/G7: sort{pi_seed(j) : 0 <= j < m}, pi_seed the
+ * keyed bijection on n-bit integers.  Host-only; out has m entries.
+ * SV_EINVAL if m > 2^n or n not in 1..40. */
+sv_status sv_marked_from_seed(int n, uint64_t m, uint64_t seed, uint64_t *out);
+
+/* Context description; any pointer may be NULL.  local_len = resident
+ * amplitudes (2^{n-g}; 2^n in emulation). */
+sv_status sv_info(const sv_ctx *ctx, int *n, int *world, int *rank, uint64_t *local_len,
+                  sv_dtype *dtype);
+
+/* Block until all work enqueued on the context's stream is done. */
+sv_status sv_synchronize(sv_ctx *ctx);
+
+/* Write a fresh ncclUniqueId (len >= 128) for rank 0 to broadcast. */
+sv_status sv_nccl_unique_id(void *out, size_t len);
+
+/* ---- schedule introspection (host only; no device needed) ---------------- */
+
+/* One step of a device schedule.  kind: 0 = tile pass, 1 = qubit-swap
+ * exchange, 2 = whole-state kernel, 3 = oracle scatter.  For a tile pass the
+ * tile is the 2^T amplitudes whose local indices differ only in the slots of
+ * tile_mask; the butterfly stages run on the slots of proc_mask before (pre)
+ * and/or after (post) the elementwise op `mid` (0 none, 1 oracle O, 2 F0 with
+ * the 2^{-n} scale).  in_recv: the pass reads the swap receive buffer. */
+typedef struct {
+    int kind;
+    int pre;
+    int mid;
+    int post;
+    int in_recv;
+    int tile_bits;
+    uint64_t tile_mask;
+    uint64_t proc_mask;
+} sv_plan_step;
+
+/* The schedule sv_iterate(k, SV_DIFFUSE_WHT) (with_oracle = 1) or
+ * sv_diffuse(SV_DIFFUSE_WHT) (with_oracle = 0, k ignored) enqueues on every
+ * rank for an n-qubit state over world = 2^g ranks.  Writes at most cap steps,
+ * *nsteps = total.  SV_EINVAL for invalid (n, world, dtype). */
+sv_status sv_plan_wht(int n, int world, sv_dtype dtype, int k, int with_oracle,
+                      sv_plan_step *out, int cap, int *nsteps);
+
+/* ---- per-kernel device timing (CUDA events on the context's stream) ------ */
+
+typedef enum {
+    SV_K_WHT_TILE = 0,   /* multi-stage WHT tile pass                */
+    SV_K_WHT_WHOLE = 1,  /* whole state in one CTA (small n)         */
+    SV_K_MEAN = 2,       /* fused flip + invert-about-mean           */
+    SV_K_REDUCE = 3,     /* read-only flipped-sum reduction          */
+    SV_K_INIT = 4,       /* state initialisation                     */
+    SV_K_ORACLE = 5,     /* standalone oracle scatter                */
+    SV_K_READOUT = 6,    /* probabilities / marked mass              */
+    SV_K_EXCHANGE = 7,   /* qubit-swap all-to-all (NCCL or emulated) */
+    SV_K_ALLREDUCE = 8,  /* scalar NCCL allreduce                    */
+    SV_K_COUNT = 9
+} sv_kernel_kind;
+
+/* enable != 0: bracket every launch with CUDA events and count launches per
+ * kind (resets the counters); 0: stop recording. */
+sv_status sv_profile(sv_ctx *ctx, int enable);
+
+/* Synchronises, then returns launches and summed device milliseconds of one
+ * kind since sv_profile(ctx, 1). */
+sv_status sv_profile_read(sv_ctx *ctx, int kind, uint64_t *launches, double *total_ms);
+
+/* ---- layout introspection (host only; used by tests/test_layouts.py) ----- */
+
+/* Tile element index and swizzled shared-memory slot held by thread `tid`,
+ * register `reg` in register layout `phase` (0 = A, 1 = B, 2 = C) of the WHT
+ * tile kernel for `dtype`.  Returns 0, or -1 for out-of-range arguments. */
+int sv_debug_tile_layout(int dtype, int phase, int tid, int reg, int *tile_elem, int *smem_index);
+/* 1 if layout `phase` runs the butterfly stage of tile bit `bit`, else 0. */
+int sv_debug_tile_owner(int dtype, int phase, int bit);
+
+/* Release every resource of the context (NULL-safe). */
+void sv_free(sv_ctx *ctx);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char *sv_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SV_H */

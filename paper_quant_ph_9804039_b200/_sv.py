@@ -1,0 +1,230 @@
+"""Thin ctypes binding of include/sv.h (argument marshalling only).
+
+Every function here has the name of the C entry point it calls; all device
+work runs in libsv.so's CUDA kernels.  There is no CPU fallback: if libsv.so
+is missing or fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libsv.so")
+
+SV_OK, SV_EINVAL, SV_ENOMEM, SV_ECUDA, SV_ENCCL, SV_ESTATE, SV_ETOOBIG = 0, -1, -2, -3, -4, -5, -6
+SV_C64, SV_C128 = 0, 1
+SV_INIT_UNIFORM, SV_INIT_GAUSSIAN, SV_INIT_ZERO_STATE = 0, 1, 2
+SV_DIFFUSE_WHT, SV_DIFFUSE_MEAN = 0, 1
+(SV_K_WHT_TILE, SV_K_WHT_WHOLE, SV_K_MEAN, SV_K_REDUCE, SV_K_INIT, SV_K_ORACLE, SV_K_READOUT,
+ SV_K_EXCHANGE, SV_K_ALLREDUCE, SV_K_COUNT) = range(10)
+KERNEL_KIND_NAMES = ["wht_tile", "wht_whole", "mean", "reduce", "init", "oracle", "readout", "exchange", "allreduce"]
+
+NP_DTYPE = {SV_C64: np.complex64, SV_C128: np.complex128}
+
+
+class SvError(RuntimeError):
+    def __init__(self, code: int, fn: str, msg: str):
+        super().__init__(f"{fn} -> {code}: {msg}")
+        self.code = code
+
+
+class sv_dist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int), ("world", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
+                ("device", ctypes.c_int), ("stream", ctypes.c_void_p)]
+
+
+class sv_plan_step(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("pre", ctypes.c_int), ("mid", ctypes.c_int), ("post", ctypes.c_int),
+                ("in_recv", ctypes.c_int), ("tile_bits", ctypes.c_int), ("tile_mask", ctypes.c_uint64),
+                ("proc_mask", ctypes.c_uint64)]
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_quant_ph_9804039_b200.build` "
+                      "(no CPU fallback exists)")
+lib = ctypes.CDLL(LIB_PATH)
+
+_u64, _i32, _vp, _dp = ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)
+_ctxp = ctypes.c_void_p
+_SIGS = {
+    "sv_init": ([ctypes.POINTER(_ctxp), _i32, _u64, _i32, _i32, ctypes.POINTER(sv_dist)], _i32),
+    "sv_reset": ([_ctxp, _u64, _i32], _i32),
+    "sv_set_marked": ([_ctxp, _vp, _u64], _i32),
+    "sv_apply_oracle": ([_ctxp, _vp, _u64], _i32),
+    "sv_diffuse": ([_ctxp, _i32], _i32),
+    "sv_iterate": ([_ctxp, _i32, _i32], _i32),
+    "sv_probabilities": ([_ctxp, _vp, _u64, _i32], _i32),
+    "sv_measure_marked_mass": ([_ctxp, _dp], _i32),
+    "sv_get_amplitudes": ([_ctxp, _vp, _u64, _u64], _i32),
+    "sv_set_amplitudes": ([_ctxp, _vp, _u64, _u64], _i32),
+    "sv_marked_from_seed": ([_i32, _u64, _u64, _vp], _i32),
+    "sv_info": ([_ctxp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32),
+                 ctypes.POINTER(_u64), ctypes.POINTER(_i32)], _i32),
+    "sv_synchronize": ([_ctxp], _i32),
+    "sv_nccl_unique_id": ([_vp, ctypes.c_size_t], _i32),
+    "sv_plan_wht": ([_i32, _i32, _i32, _i32, _i32, ctypes.POINTER(sv_plan_step), _i32, ctypes.POINTER(_i32)], _i32),
+    "sv_profile": ([_ctxp, _i32], _i32),
+    "sv_profile_read": ([_ctxp, _i32, ctypes.POINTER(_u64), _dp], _i32),
+    "sv_free": ([_ctxp], None),
+    "sv_last_error": ([], ctypes.c_char_p),
+    "sv_debug_tile_layout": ([_i32, _i32, _i32, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)], _i32),
+    "sv_debug_tile_owner": ([_i32, _i32, _i32], _i32),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+
+def _check(rc: int, fn: str) -> None:
+    if rc != SV_OK:
+        raise SvError(rc, fn, lib.sv_last_error().decode())
+
+
+def _u64_array(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint64))
+
+
+class Ctx:
+    """Owns one sv_ctx* (freed on close / garbage collection)."""
+
+    def __init__(self, ptr: int, n: int, dtype: int):
+        self.ptr = ctypes.c_void_p(ptr)
+        self.n = n
+        self.dtype = dtype
+
+    def close(self):
+        if self.ptr:
+            lib.sv_free(self.ptr)
+            self.ptr = ctypes.c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def sv_init(n: int, seed: int = 0, dtype: int = SV_C64, init: int = SV_INIT_UNIFORM, rank: int = 0, world: int = 1,
+            nccl_id: bytes | None = None, device: int = 0, stream: int | None = None) -> Ctx:
+    out = ctypes.c_void_p()
+    dist = None
+    idbuf = None
+    if world > 1 or stream is not None or device != 0:
+        idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        dist = sv_dist(rank, world, ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None, device,
+                       stream if stream else None)
+    _check(lib.sv_init(ctypes.byref(out), n, seed, dtype, init, ctypes.byref(dist) if dist else None), "sv_init")
+    return Ctx(out.value, n, dtype)
+
+
+def sv_reset(ctx: Ctx, seed: int = 0, init: int = SV_INIT_UNIFORM) -> None:
+    _check(lib.sv_reset(ctx.ptr, seed, init), "sv_reset")
+
+
+def sv_set_marked(ctx: Ctx, marked) -> None:
+    m = _u64_array(marked)
+    _check(lib.sv_set_marked(ctx.ptr, m.ctypes.data if m.size else None, m.size), "sv_set_marked")
+
+
+def sv_apply_oracle(ctx: Ctx, marked) -> None:
+    m = _u64_array(marked)
+    _check(lib.sv_apply_oracle(ctx.ptr, m.ctypes.data if m.size else None, m.size), "sv_apply_oracle")
+
+
+def sv_diffuse(ctx: Ctx, diffusion: int = SV_DIFFUSE_WHT) -> None:
+    _check(lib.sv_diffuse(ctx.ptr, diffusion), "sv_diffuse")
+
+
+def sv_iterate(ctx: Ctx, k: int, diffusion: int = SV_DIFFUSE_WHT) -> None:
+    _check(lib.sv_iterate(ctx.ptr, k, diffusion), "sv_iterate")
+
+
+def sv_info(ctx: Ctx) -> dict:
+    n, w, r, dt = _i32(), _i32(), _i32(), _i32()
+    ll = _u64()
+    _check(lib.sv_info(ctx.ptr, ctypes.byref(n), ctypes.byref(w), ctypes.byref(r), ctypes.byref(ll),
+                       ctypes.byref(dt)), "sv_info")
+    return {"n": n.value, "world": w.value, "rank": r.value, "local_len": ll.value, "dtype": dt.value}
+
+
+def sv_probabilities(ctx: Ctx, out_device_ptr: int | None = None, length: int | None = None) -> np.ndarray | None:
+    """Host path returns a float64 array; device path writes to out_device_ptr."""
+    ll = sv_info(ctx)["local_len"] if length is None else length
+    if out_device_ptr is not None:
+        _check(lib.sv_probabilities(ctx.ptr, out_device_ptr, ll, 1), "sv_probabilities")
+        return None
+    p = np.empty(ll, dtype=np.float64)
+    _check(lib.sv_probabilities(ctx.ptr, p.ctypes.data, ll, 0), "sv_probabilities")
+    return p
+
+
+def sv_measure_marked_mass(ctx: Ctx) -> float:
+    v = ctypes.c_double()
+    _check(lib.sv_measure_marked_mass(ctx.ptr, ctypes.byref(v)), "sv_measure_marked_mass")
+    return v.value
+
+
+def sv_get_amplitudes(ctx: Ctx, offset: int = 0, count: int | None = None) -> np.ndarray:
+    if count is None:
+        count = sv_info(ctx)["local_len"] - offset
+    out = np.empty(count, dtype=NP_DTYPE[ctx.dtype])
+    _check(lib.sv_get_amplitudes(ctx.ptr, out.ctypes.data, offset, count), "sv_get_amplitudes")
+    return out
+
+
+def sv_set_amplitudes(ctx: Ctx, values: np.ndarray, offset: int = 0) -> None:
+    v = np.ascontiguousarray(values, dtype=NP_DTYPE[ctx.dtype])
+    _check(lib.sv_set_amplitudes(ctx.ptr, v.ctypes.data, offset, v.size), "sv_set_amplitudes")
+
+
+def sv_marked_from_seed(n: int, m: int, seed: int) -> np.ndarray:
+    out = np.empty(m, dtype=np.uint64)
+    _check(lib.sv_marked_from_seed(n, m, seed, out.ctypes.data if m else None), "sv_marked_from_seed")
+    return out
+
+
+def sv_synchronize(ctx: Ctx) -> None:
+    _check(lib.sv_synchronize(ctx.ptr), "sv_synchronize")
+
+
+def sv_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.sv_nccl_unique_id(buf, 128), "sv_nccl_unique_id")
+    return buf.raw
+
+
+def sv_plan_wht(n: int, world: int, dtype: int, k: int, with_oracle: bool) -> list[dict]:
+    cnt = _i32()
+    _check(lib.sv_plan_wht(n, world, dtype, k, int(with_oracle), None, 0, ctypes.byref(cnt)), "sv_plan_wht")
+    arr = (sv_plan_step * max(cnt.value, 1))()
+    _check(lib.sv_plan_wht(n, world, dtype, k, int(with_oracle), arr, cnt.value, ctypes.byref(cnt)), "sv_plan_wht")
+    return [{f: getattr(arr[i], f) for f, _ in sv_plan_step._fields_} for i in range(cnt.value)]
+
+
+def sv_profile(ctx: Ctx, enable: bool) -> None:
+    _check(lib.sv_profile(ctx.ptr, int(enable)), "sv_profile")
+
+
+def sv_profile_read(ctx: Ctx, kind: int) -> tuple[int, float]:
+    n = _u64()
+    ms = ctypes.c_double()
+    _check(lib.sv_profile_read(ctx.ptr, kind, ctypes.byref(n), ctypes.byref(ms)), "sv_profile_read")
+    return n.value, ms.value
+
+
+def sv_free(ctx: Ctx) -> None:
+    ctx.close()
+
+
+def sv_last_error() -> str:
+    return lib.sv_last_error().decode()

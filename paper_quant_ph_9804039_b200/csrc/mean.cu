@@ -1,0 +1,149 @@
+// mean.cu -- fused oracle flip + inversion about the mean (sm_100a).
+//
+// One Grover iteration with the mean diffusion (north star; D = 2|s><s| - I
+// acts as a_i <- 2 mean(a) - a_i):
+//     b_i  = (O a)_i        (negate marked entries, G3)
+//     a_i' = 2 mu - b_i,    mu = (1/N) sum_i b_i
+// The global sum is the paper's "accumulate and redistribute a sum from all
+// the processors after every laser operation ... two messages" (Eq. 3,
+// P:5248-5251).  Here the sum needed by iteration t+1, sum_i (O a')_i, is
+// accumulated while iteration t writes a' -- one HBM read + one write per
+// iteration.  Per-thread fp64 accumulation, warp shuffle -> block -> per-block
+// partials -> the last block to finish sums the partials in a fixed order
+// (deterministic: no floating-point atomics, G14).
+#include <cuda_runtime.h>
+
+#include "reduce.cuh"
+#include "sv_internal.h"
+
+namespace sv {
+
+constexpr int kMeanThreads = 256;
+constexpr int kMeanUnroll = 4;
+
+template <typename E> struct Vec;                 // one 16-byte vector
+template <> struct Vec<float2> { using T = float4; static constexpr int VE = 2; };
+template <> struct Vec<double2> { using T = double2; static constexpr int VE = 1; };
+
+__device__ __forceinline__ bool is_marked(unsigned long long i, const unsigned long long *mk,
+                                          unsigned long long lo, unsigned long long hi) {
+    while (lo < hi) {  // binary search in the block's sorted sub-list
+        unsigned long long md = (lo + hi) >> 1;
+        unsigned long long v = mk[md];
+        if (v == i) return true;
+        if (v < i) lo = md + 1; else hi = md;
+    }
+    return false;
+}
+
+__device__ __forceinline__ unsigned long long lower_bound(const unsigned long long *mk, unsigned long long n,
+                                                          unsigned long long key) {
+    unsigned long long lo = 0, hi = n;
+    while (lo < hi) {
+        unsigned long long md = (lo + hi) >> 1;
+        if (mk[md] < key) lo = md + 1; else hi = md;
+    }
+    return lo;
+}
+
+template <typename E, bool WRITE>
+__global__ void __launch_bounds__(kMeanThreads) mean_kernel(MeanArgs a) {
+    using V = typename Vec<E>::T;
+    using R = decltype(E{}.x);
+    constexpr int VE = Vec<E>::VE;
+    __shared__ double red[2 * (kMeanThreads / 32)];
+    __shared__ unsigned long long s_mlo, s_mhi;
+    const unsigned long long nvec = a.N / VE;
+    unsigned long long vlo, vhi;
+    block_chunk(nvec, vlo, vhi);
+    const auto *mk = reinterpret_cast<const unsigned long long *>(a.marked);
+    if (threadIdx.x == 0) {
+        s_mlo = lower_bound(mk, a.n_marked, vlo * VE);
+        s_mhi = lower_bound(mk, a.n_marked, vhi * VE);
+    }
+    __syncthreads();
+    const unsigned long long mlo = s_mlo, mhi = s_mhi;
+    const bool any = mhi > mlo;
+
+    R two_mr = 0, two_mi = 0;
+    if (WRITE) {
+        const double mr = a.sum_in[0] * a.inv_total, mi = a.sum_in[1] * a.inv_total;
+        two_mr = (R)(2.0 * mr);
+        two_mi = (R)(2.0 * mi);
+    }
+    V *p = reinterpret_cast<V *>(a.a);
+    double sr = 0.0, si = 0.0;
+    for (unsigned long long v0 = vlo + threadIdx.x; v0 < vhi; v0 += (unsigned long long)kMeanThreads * kMeanUnroll) {
+        V buf[kMeanUnroll];
+#pragma unroll
+        for (int u = 0; u < kMeanUnroll; ++u) {
+            const unsigned long long v = v0 + (unsigned long long)u * kMeanThreads;
+            if (v < vhi) buf[u] = p[v];
+        }
+#pragma unroll
+        for (int u = 0; u < kMeanUnroll; ++u) {
+            const unsigned long long v = v0 + (unsigned long long)u * kMeanThreads;
+            if (v >= vhi) continue;
+            E e[VE];
+            if constexpr (VE == 2) {
+                e[0].x = buf[u].x; e[0].y = buf[u].y;
+                e[1].x = buf[u].z; e[1].y = buf[u].w;
+            } else {
+                e[0].x = buf[u].x; e[0].y = buf[u].y;
+            }
+#pragma unroll
+            for (int q = 0; q < VE; ++q) {
+                const bool m = any && is_marked(v * VE + q, mk, mlo, mhi);
+                if (m) { e[q].x = -e[q].x; e[q].y = -e[q].y; }   // O
+                if (WRITE) {
+                    e[q].x = two_mr - e[q].x;                       // 2 mu - (O a)_i
+                    e[q].y = two_mi - e[q].y;
+                    // contribution of (O a')_i to the next iteration's sum
+                    sr += m ? -(double)e[q].x : (double)e[q].x;
+                    si += m ? -(double)e[q].y : (double)e[q].y;
+                } else {
+                    sr += (double)e[q].x;
+                    si += (double)e[q].y;
+                }
+            }
+            if (WRITE) {
+                if constexpr (VE == 2) {
+                    buf[u].x = e[0].x; buf[u].y = e[0].y; buf[u].z = e[1].x; buf[u].w = e[1].y;
+                } else {
+                    buf[u].x = e[0].x; buf[u].y = e[0].y;
+                }
+                p[v] = buf[u];
+            }
+        }
+    }
+    block_sum2(sr, si, red);
+    finalize(sr, si, a.partials, a.counter, a.sum_out, red);
+}
+
+int mean_grid(uint64_t N, sv_dtype dt) {
+    int dev = 0, sms = 148, per = 1;
+    SV_CUDA(cudaGetDevice(&dev));
+    SV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (dt == SV_C64)
+        SV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mean_kernel<float2, true>, kMeanThreads, 0));
+    else
+        SV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mean_kernel<double2, true>, kMeanThreads, 0));
+    uint64_t want = (uint64_t)sms * (uint64_t)(per > 0 ? per : 1);  // one full wave
+    const uint64_t nvec = N * elem_bytes(dt) / 16;
+    uint64_t cap = (nvec + kMeanThreads - 1) / kMeanThreads;       // >= 1 vector per thread
+    if (cap < 1) cap = 1;
+    return (int)(want < cap ? want : cap);
+}
+
+void launch_mean_grid(sv_dtype dt, const MeanArgs &a, int grid, bool write, cudaStream_t s) {
+    if (dt == SV_C64) {
+        if (write) mean_kernel<float2, true><<<grid, kMeanThreads, 0, s>>>(a);
+        else mean_kernel<float2, false><<<grid, kMeanThreads, 0, s>>>(a);
+    } else {
+        if (write) mean_kernel<double2, true><<<grid, kMeanThreads, 0, s>>>(a);
+        else mean_kernel<double2, false><<<grid, kMeanThreads, 0, s>>>(a);
+    }
+    SV_CUDA(cudaGetLastError());
+}
+
+}  // namespace sv

@@ -1,0 +1,189 @@
+// plan.cpp -- host-side schedule of the WHT diffusion (no device code).
+//
+// A transform applies the butterfly (x, y) -> (x + y, x - y) on every qubit,
+// i.e. "a sequence of V/2 independent 2x2 transformations" per bit (section
+// 2.1; Fig. 3 with w = x = y = 1, z = -1).  Stages on different
+// qubits commute, so a transform may visit the qubits in any grouping; each
+// group is one HBM pass of a tile kernel that runs all of the group's stages
+// on-chip.
+//
+// Sharding (section 3.1): with P = 2^g ranks the top g qubits
+// are the parallel bits.  "All of the processors can run in parallel
+// operating only on local data as long as they do not use any of the QU-bits
+// in the set N.  When the computation needs to operate on one of the bits in
+// N, a new set is picked and the simulator redistributes the data"
+// (P:4108-4111).  Our new set is always the top g LOCAL slots U, so the
+// redistribution (Fig. 8) is one all-to-all of contiguous
+// chunks; a second one restores the natural layout.
+#include <algorithm>
+
+#include "sv_internal.h"
+
+namespace sv {
+
+static uint64_t range_mask(int lo, int hi) {  // slots [lo, hi)
+    uint64_t m = 0;
+    for (int s = lo; s < hi; ++s) m |= 1ull << s;
+    return m;
+}
+
+// Tile of a group: its processed slots plus the lowest unprocessed slots up
+// to T (the unprocessed low slots give contiguous runs of >= 64 B).
+static Group make_group(uint64_t proc, int T, int nl) {
+    Group gr;
+    gr.proc = proc;
+    gr.tile = proc;
+    int have = __builtin_popcountll(proc);
+    for (int s = 0; s < nl && have < T; ++s)
+        if (!((gr.tile >> s) & 1)) { gr.tile |= 1ull << s; ++have; }
+    return gr;
+}
+
+// Split an ascending slot list into m near-equal ascending chunks.
+static std::vector<uint64_t> chunk(const std::vector<int> &slots, int cap) {
+    std::vector<uint64_t> out;
+    if (slots.empty()) return out;
+    int len = (int)slots.size();
+    int m = (len + cap - 1) / cap;
+    int base = len / m, extra = len % m, pos = 0;
+    for (int i = 0; i < m; ++i) {
+        int sz = base + (i < extra ? 1 : 0);
+        uint64_t mask = 0;
+        for (int j = 0; j < sz; ++j) mask |= 1ull << slots[pos++];
+        out.push_back(mask);
+    }
+    return out;
+}
+
+Plan make_plan(int n, int g, sv_dtype dtype) {
+    SV_CHECK(n >= 1 && n <= 40, SV_EINVAL, "n must be in [1, 40]");
+    SV_CHECK(dtype == SV_C64 || dtype == SV_C128, SV_EINVAL, "dtype must be SV_C64 or SV_C128");
+    SV_CHECK(g >= 0 && g <= 6, SV_EINVAL, "world must be 2^g with g in [0, 6]");
+    Plan p;
+    p.g = g;
+    p.nl = n - g;
+    p.T = tile_bits(dtype);
+    const int T = p.T, nl = p.nl;
+    const int Rs = T - carry_bits(dtype);  // processed slots per strided tile
+    if (g == 0 && nl <= T) {                // the whole state is one tile
+        p.whole = true;
+        return p;
+    }
+    SV_CHECK(nl - g >= T, SV_EINVAL,
+             "shard too small for the sharded WHT: need n - 2*log2(world) >= " + std::to_string(T));
+    p.groups.push_back(make_group(range_mask(0, T), T, nl));  // G1: contiguous
+    if (g == 0) {
+        std::vector<int> rest;
+        for (int s = T; s < nl; ++s) rest.push_back(s);
+        for (uint64_t m : chunk(rest, Rs)) p.groups.push_back(make_group(m, T, nl));
+        for (int i = 0; i < (int)p.groups.size(); ++i) p.fwd.push_back(i);
+        return p;
+    }
+    // P > 1: U = top g local slots, processed once before the swap (they hold
+    // logical qubits nl-g..nl-1) and once after it (logical nl..n-1).
+    std::vector<int> rest;
+    for (int s = T; s < nl - g; ++s) rest.push_back(s);
+    int take = std::min<int>(Rs - g, (int)rest.size());
+    uint64_t l1 = range_mask(nl - g, nl);
+    for (int j = 0; j < take; ++j) l1 |= 1ull << rest[rest.size() - 1 - j];
+    rest.resize(rest.size() - take);
+    std::vector<int> l0 = rest;
+    for (int s = nl - g; s < nl; ++s) l0.push_back(s);
+    p.fwd.push_back(0);
+    for (uint64_t m : chunk(l0, Rs)) {
+        p.groups.push_back(make_group(m, T, nl));
+        p.fwd.push_back((int)p.groups.size() - 1);
+    }
+    p.fwd.push_back(-1);  // reorganisation (qubit swap)
+    p.groups.push_back(make_group(l1, T, nl));
+    p.fwd.push_back((int)p.groups.size() - 1);
+    return p;
+}
+
+namespace {
+enum ItemKind { VISIT, OP, SWAP };
+struct Item {
+    ItemKind kind;
+    int arg;  // group index or MidOp
+};
+}  // namespace
+
+std::vector<Step> schedule_wht(const Plan &plan, int k, bool with_oracle) {
+    std::vector<Step> steps;
+    if (plan.whole) {
+        if (!with_oracle || k > 0) {
+            Step s;
+            s.kind = STEP_WHOLE;
+            steps.push_back(s);
+        }
+        return steps;
+    }
+    std::vector<Item> items;
+    auto transform = [&](bool forward) {
+        if (forward)
+            for (int gi : plan.fwd) items.push_back(gi < 0 ? Item{SWAP, 0} : Item{VISIT, gi});
+        else
+            for (auto it = plan.fwd.rbegin(); it != plan.fwd.rend(); ++it)
+                items.push_back(*it < 0 ? Item{SWAP, 0} : Item{VISIT, *it});
+    };
+    int reps = with_oracle ? k : 1;
+    for (int it = 0; it < reps; ++it) {
+        if (with_oracle) items.push_back({OP, MID_ORACLE});
+        transform(true);
+        items.push_back({OP, MID_F0});
+        transform(false);
+    }
+    // Fuse: visit(G) op visit(G) -> one pass; op visit(G) / visit(G) op at the
+    // ends -> one pass; everything else one pass per visit.
+    bool after_swap = false;
+    size_t i = 0, L = items.size();
+    while (i < L) {
+        Step s;
+        const Item &a = items[i];
+        if (a.kind == SWAP) {
+            s.kind = STEP_SWAP;
+            steps.push_back(s);
+            after_swap = true;
+            ++i;
+            continue;
+        }
+        s.kind = STEP_PASS;
+        s.in_recv = after_swap ? 1 : 0;
+        after_swap = false;
+        if (a.kind == VISIT) {
+            s.group = a.arg;
+            s.pre = 1;
+            if (i + 2 < L && items[i + 1].kind == OP && items[i + 2].kind == VISIT &&
+                items[i + 2].arg == a.arg) {
+                s.mid = items[i + 1].arg;
+                s.post = 1;
+                i += 3;
+            } else if (i + 1 < L && items[i + 1].kind == OP &&
+                       (i + 2 == L || items[i + 2].kind != VISIT)) {
+                s.mid = items[i + 1].arg;
+                i += 2;
+            } else {
+                i += 1;
+            }
+        } else {  // OP
+            if (i + 1 < L && items[i + 1].kind == VISIT) {
+                s.group = items[i + 1].arg;
+                s.mid = a.arg;
+                s.post = 1;
+                i += 2;
+            } else {
+                s.kind = STEP_SCATTER;
+                s.mid = a.arg;
+                i += 1;
+            }
+        }
+        // the oracle needs a contiguous tile (binary search of the sorted
+        // marked list); by construction it only meets groups[0]
+        if (s.kind == STEP_PASS && s.mid == MID_ORACLE)
+            SV_CHECK(s.group == 0, SV_EINVAL, "internal: oracle fused into a strided tile");
+        steps.push_back(s);
+    }
+    return steps;
+}
+
+}  // namespace sv

@@ -1,0 +1,561 @@
+// sv_api.cu -- the C ABI of include/sv.h: context, validation, dispatch of
+// the device schedule, NCCL plumbing, profiling.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <nccl.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "sv_internal.h"
+
+namespace sv {
+
+static thread_local std::string g_err;
+void set_error(const std::string &msg) { g_err = msg; }
+
+constexpr int kMaxGrid = 4096;  // capacity of the reduction partials
+
+}  // namespace sv
+
+using namespace sv;
+
+struct ProfEvent {
+    cudaEvent_t a, b;
+    int kind;
+};
+
+struct sv_ctx {
+    int n = 0, g = 0, rank = 0, world = 1;
+    bool emulated = false;
+    sv_dtype dt = SV_C64;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    ncclComm_t comm = nullptr;
+    void *state = nullptr;
+    void *recv = nullptr;
+    uint64_t nres = 0;       // resident amplitudes (2^{n-g}; 2^n emulated)
+    uint64_t nl_amps = 0;    // amplitudes per rank (2^{n-g})
+    uint64_t *d_marked = nullptr;
+    uint64_t marked_cap = 0;
+    uint64_t n_marked = 0;   // resident (local) marked entries
+    bool has_marked = false;
+    double *d_partials = nullptr;  // 2 * kMaxGrid
+    double *d_sums = nullptr;      // [0..1], [2..3] ping-pong; [4] norm; [6] scalar out
+    unsigned int *d_counter = nullptr;
+    int mgrid = 1;
+    Plan plan;
+    // profiling
+    bool prof = false;
+    std::vector<ProfEvent> pending;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
+    uint64_t launches[SV_K_COUNT] = {};
+    double ms[SV_K_COUNT] = {};
+};
+
+namespace {
+
+template <class F>
+sv_status guarded(F &&f) {
+    try {
+        f();
+        g_err.clear();
+        return SV_OK;
+    } catch (const Error &e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc &) {
+        g_err = "host allocation failed";
+        return SV_ENOMEM;
+    } catch (...) {
+        g_err = "unexpected exception";
+        return SV_ECUDA;
+    }
+}
+
+void dmalloc(void **p, size_t bytes, const char *what) {
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        throw Error{SV_ENOMEM, std::string("cudaMalloc(") + what + ", " + std::to_string(bytes) + " B) failed"};
+    }
+    SV_CUDA(e);
+}
+
+// Bracket one device operation with events when profiling; count launches.
+template <class F>
+void run(sv_ctx *c, int kind, F &&f) {
+    c->launches[kind] += 1;
+    if (!c->prof) {
+        f();
+        return;
+    }
+    std::pair<cudaEvent_t, cudaEvent_t> ev;
+    if (!c->pool.empty()) {
+        ev = c->pool.back();
+        c->pool.pop_back();
+    } else {
+        SV_CUDA(cudaEventCreate(&ev.first));
+        SV_CUDA(cudaEventCreate(&ev.second));
+    }
+    SV_CUDA(cudaEventRecord(ev.first, c->stream));
+    f();
+    SV_CUDA(cudaEventRecord(ev.second, c->stream));
+    c->pending.push_back({ev.first, ev.second, kind});
+}
+
+void drain_profile(sv_ctx *c) {
+    if (c->pending.empty()) return;
+    SV_CUDA(cudaStreamSynchronize(c->stream));
+    for (auto &p : c->pending) {
+        float ms = 0.f;
+        SV_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+        c->ms[p.kind] += ms;
+        c->pool.push_back({p.a, p.b});
+    }
+    c->pending.clear();
+}
+
+bool origin_here(const sv_ctx *c) { return c->emulated || c->rank == 0; }
+
+void allreduce_sum(sv_ctx *c, double *buf, size_t count) {
+    if (c->comm == nullptr) return;
+    run(c, SV_K_ALLREDUCE, [&] {
+        SV_NCCL(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, c->stream));
+    });
+}
+
+void do_init(sv_ctx *c, uint64_t seed, sv_init_kind kind) {
+    SV_CUDA(cudaSetDevice(c->device));
+    switch (kind) {
+        case SV_INIT_UNIFORM:
+            run(c, SV_K_INIT, [&] { launch_init_uniform(c->dt, c->state, c->nres, c->n, c->stream); });
+            break;
+        case SV_INIT_ZERO_STATE:
+            run(c, SV_K_INIT, [&] { launch_init_zero(c->dt, c->state, c->nres, origin_here(c) ? 1 : 0, c->stream); });
+            break;
+        case SV_INIT_GAUSSIAN: {
+            const uint64_t key = gauss_key(seed);
+            const uint64_t off = c->emulated ? 0 : (uint64_t)c->rank * c->nl_amps;
+            double *norm = c->d_sums + 4;
+            run(c, SV_K_INIT, [&] {
+                launch_gauss_norm(key, off, c->nres, c->d_partials, c->d_counter, norm, c->stream);
+            });
+            allreduce_sum(c, norm, 1);
+            run(c, SV_K_INIT, [&] { launch_gauss_write(c->dt, c->state, key, off, c->nres, norm, c->stream); });
+            break;
+        }
+        default:
+            throw Error{SV_EINVAL, "unknown sv_init_kind"};
+    }
+}
+
+void exchange(sv_ctx *c) {
+    const size_t eb = elem_bytes(c->dt);
+    const uint64_t P = 1ull << c->g;
+    const uint64_t B = c->nl_amps / P;  // amplitudes per (rank, peer) block
+    run(c, SV_K_EXCHANGE, [&] {
+        if (c->comm != nullptr) {
+            // chunk j of the shard (top-g local bits == j) goes to rank j and
+            // lands as its chunk `rank` (Fig. 8: blocks whose owner changes
+            // are sent; chunk j == rank stays local).
+            SV_NCCL(ncclAlltoAll(c->state, c->recv, B * (eb / 8), ncclUint64, c->comm, c->stream));
+        } else {
+            char *src = (char *)c->state, *dst = (char *)c->recv;
+            for (uint64_t r = 0; r < P; ++r)
+                for (uint64_t j = 0; j < P; ++j)
+                    SV_CUDA(cudaMemcpyAsync(dst + (j * c->nl_amps + r * B) * eb, src + (r * c->nl_amps + j * B) * eb,
+                                            B * eb, cudaMemcpyDeviceToDevice, c->stream));
+        }
+    });
+}
+
+void run_wht_schedule(sv_ctx *c, int k, bool with_oracle) {
+    if (c->plan.whole) {
+        if (with_oracle && k == 0) return;
+        run(c, SV_K_WHT_WHOLE, [&] {
+            launch_whole_state(c->dt, c->state, c->n, with_oracle ? k : 1, with_oracle ? 1 : 0, SV_DIFFUSE_WHT,
+                               c->d_marked, c->n_marked, c->stream);
+        });
+        return;
+    }
+    const std::vector<Step> steps = schedule_wht(c->plan, k, with_oracle);
+    const int total_bits = c->emulated ? c->n : c->plan.nl;
+    for (const Step &s : steps) {
+        if (s.kind == STEP_SWAP) {
+            exchange(c);
+            continue;
+        }
+        if (s.kind == STEP_SCATTER) {
+            if (s.mid == MID_ORACLE)
+                run(c, SV_K_ORACLE, [&] { launch_oracle_scatter(c->dt, c->state, c->d_marked, c->n_marked, c->stream); });
+            continue;
+        }
+        PassArgs a;
+        a.in = s.in_recv ? c->recv : c->state;
+        a.out = c->state;
+        a.marked = c->d_marked;
+        a.n_marked = c->n_marked;
+        a.f0_scale = ldexp(1.0, -c->n);
+        a.mid = s.mid;
+        a.has_origin = origin_here(c) ? 1 : 0;
+        a.pre = s.pre;
+        a.post = s.post;
+        a.tile_mask = c->plan.groups[s.group].tile;
+        a.proc_mask = c->plan.groups[s.group].proc;
+        a.total_bits = total_bits;
+        run(c, SV_K_WHT_TILE, [&] { launch_wht_tile_pass(c->dt, a, c->stream); });
+    }
+}
+
+MeanArgs mean_args(sv_ctx *c, bool with_oracle) {
+    MeanArgs m;
+    m.a = c->state;
+    m.N = c->nres;
+    m.inv_total = ldexp(1.0, -c->n);
+    m.marked = with_oracle ? c->d_marked : nullptr;
+    m.n_marked = with_oracle ? c->n_marked : 0;
+    m.partials = c->d_partials;
+    m.counter = c->d_counter;
+    return m;
+}
+
+void run_mean(sv_ctx *c, int k, bool with_oracle) {
+    if (c->plan.whole) {
+        if (with_oracle && k == 0) return;
+        run(c, SV_K_WHT_WHOLE, [&] {
+            launch_whole_state(c->dt, c->state, c->n, with_oracle ? k : 1, with_oracle ? 1 : 0, SV_DIFFUSE_MEAN,
+                               c->d_marked, c->n_marked, c->stream);
+        });
+        return;
+    }
+    const int reps = with_oracle ? k : 1;
+    if (reps == 0) return;
+    MeanArgs m = mean_args(c, with_oracle);
+    // first mu: sum of (O a) over the whole register (Eq. 3's accumulate)
+    m.sum_out = c->d_sums;
+    run(c, SV_K_REDUCE, [&] { launch_mean_grid(c->dt, m, c->mgrid, false, c->stream); });
+    allreduce_sum(c, c->d_sums, 2);  // ... and redistribute
+    for (int it = 0; it < reps; ++it) {
+        m.sum_in = c->d_sums + 2 * (it & 1);
+        m.sum_out = c->d_sums + 2 * ((it + 1) & 1);
+        run(c, SV_K_MEAN, [&] { launch_mean_grid(c->dt, m, c->mgrid, true, c->stream); });
+        if (it + 1 < reps) allreduce_sum(c, m.sum_out, 2);
+    }
+}
+
+void store_marked(sv_ctx *c, const uint64_t *marked, uint64_t m) {
+    const uint64_t N = 1ull << c->n;
+    SV_CHECK(m <= N, SV_EINVAL, "marked set larger than 2^n");
+    SV_CHECK(m == 0 || marked != nullptr, SV_EINVAL, "marked is NULL");
+    for (uint64_t j = 0; j < m; ++j) {
+        SV_CHECK(marked[j] < N, SV_EINVAL, "marked index " + std::to_string(marked[j]) + " >= 2^n");
+        SV_CHECK(j == 0 || marked[j] > marked[j - 1], SV_EINVAL,
+                 "marked indices must be strictly increasing (duplicates are errors)");
+    }
+    // resident part, rebased to local indices
+    uint64_t lo = 0, hi = m;
+    uint64_t base = 0;
+    if (!c->emulated && c->world > 1) {
+        base = (uint64_t)c->rank * c->nl_amps;
+        lo = std::lower_bound(marked, marked + m, base) - marked;
+        hi = std::lower_bound(marked, marked + m, base + c->nl_amps) - marked;
+    }
+    const uint64_t cnt = hi - lo;
+    std::vector<uint64_t> loc(cnt);
+    for (uint64_t j = 0; j < cnt; ++j) loc[j] = marked[lo + j] - base;
+    if (cnt > c->marked_cap) {
+        if (c->d_marked) SV_CUDA(cudaFree(c->d_marked));
+        c->d_marked = nullptr;
+        c->marked_cap = 0;
+        dmalloc((void **)&c->d_marked, std::max<uint64_t>(cnt, 1) * 8, "marked");
+        c->marked_cap = cnt;
+    }
+    if (cnt) SV_CUDA(cudaMemcpyAsync(c->d_marked, loc.data(), cnt * 8, cudaMemcpyHostToDevice, c->stream));
+    SV_CUDA(cudaStreamSynchronize(c->stream));  // loc is freed on return
+    c->n_marked = cnt;
+    c->has_marked = true;
+}
+
+void check_ctx(const sv_ctx *c) { SV_CHECK(c != nullptr, SV_EINVAL, "ctx is NULL"); }
+
+void destroy(sv_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (auto &p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+    for (auto &p : c->pool) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+    if (c->comm) ncclCommDestroy(c->comm);
+    cudaFree(c->state);
+    cudaFree(c->recv);
+    cudaFree(c->d_marked);
+    cudaFree(c->d_partials);
+    cudaFree(c->d_sums);
+    cudaFree(c->d_counter);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *sv_last_error(void) { return g_err.c_str(); }
+
+sv_status sv_init(sv_ctx **out, int n, uint64_t seed, sv_dtype dtype, sv_init_kind init, const sv_dist *dist) {
+    sv_ctx *c = nullptr;
+    sv_status st = guarded([&] {
+        SV_CHECK(out != nullptr, SV_EINVAL, "out is NULL");
+        *out = nullptr;
+        int world = dist ? dist->world : 1;
+        SV_CHECK(world >= 1 && (world & (world - 1)) == 0, SV_EINVAL, "world must be a power of two");
+        int g = 0;
+        while ((1 << g) < world) ++g;
+        SV_CHECK(g <= n, SV_EINVAL, "world larger than 2^n");
+        c = new sv_ctx();
+        c->n = n;
+        c->g = g;
+        c->world = world;
+        c->dt = dtype;
+        c->plan = make_plan(n, g, dtype);  // validates n, dtype, shard size
+        c->emulated = dist && world > 1 && dist->nccl_id == nullptr;
+        c->rank = (dist && !c->emulated) ? dist->rank : 0;
+        SV_CHECK(c->rank >= 0 && c->rank < world, SV_EINVAL, "rank out of range");
+        c->device = dist ? dist->device : 0;
+        if (!dist) SV_CUDA(cudaGetDevice(&c->device));
+        SV_CUDA(cudaSetDevice(c->device));
+        if (dist && dist->stream) {
+            c->stream = (cudaStream_t)dist->stream;
+        } else {
+            SV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+            c->own_stream = true;
+        }
+        c->nl_amps = 1ull << (n - g);
+        c->nres = c->emulated ? (1ull << n) : c->nl_amps;
+        const size_t bytes = c->nres * elem_bytes(dtype);
+        dmalloc(&c->state, bytes, "state");
+        if (g > 0) dmalloc(&c->recv, bytes, "swap receive buffer");
+        dmalloc((void **)&c->d_partials, 2 * kMaxGrid * sizeof(double), "partials");
+        dmalloc((void **)&c->d_sums, 8 * sizeof(double), "sums");
+        dmalloc((void **)&c->d_counter, sizeof(unsigned int), "counter");
+        SV_CUDA(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned int), c->stream));
+        SV_CUDA(cudaMemsetAsync(c->d_sums, 0, 8 * sizeof(double), c->stream));
+        c->mgrid = std::min(mean_grid(c->nres, dtype), kMaxGrid);
+        if (dist && world > 1 && !c->emulated) {
+            ncclUniqueId id;
+            memcpy(&id, dist->nccl_id, sizeof(id));
+            SV_NCCL(ncclCommInitRank(&c->comm, world, id, c->rank));
+        }
+        do_init(c, seed, init);
+        *out = c;
+    });
+    if (st != SV_OK) {
+        std::string msg = g_err;
+        destroy(c);
+        g_err = msg;
+    }
+    return st;
+}
+
+sv_status sv_reset(sv_ctx *c, uint64_t seed, sv_init_kind init) {
+    return guarded([&] {
+        check_ctx(c);
+        do_init(c, seed, init);
+    });
+}
+
+sv_status sv_set_marked(sv_ctx *c, const uint64_t *marked, uint64_t m) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CUDA(cudaSetDevice(c->device));
+        store_marked(c, marked, m);
+    });
+}
+
+sv_status sv_apply_oracle(sv_ctx *c, const uint64_t *marked, uint64_t m) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CUDA(cudaSetDevice(c->device));
+        store_marked(c, marked, m);
+        run(c, SV_K_ORACLE, [&] { launch_oracle_scatter(c->dt, c->state, c->d_marked, c->n_marked, c->stream); });
+    });
+}
+
+sv_status sv_diffuse(sv_ctx *c, sv_diffusion d) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CUDA(cudaSetDevice(c->device));
+        if (d == SV_DIFFUSE_WHT) run_wht_schedule(c, 1, false);
+        else if (d == SV_DIFFUSE_MEAN) run_mean(c, 1, false);
+        else throw Error{SV_EINVAL, "unknown diffusion"};
+    });
+}
+
+sv_status sv_iterate(sv_ctx *c, int k, sv_diffusion d) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CHECK(k >= 0, SV_EINVAL, "k must be >= 0");
+        SV_CHECK(c->has_marked, SV_ESTATE, "sv_iterate before any marked set (sv_set_marked / sv_apply_oracle)");
+        SV_CUDA(cudaSetDevice(c->device));
+        if (d == SV_DIFFUSE_WHT) run_wht_schedule(c, k, true);
+        else if (d == SV_DIFFUSE_MEAN) run_mean(c, k, true);
+        else throw Error{SV_EINVAL, "unknown diffusion"};
+    });
+}
+
+sv_status sv_probabilities(sv_ctx *c, double *out, uint64_t len, int on_device) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CHECK(out != nullptr, SV_EINVAL, "out is NULL");
+        SV_CHECK(len == c->nres, SV_EINVAL, "len must equal the resident length");
+        SV_CUDA(cudaSetDevice(c->device));
+        if (on_device) {
+            run(c, SV_K_READOUT, [&] { launch_probabilities(c->dt, c->state, out, c->nres, c->stream); });
+            return;
+        }
+        SV_CHECK(c->nres <= (1ull << 26), SV_ETOOBIG, "host gather above 2^26 entries");
+        double *tmp = nullptr;
+        dmalloc((void **)&tmp, c->nres * sizeof(double), "probabilities");
+        try {
+            run(c, SV_K_READOUT, [&] { launch_probabilities(c->dt, c->state, tmp, c->nres, c->stream); });
+            SV_CUDA(cudaMemcpyAsync(out, tmp, c->nres * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            SV_CUDA(cudaStreamSynchronize(c->stream));
+        } catch (...) {
+            cudaFree(tmp);
+            throw;
+        }
+        SV_CUDA(cudaFree(tmp));
+    });
+}
+
+sv_status sv_measure_marked_mass(sv_ctx *c, double *out) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CHECK(out != nullptr, SV_EINVAL, "out is NULL");
+        SV_CHECK(c->has_marked, SV_ESTATE, "no marked set");
+        SV_CUDA(cudaSetDevice(c->device));
+        double *d = c->d_sums + 6;
+        run(c, SV_K_READOUT, [&] { launch_marked_mass(c->dt, c->state, c->d_marked, c->n_marked, d, c->stream); });
+        allreduce_sum(c, d, 1);
+        SV_CUDA(cudaMemcpyAsync(out, d, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        SV_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+sv_status sv_get_amplitudes(sv_ctx *c, void *host_out, uint64_t offset, uint64_t count) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CHECK(host_out != nullptr || count == 0, SV_EINVAL, "host_out is NULL");
+        SV_CHECK(offset <= c->nres && count <= c->nres - offset, SV_EINVAL, "range outside the resident state");
+        SV_CUDA(cudaSetDevice(c->device));
+        const size_t eb = elem_bytes(c->dt);
+        SV_CUDA(cudaMemcpyAsync(host_out, (char *)c->state + offset * eb, count * eb, cudaMemcpyDeviceToHost, c->stream));
+        SV_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+sv_status sv_set_amplitudes(sv_ctx *c, const void *host_in, uint64_t offset, uint64_t count) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CHECK(host_in != nullptr || count == 0, SV_EINVAL, "host_in is NULL");
+        SV_CHECK(offset <= c->nres && count <= c->nres - offset, SV_EINVAL, "range outside the resident state");
+        SV_CUDA(cudaSetDevice(c->device));
+        const size_t eb = elem_bytes(c->dt);
+        SV_CUDA(cudaMemcpyAsync((char *)c->state + offset * eb, host_in, count * eb, cudaMemcpyHostToDevice, c->stream));
+        SV_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+sv_status sv_marked_from_seed(int n, uint64_t m, uint64_t seed, uint64_t *out) {
+    return guarded([&] {
+        SV_CHECK(n >= 1 && n <= 40, SV_EINVAL, "n must be in [1, 40]");
+        SV_CHECK(m <= (1ull << n), SV_EINVAL, "m > 2^n");
+        SV_CHECK(out != nullptr || m == 0, SV_EINVAL, "out is NULL");
+        for (uint64_t j = 0; j < m; ++j) out[j] = perm_seeded(n, seed, j);
+        std::sort(out, out + m);
+    });
+}
+
+sv_status sv_info(const sv_ctx *c, int *n, int *world, int *rank, uint64_t *local_len, sv_dtype *dtype) {
+    return guarded([&] {
+        check_ctx(c);
+        if (n) *n = c->n;
+        if (world) *world = c->world;
+        if (rank) *rank = c->rank;
+        if (local_len) *local_len = c->nres;
+        if (dtype) *dtype = c->dt;
+    });
+}
+
+sv_status sv_synchronize(sv_ctx *c) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CUDA(cudaSetDevice(c->device));
+        SV_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+sv_status sv_nccl_unique_id(void *out, size_t len) {
+    return guarded([&] {
+        SV_CHECK(out != nullptr && len >= sizeof(ncclUniqueId), SV_EINVAL, "need a 128-byte buffer");
+        ncclUniqueId id;
+        SV_NCCL(ncclGetUniqueId(&id));
+        memcpy(out, &id, sizeof(id));
+    });
+}
+
+sv_status sv_plan_wht(int n, int world, sv_dtype dtype, int k, int with_oracle, sv_plan_step *out, int cap,
+                      int *nsteps) {
+    return guarded([&] {
+        SV_CHECK(world >= 1 && (world & (world - 1)) == 0, SV_EINVAL, "world must be a power of two");
+        SV_CHECK(k >= 0, SV_EINVAL, "k must be >= 0");
+        int g = 0;
+        while ((1 << g) < world) ++g;
+        SV_CHECK(g <= n, SV_EINVAL, "world larger than 2^n");
+        Plan p = make_plan(n, g, dtype);
+        std::vector<Step> steps = schedule_wht(p, k, with_oracle != 0);
+        if (nsteps) *nsteps = (int)steps.size();
+        for (int i = 0; i < (int)steps.size() && i < cap && out; ++i) {
+            const Step &s = steps[i];
+            sv_plan_step &o = out[i];
+            o.kind = s.kind;
+            o.pre = s.pre;
+            o.mid = s.mid;
+            o.post = s.post;
+            o.in_recv = s.in_recv;
+            o.tile_bits = p.whole ? p.nl : p.T;
+            o.tile_mask = (s.group >= 0) ? p.groups[s.group].tile : 0;
+            o.proc_mask = (s.group >= 0) ? p.groups[s.group].proc : 0;
+        }
+    });
+}
+
+sv_status sv_profile(sv_ctx *c, int enable) {
+    return guarded([&] {
+        check_ctx(c);
+        drain_profile(c);
+        c->prof = enable != 0;
+        for (int i = 0; i < SV_K_COUNT; ++i) {
+            c->launches[i] = 0;
+            c->ms[i] = 0.0;
+        }
+    });
+}
+
+sv_status sv_profile_read(sv_ctx *c, int kind, uint64_t *launches, double *total_ms) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CHECK(kind >= 0 && kind < SV_K_COUNT, SV_EINVAL, "kind out of range");
+        drain_profile(c);
+        if (launches) *launches = c->launches[kind];
+        if (total_ms) *total_ms = c->ms[kind];
+    });
+}
+
+void sv_free(sv_ctx *c) { destroy(c); }
+
+}  // extern "C"

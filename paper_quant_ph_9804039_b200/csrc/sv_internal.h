@@ -1,0 +1,152 @@
+// sv_internal.h -- internal declarations of libsv.so (not part of the ABI).
+// Citations: P:NNNN = line of the paper text, S:NNN = SPEC line, G<k> = a
+// reading in DESIGN.md.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sv.h"
+
+namespace sv {
+
+// ------------------------------------------------------------------------- //
+// Error plumbing                                                             //
+// ------------------------------------------------------------------------- //
+void set_error(const std::string &msg);
+
+struct Error {
+    sv_status code;
+    std::string msg;
+};
+
+#define SV_CUDA(call)                                                                     \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            throw ::sv::Error{SV_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+    } while (0)
+
+#define SV_NCCL(call)                                                                     \
+    do {                                                                                  \
+        ncclResult_t r_ = (call);                                                         \
+        if (r_ != ncclSuccess)                                                            \
+            throw ::sv::Error{SV_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)}; \
+    } while (0)
+
+#define SV_CHECK(cond, code, msg)                                   \
+    do {                                                            \
+        if (!(cond)) throw ::sv::Error{(code), std::string(msg)};   \
+    } while (0)
+
+// ------------------------------------------------------------------------- //
+// Tile geometry per dtype                       //
+// ------------------------------------------------------------------------- //
+constexpr int kTileBitsC64 = 13;   // 2^13 x 8 B  = 64 KiB smem tile
+constexpr int kRegBitsC64 = 5;     // 32 amplitudes per thread, 256 threads
+constexpr int kTileBitsC128 = 12;  // 2^12 x 16 B = 64 KiB smem tile
+constexpr int kRegBitsC128 = 4;    // 16 amplitudes per thread, 256 threads
+// minimum unprocessed low slots kept in a strided tile: 2^c amplitudes = 64 B
+// contiguous runs (c64: 8 x 8 B, c128: 4 x 16 B)
+constexpr int kCarryC64 = 3;
+constexpr int kCarryC128 = 2;
+
+inline int tile_bits(sv_dtype d) { return d == SV_C64 ? kTileBitsC64 : kTileBitsC128; }
+inline int carry_bits(sv_dtype d) { return d == SV_C64 ? kCarryC64 : kCarryC128; }
+inline size_t elem_bytes(sv_dtype d) { return d == SV_C64 ? 8 : 16; }
+
+// ------------------------------------------------------------------------- //
+// Schedule (plan.cpp)                                                        //
+// ------------------------------------------------------------------------- //
+enum StepKind { STEP_PASS = 0, STEP_SWAP = 1, STEP_WHOLE = 2, STEP_SCATTER = 3 };
+enum MidOp { MID_NONE = 0, MID_ORACLE = 1, MID_F0 = 2 };
+
+struct Group {
+    uint64_t proc = 0;   // slots whose butterfly stages run in this pass
+    uint64_t tile = 0;   // slots spanned by one tile (popcount == T), proc subset
+};
+
+struct Step {
+    int kind = STEP_PASS;
+    int group = -1;
+    int pre = 0, mid = MID_NONE, post = 0;
+    int in_recv = 0;
+};
+
+struct Plan {
+    int nl = 0;       // local index bits (n - g)
+    int g = 0;        // rank bits
+    int T = 0;        // tile bits
+    bool whole = false;
+    std::vector<Group> groups;   // groups[0] = contiguous slots [0, T)
+    std::vector<int> fwd;        // first transform: group indices, -1 = swap
+};
+
+// Validates (n, g, dtype) and builds the group structure.  Throws Error.
+Plan make_plan(int n, int g, sv_dtype dtype);
+// Expand an op sequence to fused device steps.
+//   with_oracle: iterations (O, WHT, F0, WHT) x k; else one (WHT, F0, WHT).
+std::vector<Step> schedule_wht(const Plan &plan, int k, bool with_oracle);
+
+// ------------------------------------------------------------------------- //
+// Kernel launchers (wht.cu, mean.cu, misc.cu)                                //
+// ------------------------------------------------------------------------- //
+struct PassArgs {
+    void *in = nullptr;
+    void *out = nullptr;
+    const uint64_t *marked = nullptr;   // sorted local indices (device)
+    uint64_t n_marked = 0;
+    double f0_scale = 0.0;              // 2^-n
+    int mid = MID_NONE;
+    int has_origin = 0;                 // global index 0 resident at local 0
+    int pre = 0, post = 0;
+    uint64_t tile_mask = 0;             // slots of one tile
+    uint64_t proc_mask = 0;             // processed slots (subset of tile_mask)
+    int total_bits = 0;                 // index bits of the launched buffer
+};
+
+void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s);
+void launch_whole_state(sv_dtype dt, void *state, int n, int k, int with_oracle, int diffusion,
+                        const uint64_t *marked, uint64_t m, cudaStream_t s);
+
+struct MeanArgs {
+    void *a = nullptr;
+    uint64_t N = 0;                    // resident amplitudes
+    double inv_total = 0.0;            // 1 / 2^n (global N)
+    const uint64_t *marked = nullptr;  // sorted local indices
+    uint64_t n_marked = 0;
+    const double *sum_in = nullptr;    // complex sum of (O a) over all ranks
+    double *sum_out = nullptr;         // local complex sum of (O a_new)
+    double *partials = nullptr;        // 2 * grid doubles
+    unsigned int *counter = nullptr;   // zero-initialised ticket
+};
+// One wave of blocks (SM count x resident blocks), capped by the work.
+int mean_grid(uint64_t N, sv_dtype dt);
+// write = true: fused flip + invert-about-mean + next-sum; false: read-only
+// sum of (O a) (the first mu of an sv_iterate call).
+void launch_mean_grid(sv_dtype dt, const MeanArgs &a, int grid, bool write, cudaStream_t s);
+
+void launch_init_uniform(sv_dtype dt, void *a, uint64_t N, int n, cudaStream_t s);
+void launch_init_zero(sv_dtype dt, void *a, uint64_t N, int has_origin, cudaStream_t s);
+// Gaussian (G8): pass 1 writes the local sum |z|^2 into *norm_out (fp64),
+// pass 2 regenerates and scales by 1/sqrt(*norm_in).
+void launch_gauss_norm(uint64_t key, uint64_t global_offset, uint64_t N, double *partials,
+                       unsigned int *counter, double *norm_out, cudaStream_t s);
+void launch_gauss_write(sv_dtype dt, void *a, uint64_t key, uint64_t global_offset, uint64_t N,
+                        const double *norm_in, cudaStream_t s);
+void launch_oracle_scatter(sv_dtype dt, void *a, const uint64_t *marked, uint64_t m, cudaStream_t s);
+void launch_probabilities(sv_dtype dt, const void *a, double *p, uint64_t N, cudaStream_t s);
+void launch_marked_mass(sv_dtype dt, const void *a, const uint64_t *marked, uint64_t m, double *out,
+                        cudaStream_t s);
+
+// Seeded generators (host side of the library; G6, G8).
+uint64_t splitmix64_next(uint64_t &state);
+uint64_t hash64(uint64_t x);
+uint64_t gauss_key(uint64_t seed);
+uint64_t perm_seeded(int n, uint64_t seed, uint64_t x);
+
+}  // namespace sv

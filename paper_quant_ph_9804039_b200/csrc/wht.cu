@@ -1,0 +1,498 @@
+// wht.cu -- fused multi-stage Walsh-Hadamard tile pass (sm_100a).
+//
+// What it computes: for one group of qubits (slots), every butterfly stage
+//   (x, y) -> (x + y, x - y)  on index pairs that differ only in that bit,
+// i.e. Fig. 3's 2x2 transformation with w = x = y = 1, z = -1,
+// applied as "a sequence of V/2 independent 2x2 transformations" per qubit
+// (section 2.1).  Optionally an elementwise op between two
+// stage sets of the same group: the phase oracle O (negate marked entries,
+// G3) or F0 = 2|0><0| - I with the exact 2^{-n} scale (G2, G5).
+//
+// How (B200 design):
+//  * A tile is 2^T amplitudes whose local indices differ only in T slots
+//    (the group's processed slots + the lowest unprocessed slots, so every
+//    tile row is a >= 64 B contiguous run).  One CTA = one tile; 256 threads
+//    hold 2^R amplitudes each in registers.
+//  * The T tile bits are covered by three register layouts A, B, C; each runs
+//    its R butterfly stages in registers.  Layout changes go through one
+//    swizzled shared-memory tile (one __syncthreads each: every thread writes
+//    exactly the slots it read in the previous layout).
+//  * Layout A owns tile bit 0 and the top tile bits, so HBM is touched with
+//    coalesced 128-bit loads (512 contiguous bytes per warp instruction on a
+//    contiguous tile).  No tensor cores: the path is add/sub only (<= 1.75
+//    FLOP/B), memory-bound.
+#include <cuda_runtime.h>
+
+#include "sv_internal.h"
+
+namespace sv {
+
+template <typename E> struct RealOf;
+template <> struct RealOf<float2> { using T = float; };
+template <> struct RealOf<double2> { using T = double; };
+
+// ------------------------------------------------------------------------- //
+// Register / shared-memory layouts of a 2^TB tile with 2^RB amps per thread  //
+// ------------------------------------------------------------------------- //
+template <typename E, int TB, int RB>
+struct Layout {
+    static constexpr int VE = (sizeof(E) == 8) ? 2 : 1;   // amplitudes per 16 B
+    static constexpr int NT = 1 << (TB - RB);             // threads
+    static constexpr int NR = 1 << RB;                    // amplitudes per thread
+    static constexpr int kTB = TB, kRB = RB;
+    static_assert(TB >= 2 * RB && TB <= 3 * RB, "three layouts must cover the tile");
+    static_assert(TB - RB >= 5, "need at least one warp");
+
+    // i-th register bit (ascending) of layout ph (0 = A, 1 = B, 2 = C).
+    __host__ __device__ static constexpr int reg_bit(int ph, int i) {
+        return VE == 2 ? (ph == 0 ? (i == 0 ? 0 : TB - RB + i) : ph == 1 ? 1 + i : TB - 2 * RB + 1 + i)
+                       : (ph == 0 ? TB - RB + i : ph == 1 ? i : TB - 2 * RB + i);
+    }
+    __host__ __device__ static constexpr bool is_reg(int ph, int b) {
+        bool r = false;
+        for (int i = 0; i < RB; ++i) r = r || (reg_bit(ph, i) == b);
+        return r;
+    }
+    // i-th thread bit (ascending) of layout ph: the tile bits that are not
+    // register bits.  Lane = thread bits 0..4.
+    __host__ __device__ static constexpr int thr_bit(int ph, int i) {
+        int c = 0;
+        for (int b = 0; b < TB; ++b)
+            if (!is_reg(ph, b)) {
+                if (c == i) return b;
+                ++c;
+            }
+        return -1;
+    }
+    // Each tile bit's stage runs in exactly one layout: A and B are disjoint;
+    // C runs only the bits B does not have.
+    __host__ __device__ static constexpr bool owns(int ph, int b) {
+        return ph == 0 ? is_reg(0, b) : ph == 1 ? is_reg(1, b) : (is_reg(2, b) && !is_reg(1, b) && !is_reg(0, b));
+    }
+    // XOR swizzle of the shared-memory index (linear over GF(2)): makes the
+    // 8-lane (16 B) / 16-lane (8 B) wavefronts of every layout bank-conflict
+    // free -- checked exhaustively by tests/test_layouts.py via sv_debug.
+    __host__ __device__ static constexpr uint32_t swz(uint32_t e) {
+        return VE == 2 ? (e ^ (((e >> (RB + 1)) & 7u) << 1)) : (e ^ ((e >> RB) & 7u));
+    }
+    __host__ __device__ static constexpr uint32_t ereg(int ph, int j) {
+        uint32_t e = 0;
+        for (int i = 0; i < RB; ++i)
+            if ((j >> i) & 1) e |= 1u << reg_bit(ph, i);
+        return e;
+    }
+    __host__ __device__ static constexpr uint32_t ethr(int ph, uint32_t t) {
+        uint32_t e = 0;
+        for (int i = 0; i < TB - RB; ++i)
+            if ((t >> i) & 1) e |= 1u << thr_bit(ph, i);
+        return e;
+    }
+};
+
+struct KParams {
+    const void *in;
+    void *out;
+    const unsigned long long *marked;
+    unsigned long long n_marked;
+    double f0_scale;
+    int mid;
+    int has_origin;
+    unsigned int proc;       // processed tile bits
+    unsigned long long free_mask;  // slots not in the tile; tile id bits scatter into them
+    signed char slot[16];          // tile bit -> slot
+};
+
+template <typename E>
+__device__ __forceinline__ void bfly(E &x, E &y) {
+    E t = x;
+    x.x = t.x + y.x;
+    x.y = t.y + y.y;
+    y.x = t.x - y.x;
+    y.y = t.y - y.y;
+}
+
+template <class L, int PH, typename E>
+__device__ __forceinline__ void run_stages(E (&x)[L::NR], unsigned int proc) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        if (i < L::kRB) {
+            const int b = L::reg_bit(PH, i);
+            if (L::owns(PH, b) && ((proc >> b) & 1u)) {
+#pragma unroll
+                for (int j = 0; j < L::NR; ++j)
+                    if (!(j & (1 << i))) bfly(x[j], x[j | (1 << i)]);
+            }
+        }
+    }
+}
+
+// Shared-memory layout change PW -> PR.  One barrier: each thread writes the
+// positions it read in the previous change (or, for the first write, nobody
+// has read yet), so no write can race a pending read.
+template <class L, int PW, int PR, typename E>
+__device__ __forceinline__ void relayout(E (&x)[L::NR], E *sm, int tid) {
+    const uint32_t sw = L::swz(L::ethr(PW, tid));
+    const uint32_t sr = L::swz(L::ethr(PR, tid));
+    if constexpr (L::VE == 2 && PW == 0) {
+#pragma unroll
+        for (int v = 0; v < L::NR / 2; ++v) {
+            float4 q;
+            q.x = x[2 * v].x; q.y = x[2 * v].y; q.z = x[2 * v + 1].x; q.w = x[2 * v + 1].y;
+            *reinterpret_cast<float4 *>(&sm[sw ^ L::swz(L::ereg(PW, 2 * v))]) = q;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < L::NR; ++j) sm[sw ^ L::swz(L::ereg(PW, j))] = x[j];
+    }
+    __syncthreads();
+    if constexpr (L::VE == 2 && PR == 0) {
+#pragma unroll
+        for (int v = 0; v < L::NR / 2; ++v) {
+            float4 q = *reinterpret_cast<const float4 *>(&sm[sr ^ L::swz(L::ereg(PR, 2 * v))]);
+            x[2 * v].x = q.x; x[2 * v].y = q.y; x[2 * v + 1].x = q.z; x[2 * v + 1].y = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < L::NR; ++j) x[j] = sm[sr ^ L::swz(L::ereg(PR, j))];
+    }
+}
+
+// Global offset (elements) of tile element e under the pass's slot map.
+template <class L, int PH>
+__device__ __forceinline__ unsigned long long goff_thr(const KParams &p, int tid) {
+    unsigned long long o = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+        if (i < (L::kTB - L::kRB))
+            if ((tid >> i) & 1) o += 1ull << p.slot[L::thr_bit(PH, i)];
+    return o;
+}
+
+template <class L, int PH, typename E>
+__device__ __forceinline__ void global_load(E (&x)[L::NR], const E *g, const KParams &p, int tid) {
+    const unsigned long long t = goff_thr<L, PH>(p, tid);
+    unsigned long long st[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+        if (i < L::kRB) st[i] = 1ull << p.slot[L::reg_bit(PH, i)];
+    if constexpr (L::VE == 2 && PH == 0) {
+#pragma unroll
+        for (int v = 0; v < L::NR / 2; ++v) {
+            unsigned long long o = t;
+#pragma unroll
+            for (int i = 1; i < 16; ++i)
+                if (i < L::kRB && (((2 * v) >> i) & 1)) o += st[i];
+            float4 q = *reinterpret_cast<const float4 *>(g + o);
+            x[2 * v].x = q.x; x[2 * v].y = q.y; x[2 * v + 1].x = q.z; x[2 * v + 1].y = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < L::NR; ++j) {
+            unsigned long long o = t;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                if (i < L::kRB && ((j >> i) & 1)) o += st[i];
+            x[j] = g[o];
+        }
+    }
+}
+
+template <class L, int PH, typename E>
+__device__ __forceinline__ void global_store(const E (&x)[L::NR], E *g, const KParams &p, int tid) {
+    const unsigned long long t = goff_thr<L, PH>(p, tid);
+    unsigned long long st[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+        if (i < L::kRB) st[i] = 1ull << p.slot[L::reg_bit(PH, i)];
+    if constexpr (L::VE == 2 && PH == 0) {
+#pragma unroll
+        for (int v = 0; v < L::NR / 2; ++v) {
+            unsigned long long o = t;
+#pragma unroll
+            for (int i = 1; i < 16; ++i)
+                if (i < L::kRB && (((2 * v) >> i) & 1)) o += st[i];
+            float4 q;
+            q.x = x[2 * v].x; q.y = x[2 * v].y; q.z = x[2 * v + 1].x; q.w = x[2 * v + 1].y;
+            *reinterpret_cast<float4 *>(g + o) = q;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < L::NR; ++j) {
+            unsigned long long o = t;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                if (i < L::kRB && ((j >> i) & 1)) o += st[i];
+            g[o] = x[j];
+        }
+    }
+}
+
+// Elementwise op between the two stage sets, in register layout PH.
+template <class L, int PH, typename E>
+__device__ __forceinline__ void mid_op(E (&x)[L::NR], const KParams &p, unsigned long long base, int tid,
+                                       unsigned long long mlo, unsigned long long mcnt) {
+    using R = typename RealOf<E>::T;
+    if (p.mid == MID_F0) {
+        // F0 = 2|0><0| - I with the 2^{-n} scale of the two unnormalised
+        // transforms (G2, G5): -2^{-n} x everywhere, +2^{-n} x at index 0.
+        const R s = (R)(-p.f0_scale);
+#pragma unroll
+        for (int j = 0; j < L::NR; ++j) { x[j].x *= s; x[j].y *= s; }
+        if (p.has_origin && base == 0 && tid == 0) { x[0].x = -x[0].x; x[0].y = -x[0].y; }
+    } else if (p.mid == MID_ORACLE) {
+        // O: negate marked amplitudes (G3).  The tile is contiguous (slots
+        // 0..TB-1), so tile element e = m - base.
+        for (unsigned long long r = 0; r < mcnt; ++r) {
+            const uint32_t e = (uint32_t)(p.marked[mlo + r] - base);
+            uint32_t t = 0, jj = 0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                if (i < (L::kTB - L::kRB)) t |= ((e >> L::thr_bit(PH, i)) & 1u) << i;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                if (i < L::kRB) jj |= ((e >> L::reg_bit(PH, i)) & 1u) << i;
+            if ((int)t == tid) {
+#pragma unroll
+                for (int j = 0; j < L::NR; ++j)
+                    if ((uint32_t)j == jj) { x[j].x = -x[j].x; x[j].y = -x[j].y; }
+            }
+        }
+    }
+}
+
+template <typename E, int TB, int RB, bool PRE, bool POST>
+__global__ void __launch_bounds__(1 << (TB - RB), 2) wht_tile_kernel(const KParams p) {
+    using L = Layout<E, TB, RB>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    E *sm = reinterpret_cast<E *>(smem_raw);
+    __shared__ unsigned long long s_mlo, s_mcnt;
+    const int tid = threadIdx.x;
+
+    // tile base: scatter the tile id into the free slots (software pdep)
+    unsigned long long tile = blockIdx.x, base = 0, fm = p.free_mask;
+    while (fm) {
+        const unsigned long long low = fm & (~fm + 1ull);
+        if (tile & 1ull) base |= low;
+        tile >>= 1;
+        fm ^= low;
+    }
+
+    if (p.mid == MID_ORACLE && tid == 0) {
+        // marked entries inside [base, base + 2^TB): lower_bound twice
+        unsigned long long lo = 0, hi = p.n_marked;
+        while (lo < hi) {
+            unsigned long long md = (lo + hi) >> 1;
+            if (p.marked[md] < base) lo = md + 1; else hi = md;
+        }
+        unsigned long long a = lo;
+        hi = p.n_marked;
+        const unsigned long long end = base + (1ull << TB);
+        while (lo < hi) {
+            unsigned long long md = (lo + hi) >> 1;
+            if (p.marked[md] < end) lo = md + 1; else hi = md;
+        }
+        s_mlo = a;
+        s_mcnt = lo - a;
+    }
+
+    E x[L::NR];
+    global_load<L, 0>(x, reinterpret_cast<const E *>(p.in) + base, p, tid);
+    E *gout = reinterpret_cast<E *>(p.out) + base;
+
+    if (PRE) {
+        run_stages<L, 0>(x, p.proc);
+        relayout<L, 0, 1>(x, sm, tid);
+        run_stages<L, 1>(x, p.proc);
+        relayout<L, 1, 2>(x, sm, tid);
+        run_stages<L, 2>(x, p.proc);
+        if (p.mid != MID_NONE) mid_op<L, 2>(x, p, base, tid, s_mlo, s_mcnt);
+        if (POST) {
+            run_stages<L, 2>(x, p.proc);
+            relayout<L, 2, 1>(x, sm, tid);
+            run_stages<L, 1>(x, p.proc);
+            relayout<L, 1, 0>(x, sm, tid);
+            run_stages<L, 0>(x, p.proc);
+            global_store<L, 0>(x, gout, p, tid);
+        } else {
+            global_store<L, 2>(x, gout, p, tid);
+        }
+    } else {
+        if (p.mid == MID_ORACLE) __syncthreads();  // s_mlo / s_mcnt
+        if (p.mid != MID_NONE) mid_op<L, 0>(x, p, base, tid, s_mlo, s_mcnt);
+        if (POST) {
+            run_stages<L, 0>(x, p.proc);
+            relayout<L, 0, 1>(x, sm, tid);
+            run_stages<L, 1>(x, p.proc);
+            relayout<L, 1, 2>(x, sm, tid);
+            run_stages<L, 2>(x, p.proc);
+            global_store<L, 2>(x, gout, p, tid);
+        } else {
+            global_store<L, 0>(x, gout, p, tid);
+        }
+    }
+}
+
+template <typename E, int TB, int RB, bool PRE, bool POST>
+static void launch_tile_t(const KParams &kp, unsigned long long ntiles, cudaStream_t s) {
+    using L = Layout<E, TB, RB>;
+    auto fn = wht_tile_kernel<E, TB, RB, PRE, POST>;
+    const int smem = (1 << TB) * (int)sizeof(E);
+    static bool attr = false;
+    if (!attr) {
+        SV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+    }
+    SV_CHECK(ntiles <= 0x7fffffffull, SV_EINVAL, "too many tiles for one launch");
+    fn<<<(unsigned int)ntiles, L::NT, smem, s>>>(kp);
+    SV_CUDA(cudaGetLastError());
+}
+
+template <typename E, int TB, int RB>
+static void launch_tile_cfg(const KParams &kp, int pre, int post, unsigned long long ntiles, cudaStream_t s) {
+    if (pre && post) launch_tile_t<E, TB, RB, true, true>(kp, ntiles, s);
+    else if (pre) launch_tile_t<E, TB, RB, true, false>(kp, ntiles, s);
+    else if (post) launch_tile_t<E, TB, RB, false, true>(kp, ntiles, s);
+    else SV_CHECK(false, SV_EINVAL, "internal: tile pass without stages");
+}
+
+void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
+    const int TB = tile_bits(dt);
+    KParams kp{};
+    kp.in = a.in;
+    kp.out = a.out;
+    kp.marked = reinterpret_cast<const unsigned long long *>(a.marked);
+    kp.n_marked = a.n_marked;
+    kp.f0_scale = a.f0_scale;
+    kp.mid = a.mid;
+    kp.has_origin = a.has_origin;
+    int b = 0, f = 0;
+    unsigned int proc = 0;
+    kp.free_mask = 0;
+    for (int sl = 0; sl < a.total_bits; ++sl) {
+        if ((a.tile_mask >> sl) & 1) {
+            SV_CHECK(b < 16, SV_EINVAL, "internal: tile too large");
+            if ((a.proc_mask >> sl) & 1) proc |= 1u << b;
+            kp.slot[b++] = (signed char)sl;
+        } else {
+            kp.free_mask |= 1ull << sl;
+            ++f;
+        }
+    }
+    SV_CHECK(b == TB, SV_EINVAL, "internal: tile mask does not have T slots");
+    SV_CHECK(kp.slot[0] == 0, SV_EINVAL, "internal: tile must contain slot 0");
+    if (a.mid == MID_ORACLE)
+        for (int i = 0; i < TB; ++i) SV_CHECK(kp.slot[i] == i, SV_EINVAL, "internal: oracle needs a contiguous tile");
+    kp.proc = proc;
+    const unsigned long long ntiles = 1ull << f;
+    if (dt == SV_C64) launch_tile_cfg<float2, kTileBitsC64, kRegBitsC64>(kp, a.pre, a.post, ntiles, s);
+    else launch_tile_cfg<double2, kTileBitsC128, kRegBitsC128>(kp, a.pre, a.post, ntiles, s);
+}
+
+// ------------------------------------------------------------------------- //
+// Whole state in one CTA (n <= T): k iterations without leaving shared memory //
+// ------------------------------------------------------------------------- //
+template <typename E>
+__global__ void __launch_bounds__(512) whole_state_kernel(E *a, int n, int k, int with_oracle, int diffusion,
+                                                          const unsigned long long *marked,
+                                                          unsigned long long m, double f0_scale) {
+    using R = typename RealOf<E>::T;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    E *s = reinterpret_cast<E *>(smem_raw);
+    __shared__ double red[2 * 32];
+    const unsigned int N = 1u << n, tid = threadIdx.x, nt = blockDim.x;
+    for (unsigned int i = tid; i < N; i += nt) s[i] = a[i];
+    __syncthreads();
+    auto transform = [&]() {
+        for (int q = 0; q < n; ++q) {
+            const unsigned int bit = 1u << q;
+            for (unsigned int pr = tid; pr < N / 2; pr += nt) {
+                const unsigned int i = ((pr >> q) << (q + 1)) | (pr & (bit - 1));
+                bfly(s[i], s[i | bit]);
+            }
+            __syncthreads();
+        }
+    };
+    const int reps = k;
+    for (int it = 0; it < reps; ++it) {
+        if (with_oracle) {
+            for (unsigned long long j = tid; j < m; j += nt) {
+                E &v = s[marked[j]];
+                v.x = -v.x;
+                v.y = -v.y;
+            }
+            __syncthreads();
+        }
+        if (diffusion == SV_DIFFUSE_WHT) {
+            transform();
+            for (unsigned int i = tid; i < N; i += nt) {
+                const R sc = (R)(i == 0 ? f0_scale : -f0_scale);
+                s[i].x *= sc;
+                s[i].y *= sc;
+            }
+            __syncthreads();
+            transform();
+        } else {
+            // fixed-order block reduction in fp64 (deterministic)
+            double re = 0.0, im = 0.0;
+            for (unsigned int i = tid; i < N; i += nt) { re += (double)s[i].x; im += (double)s[i].y; }
+            for (int o = 16; o > 0; o >>= 1) {
+                re += __shfl_xor_sync(0xffffffffu, re, o);
+                im += __shfl_xor_sync(0xffffffffu, im, o);
+            }
+            if ((tid & 31) == 0) { red[2 * (tid >> 5)] = re; red[2 * (tid >> 5) + 1] = im; }
+            __syncthreads();
+            double mr = 0.0, mi = 0.0;
+            for (unsigned int w = 0; w < nt / 32; ++w) { mr += red[2 * w]; mi += red[2 * w + 1]; }
+            mr *= f0_scale;  // 1/N
+            mi *= f0_scale;
+            const R two_mr = (R)(2.0 * mr), two_mi = (R)(2.0 * mi);
+            for (unsigned int i = tid; i < N; i += nt) { s[i].x = two_mr - s[i].x; s[i].y = two_mi - s[i].y; }
+            __syncthreads();
+        }
+    }
+    for (unsigned int i = tid; i < N; i += nt) a[i] = s[i];
+}
+
+void launch_whole_state(sv_dtype dt, void *state, int n, int k, int with_oracle, int diffusion,
+                        const uint64_t *marked, uint64_t m, cudaStream_t s) {
+    const unsigned int N = 1u << n;
+    const int threads = N >= 1024 ? 512 : (N / 2 >= 32 ? (int)(N / 2) : 32);
+    const double f0 = ldexp(1.0, -n);
+    const auto mk = reinterpret_cast<const unsigned long long *>(marked);
+    if (dt == SV_C64) {
+        const int smem = (int)(N * sizeof(float2));
+        SV_CUDA(cudaFuncSetAttribute(whole_state_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        whole_state_kernel<float2><<<1, threads, smem, s>>>((float2 *)state, n, k, with_oracle, diffusion, mk, m, f0);
+    } else {
+        const int smem = (int)(N * sizeof(double2));
+        SV_CUDA(cudaFuncSetAttribute(whole_state_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        whole_state_kernel<double2><<<1, threads, smem, s>>>((double2 *)state, n, k, with_oracle, diffusion, mk, m, f0);
+    }
+    SV_CUDA(cudaGetLastError());
+}
+
+// Host-side view of the tile layouts for tests/test_layouts.py (no device).
+extern "C" int sv_debug_tile_layout(int dtype, int phase, int tid, int reg, int *tile_elem, int *smem_index) {
+    if (phase < 0 || phase > 2) return -1;
+    if (dtype == SV_C64) {
+        using L = Layout<float2, kTileBitsC64, kRegBitsC64>;
+        if (tid < 0 || tid >= L::NT || reg < 0 || reg >= L::NR) return -1;
+        const uint32_t e = L::ethr(phase, tid) | L::ereg(phase, reg);
+        *tile_elem = (int)e;
+        *smem_index = (int)L::swz(e);
+        return 0;
+    }
+    using L = Layout<double2, kTileBitsC128, kRegBitsC128>;
+    if (tid < 0 || tid >= L::NT || reg < 0 || reg >= L::NR) return -1;
+    const uint32_t e = L::ethr(phase, tid) | L::ereg(phase, reg);
+    *tile_elem = (int)e;
+    *smem_index = (int)L::swz(e);
+    return 0;
+}
+
+extern "C" int sv_debug_tile_owner(int dtype, int phase, int bit) {
+    if (dtype == SV_C64) return Layout<float2, kTileBitsC64, kRegBitsC64>::owns(phase, bit) ? 1 : 0;
+    return Layout<double2, kTileBitsC128, kRegBitsC128>::owns(phase, bit) ? 1 : 0;
+}
+
+}  // namespace sv
