@@ -184,7 +184,9 @@ def run_ours(args):
     dtype = sv.SV_C64 if dts == "c64" else sv.SV_C128
     dflag = sv.SV_DIFFUSE_WHT if diff == "wht" else sv.SV_DIFFUSE_MEAN
     ikind = sv.SV_INIT_UNIFORM if init == "uniform" else sv.SV_INIT_GAUSSIAN
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream shared by libsv and the timing events
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx = svd.sharded_init(n, seed, dtype, ikind, stream=stream.cuda_stream)
     marked = sv.sv_marked_from_seed(n, M, seed)
     sv.sv_set_marked(ctx, marked)

@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libsv.so")
+# SV_LIB may point at an alternative build of the same library (A/B tuning).
+LIB_PATH = os.environ.get("SV_LIB") or os.path.join(_PKG, "libsv.so")
 
 SV_OK, SV_EINVAL, SV_ENOMEM, SV_ECUDA, SV_ENCCL, SV_ESTATE, SV_ETOOBIG = 0, -1, -2, -3, -4, -5, -6
 SV_C64, SV_C128 = 0, 1

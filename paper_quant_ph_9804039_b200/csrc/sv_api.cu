@@ -42,6 +42,7 @@ struct sv_ctx {
     uint64_t nl_amps = 0;    // amplitudes per rank (2^{n-g})
     uint64_t *d_marked = nullptr;
     uint64_t marked_cap = 0;
+    unsigned int *d_tilemap = nullptr;  // one bit per contiguous 2^T tile of the resident state
     uint64_t n_marked = 0;   // resident (local) marked entries
     bool has_marked = false;
     double *d_partials = nullptr;  // 2 * kMaxGrid
@@ -200,6 +201,7 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle) {
         a.out = c->state;
         a.marked = c->d_marked;
         a.n_marked = c->n_marked;
+        a.tilemap = c->d_tilemap;
         a.f0_scale = ldexp(1.0, -c->n);
         a.mid = s.mid;
         a.has_origin = origin_here(c) ? 1 : 0;
@@ -276,7 +278,16 @@ void store_marked(sv_ctx *c, const uint64_t *marked, uint64_t m) {
         c->marked_cap = cnt;
     }
     if (cnt) SV_CUDA(cudaMemcpyAsync(c->d_marked, loc.data(), cnt * 8, cudaMemcpyHostToDevice, c->stream));
-    SV_CUDA(cudaStreamSynchronize(c->stream));  // loc is freed on return
+    // tile bitmap for the oracle-fused contiguous passes
+    std::vector<unsigned int> map;
+    if (!c->plan.whole) {
+        const uint64_t ntiles = c->nres >> c->plan.T;
+        map.assign((ntiles + 31) / 32, 0u);
+        for (uint64_t v : loc) map[(v >> c->plan.T) >> 5] |= 1u << ((v >> c->plan.T) & 31);
+        if (!c->d_tilemap) dmalloc((void **)&c->d_tilemap, map.size() * 4, "tile bitmap");
+        SV_CUDA(cudaMemcpyAsync(c->d_tilemap, map.data(), map.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    }
+    SV_CUDA(cudaStreamSynchronize(c->stream));  // loc / map are freed on return
     c->n_marked = cnt;
     c->has_marked = true;
 }
@@ -293,6 +304,7 @@ void destroy(sv_ctx *c) {
     cudaFree(c->state);
     cudaFree(c->recv);
     cudaFree(c->d_marked);
+    cudaFree(c->d_tilemap);
     cudaFree(c->d_partials);
     cudaFree(c->d_sums);
     cudaFree(c->d_counter);

@@ -100,6 +100,7 @@ struct PassArgs {
     void *out = nullptr;
     const uint64_t *marked = nullptr;   // sorted local indices (device)
     uint64_t n_marked = 0;
+    const unsigned int *tilemap = nullptr;  // bit per contiguous 2^T tile: holds a marked index
     double f0_scale = 0.0;              // 2^-n
     int mid = MID_NONE;
     int has_origin = 0;                 // global index 0 resident at local 0

@@ -25,6 +25,10 @@
 
 #include "sv_internal.h"
 
+#ifndef SV_TILE_MIN_BLOCKS
+#define SV_TILE_MIN_BLOCKS 2
+#endif
+
 namespace sv {
 
 template <typename E> struct RealOf;
@@ -94,6 +98,7 @@ struct KParams {
     void *out;
     const unsigned long long *marked;
     unsigned long long n_marked;
+    const unsigned int *tilemap;   // bit t: contiguous tile t holds a marked index
     double f0_scale;
     int mid;
     int has_origin;
@@ -111,13 +116,43 @@ __device__ __forceinline__ void bfly(E &x, E &y) {
     y.y = t.y - y.y;
 }
 
-template <class L, int PH, typename E>
-__device__ __forceinline__ void run_stages(E (&x)[L::NR], unsigned int proc) {
+// complex64: one packed FADD2 for the sum and one for the difference
+// (sm_100a add/sub.rn.f32x2; per-lane IEEE fp32, identical to two FADDs).
+template <>
+__device__ __forceinline__ void bfly<float2>(float2 &x, float2 &y) {
+    unsigned long long a = *reinterpret_cast<unsigned long long *>(&x);
+    unsigned long long b = *reinterpret_cast<unsigned long long *>(&y);
+    unsigned long long s, d;
+    asm("add.rn.f32x2 %0, %2, %3;\n\tsub.rn.f32x2 %1, %2, %3;" : "=l"(s), "=l"(d) : "l"(a), "l"(b));
+    x = *reinterpret_cast<float2 *>(&s);
+    y = *reinterpret_cast<float2 *>(&d);
+}
+
+template <typename E, typename R>
+__device__ __forceinline__ void scale(E &x, R s) {
+    x.x *= s;
+    x.y *= s;
+}
+
+template <>
+__device__ __forceinline__ void scale<float2, float>(float2 &x, float s) {
+    unsigned long long a = *reinterpret_cast<unsigned long long *>(&x), r;
+    float2 ss = make_float2(s, s);
+    unsigned long long b = *reinterpret_cast<unsigned long long *>(&ss);
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    x = *reinterpret_cast<float2 *>(&r);
+}
+
+// Stages of layout PH.  The processed tile bits are always [U, TB): the
+// unprocessed slots of a tile are its lowest ones (plan.cpp make_group), so
+// U is a template parameter and the unrolled stage code has no branches.
+template <class L, int PH, int U, typename E>
+__device__ __forceinline__ void run_stages(E (&x)[L::NR]) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
         if (i < L::kRB) {
             const int b = L::reg_bit(PH, i);
-            if (L::owns(PH, b) && ((proc >> b) & 1u)) {
+            if (L::owns(PH, b) && b >= U) {
 #pragma unroll
                 for (int j = 0; j < L::NR; ++j)
                     if (!(j & (1 << i))) bfly(x[j], x[j | (1 << i)]);
@@ -237,7 +272,7 @@ __device__ __forceinline__ void mid_op(E (&x)[L::NR], const KParams &p, unsigned
         // transforms (G2, G5): -2^{-n} x everywhere, +2^{-n} x at index 0.
         const R s = (R)(-p.f0_scale);
 #pragma unroll
-        for (int j = 0; j < L::NR; ++j) { x[j].x *= s; x[j].y *= s; }
+        for (int j = 0; j < L::NR; ++j) scale(x[j], s);
         if (p.has_origin && base == 0 && tid == 0) { x[0].x = -x[0].x; x[0].y = -x[0].y; }
     } else if (p.mid == MID_ORACLE) {
         // O: negate marked amplitudes (G3).  The tile is contiguous (slots
@@ -260,8 +295,8 @@ __device__ __forceinline__ void mid_op(E (&x)[L::NR], const KParams &p, unsigned
     }
 }
 
-template <typename E, int TB, int RB, bool PRE, bool POST>
-__global__ void __launch_bounds__(1 << (TB - RB), 2) wht_tile_kernel(const KParams p) {
+template <typename E, int TB, int RB, bool PRE, bool POST, int U>
+__global__ void __launch_bounds__(1 << (TB - RB), SV_TILE_MIN_BLOCKS) wht_tile_kernel(const KParams p) {
     using L = Layout<E, TB, RB>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     E *sm = reinterpret_cast<E *>(smem_raw);
@@ -277,54 +312,59 @@ __global__ void __launch_bounds__(1 << (TB - RB), 2) wht_tile_kernel(const KPara
         fm ^= low;
     }
 
-    if (p.mid == MID_ORACLE && tid == 0) {
-        // marked entries inside [base, base + 2^TB): lower_bound twice
-        unsigned long long lo = 0, hi = p.n_marked;
-        while (lo < hi) {
-            unsigned long long md = (lo + hi) >> 1;
-            if (p.marked[md] < base) lo = md + 1; else hi = md;
-        }
-        unsigned long long a = lo;
-        hi = p.n_marked;
-        const unsigned long long end = base + (1ull << TB);
-        while (lo < hi) {
-            unsigned long long md = (lo + hi) >> 1;
-            if (p.marked[md] < end) lo = md + 1; else hi = md;
-        }
-        s_mlo = a;
-        s_mcnt = lo - a;
-    }
-
     E x[L::NR];
     global_load<L, 0>(x, reinterpret_cast<const E *>(p.in) + base, p, tid);
     E *gout = reinterpret_cast<E *>(p.out) + base;
 
+    // Oracle tiles: one bitmap word says whether this tile holds a marked
+    // index (rare); only then does thread 0 binary-search the sorted list.
+    bool has_marked = false;
+    if (p.mid == MID_ORACLE) {
+        has_marked = (__ldg(&p.tilemap[blockIdx.x >> 5]) >> (blockIdx.x & 31)) & 1u;
+        if (has_marked && tid == 0) {
+            unsigned long long lo = 0, hi = p.n_marked;
+            while (lo < hi) {
+                unsigned long long md = (lo + hi) >> 1;
+                if (p.marked[md] < base) lo = md + 1; else hi = md;
+            }
+            unsigned long long a = lo;
+            hi = p.n_marked;
+            const unsigned long long end = base + (1ull << TB);
+            while (lo < hi) {
+                unsigned long long md = (lo + hi) >> 1;
+                if (p.marked[md] < end) lo = md + 1; else hi = md;
+            }
+            s_mlo = a;
+            s_mcnt = lo - a;
+        }
+    }
+
     if (PRE) {
-        run_stages<L, 0>(x, p.proc);
+        run_stages<L, 0, U>(x);
         relayout<L, 0, 1>(x, sm, tid);
-        run_stages<L, 1>(x, p.proc);
+        run_stages<L, 1, U>(x);
         relayout<L, 1, 2>(x, sm, tid);
-        run_stages<L, 2>(x, p.proc);
-        if (p.mid != MID_NONE) mid_op<L, 2>(x, p, base, tid, s_mlo, s_mcnt);
+        run_stages<L, 2, U>(x);
+        if (p.mid == MID_F0 || has_marked) mid_op<L, 2>(x, p, base, tid, s_mlo, s_mcnt);
         if (POST) {
-            run_stages<L, 2>(x, p.proc);
+            run_stages<L, 2, U>(x);
             relayout<L, 2, 1>(x, sm, tid);
-            run_stages<L, 1>(x, p.proc);
+            run_stages<L, 1, U>(x);
             relayout<L, 1, 0>(x, sm, tid);
-            run_stages<L, 0>(x, p.proc);
+            run_stages<L, 0, U>(x);
             global_store<L, 0>(x, gout, p, tid);
         } else {
             global_store<L, 2>(x, gout, p, tid);
         }
     } else {
-        if (p.mid == MID_ORACLE) __syncthreads();  // s_mlo / s_mcnt
-        if (p.mid != MID_NONE) mid_op<L, 0>(x, p, base, tid, s_mlo, s_mcnt);
+        if (has_marked) __syncthreads();  // s_mlo / s_mcnt (uniform branch)
+        if (p.mid == MID_F0 || has_marked) mid_op<L, 0>(x, p, base, tid, s_mlo, s_mcnt);
         if (POST) {
-            run_stages<L, 0>(x, p.proc);
+            run_stages<L, 0, U>(x);
             relayout<L, 0, 1>(x, sm, tid);
-            run_stages<L, 1>(x, p.proc);
+            run_stages<L, 1, U>(x);
             relayout<L, 1, 2>(x, sm, tid);
-            run_stages<L, 2>(x, p.proc);
+            run_stages<L, 2, U>(x);
             global_store<L, 2>(x, gout, p, tid);
         } else {
             global_store<L, 0>(x, gout, p, tid);
@@ -332,10 +372,10 @@ __global__ void __launch_bounds__(1 << (TB - RB), 2) wht_tile_kernel(const KPara
     }
 }
 
-template <typename E, int TB, int RB, bool PRE, bool POST>
+template <typename E, int TB, int RB, bool PRE, bool POST, int U>
 static void launch_tile_t(const KParams &kp, unsigned long long ntiles, cudaStream_t s) {
     using L = Layout<E, TB, RB>;
-    auto fn = wht_tile_kernel<E, TB, RB, PRE, POST>;
+    auto fn = wht_tile_kernel<E, TB, RB, PRE, POST, U>;
     const int smem = (1 << TB) * (int)sizeof(E);
     static bool attr = false;
     if (!attr) {
@@ -347,12 +387,17 @@ static void launch_tile_t(const KParams &kp, unsigned long long ntiles, cudaStre
     SV_CUDA(cudaGetLastError());
 }
 
-template <typename E, int TB, int RB>
-static void launch_tile_cfg(const KParams &kp, int pre, int post, unsigned long long ntiles, cudaStream_t s) {
-    if (pre && post) launch_tile_t<E, TB, RB, true, true>(kp, ntiles, s);
-    else if (pre) launch_tile_t<E, TB, RB, true, false>(kp, ntiles, s);
-    else if (post) launch_tile_t<E, TB, RB, false, true>(kp, ntiles, s);
-    else SV_CHECK(false, SV_EINVAL, "internal: tile pass without stages");
+template <typename E, int TB, int RB, int U>
+static void launch_tile_u(const KParams &kp, int pre, int post, int u, unsigned long long ntiles, cudaStream_t s) {
+    if constexpr (U < TB) {
+        if (u != U) return launch_tile_u<E, TB, RB, U + 1>(kp, pre, post, u, ntiles, s);
+        if (pre && post) launch_tile_t<E, TB, RB, true, true, U>(kp, ntiles, s);
+        else if (pre) launch_tile_t<E, TB, RB, true, false, U>(kp, ntiles, s);
+        else if (post) launch_tile_t<E, TB, RB, false, true, U>(kp, ntiles, s);
+        else SV_CHECK(false, SV_EINVAL, "internal: tile pass without stages");
+    } else {
+        SV_CHECK(false, SV_EINVAL, "internal: no processed tile bits");
+    }
 }
 
 void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
@@ -361,6 +406,7 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
     kp.in = a.in;
     kp.out = a.out;
     kp.marked = reinterpret_cast<const unsigned long long *>(a.marked);
+    kp.tilemap = a.tilemap;
     kp.n_marked = a.n_marked;
     kp.f0_scale = a.f0_scale;
     kp.mid = a.mid;
@@ -380,12 +426,19 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
     }
     SV_CHECK(b == TB, SV_EINVAL, "internal: tile mask does not have T slots");
     SV_CHECK(kp.slot[0] == 0, SV_EINVAL, "internal: tile must contain slot 0");
-    if (a.mid == MID_ORACLE)
+    if (a.mid == MID_ORACLE) {
         for (int i = 0; i < TB; ++i) SV_CHECK(kp.slot[i] == i, SV_EINVAL, "internal: oracle needs a contiguous tile");
+        SV_CHECK(a.tilemap != nullptr, SV_EINVAL, "internal: oracle pass without tile bitmap");
+    }
     kp.proc = proc;
+    // processed tile bits must be [u, TB) (see run_stages)
+    int u = 0;
+    while (u < TB && !((proc >> u) & 1u)) ++u;
+    SV_CHECK(u < TB && proc == (((1u << TB) - 1u) & ~((1u << u) - 1u)), SV_EINVAL,
+             "internal: processed tile bits are not the top ones");
     const unsigned long long ntiles = 1ull << f;
-    if (dt == SV_C64) launch_tile_cfg<float2, kTileBitsC64, kRegBitsC64>(kp, a.pre, a.post, ntiles, s);
-    else launch_tile_cfg<double2, kTileBitsC128, kRegBitsC128>(kp, a.pre, a.post, ntiles, s);
+    if (dt == SV_C64) launch_tile_u<float2, kTileBitsC64, kRegBitsC64, 0>(kp, a.pre, a.post, u, ntiles, s);
+    else launch_tile_u<double2, kTileBitsC128, kRegBitsC128, 0>(kp, a.pre, a.post, u, ntiles, s);
 }
 
 // ------------------------------------------------------------------------- //

@@ -286,7 +286,7 @@ def test_errors():
     with pytest.raises(sv.SvError):
         sv.sv_init(16, world=3)
     with pytest.raises(sv.SvError):
-        sv.sv_init(20, world=8)  # n - 2g < T
+        sv.sv_init(18, world=8)  # n - 2g < T
     with sv.sv_init(12, 0, sv.SV_C64) as c:
         with pytest.raises(sv.SvError) as e:
             sv.sv_iterate(c, 1)
