@@ -209,6 +209,11 @@ sv_status sv_profile(sv_ctx *ctx, int enable);
  * kind since sv_profile(ctx, 1). */
 sv_status sv_profile_read(sv_ctx *ctx, int kind, uint64_t *launches, double *total_ms);
 
+/* Synchronises, then writes the kind and device milliseconds of each profiled
+ * launch since sv_profile(ctx, 1), in launch order (at most cap entries;
+ * *count = total).  Pairs with sv_plan_wht to attribute time to passes. */
+sv_status sv_profile_timeline(sv_ctx *ctx, int *kinds, double *ms, uint64_t cap, uint64_t *count);
+
 /* ---- layout introspection (host only; used by tests/test_layouts.py) ----- */
 
 /* Tile element index and swizzled shared-memory slot held by thread `tid`,

@@ -44,7 +44,7 @@ class sv_plan_step(ctypes.Structure):
 
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_quant_ph_9804039_b200.build` "
+    raise ImportError(f"{LIB_PATH} is missing: run `python paper_quant_ph_9804039_b200/build.py` "
                       "(no CPU fallback exists)")
 lib = ctypes.CDLL(LIB_PATH)
 
@@ -69,6 +69,7 @@ _SIGS = {
     "sv_plan_wht": ([_i32, _i32, _i32, _i32, _i32, ctypes.POINTER(sv_plan_step), _i32, ctypes.POINTER(_i32)], _i32),
     "sv_profile": ([_ctxp, _i32], _i32),
     "sv_profile_read": ([_ctxp, _i32, ctypes.POINTER(_u64), _dp], _i32),
+    "sv_profile_timeline": ([_ctxp, _vp, _vp, _u64, ctypes.POINTER(_u64)], _i32),
     "sv_free": ([_ctxp], None),
     "sv_last_error": ([], ctypes.c_char_p),
     "sv_debug_tile_layout": ([_i32, _i32, _i32, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)], _i32),
@@ -221,6 +222,16 @@ def sv_profile_read(ctx: Ctx, kind: int) -> tuple[int, float]:
     ms = ctypes.c_double()
     _check(lib.sv_profile_read(ctx.ptr, kind, ctypes.byref(n), ctypes.byref(ms)), "sv_profile_read")
     return n.value, ms.value
+
+
+def sv_profile_timeline(ctx: Ctx) -> list[tuple[int, float]]:
+    cnt = _u64()
+    _check(lib.sv_profile_timeline(ctx.ptr, None, None, 0, ctypes.byref(cnt)), "sv_profile_timeline")
+    kinds = np.zeros(max(cnt.value, 1), dtype=np.int32)
+    ms = np.zeros(max(cnt.value, 1), dtype=np.float64)
+    _check(lib.sv_profile_timeline(ctx.ptr, kinds.ctypes.data, ms.ctypes.data, cnt.value, ctypes.byref(cnt)),
+           "sv_profile_timeline")
+    return [(int(kinds[i]), float(ms[i])) for i in range(cnt.value)]
 
 
 def sv_free(ctx: Ctx) -> None:

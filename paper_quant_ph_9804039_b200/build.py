@@ -1,6 +1,6 @@
 """Build libsv.so (hand-written CUDA for sm_100a + NCCL) in-tree with nvcc.
 
-python -m paper_quant_ph_9804039_b200.build [--force] [--verbose]
+python paper_quant_ph_9804039_b200/build.py [--force] [--verbose] [-DMACRO=V --out=PATH]
 Compiles every csrc/*.cu and csrc/*.cpp to an object (in parallel) and links
 paper_quant_ph_9804039_b200/libsv.so; objects and the .so are git-ignored but
 travel to the GPU box with the gpurun snapshot.

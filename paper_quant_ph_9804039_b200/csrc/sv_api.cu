@@ -56,6 +56,7 @@ struct sv_ctx {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
     uint64_t launches[SV_K_COUNT] = {};
     double ms[SV_K_COUNT] = {};
+    std::vector<std::pair<int, double>> timeline;  // (kind, ms) per profiled launch, in order
 };
 
 namespace {
@@ -116,6 +117,7 @@ void drain_profile(sv_ctx *c) {
         float ms = 0.f;
         SV_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
         c->ms[p.kind] += ms;
+        c->timeline.emplace_back(p.kind, (double)ms);
         c->pool.push_back({p.a, p.b});
     }
     c->pending.clear();
@@ -554,6 +556,19 @@ sv_status sv_profile(sv_ctx *c, int enable) {
         for (int i = 0; i < SV_K_COUNT; ++i) {
             c->launches[i] = 0;
             c->ms[i] = 0.0;
+        }
+        c->timeline.clear();
+    });
+}
+
+sv_status sv_profile_timeline(sv_ctx *c, int *kinds, double *ms, uint64_t cap, uint64_t *count) {
+    return guarded([&] {
+        check_ctx(c);
+        drain_profile(c);
+        if (count) *count = c->timeline.size();
+        for (uint64_t i = 0; i < cap && i < c->timeline.size(); ++i) {
+            if (kinds) kinds[i] = c->timeline[i].first;
+            if (ms) ms[i] = c->timeline[i].second;
         }
     });
 }

@@ -46,7 +46,10 @@ struct Error {
 // ------------------------------------------------------------------------- //
 // Tile geometry per dtype                       //
 // ------------------------------------------------------------------------- //
-constexpr int kTileBitsC64 = 13;   // 2^13 x 8 B  = 64 KiB smem tile
+#ifndef SV_TILE_BITS_C64
+#define SV_TILE_BITS_C64 13
+#endif
+constexpr int kTileBitsC64 = SV_TILE_BITS_C64;  // 2^13 x 8 B = 64 KiB smem tile (14: 128 KiB, A/B only)
 constexpr int kRegBitsC64 = 5;     // 32 amplitudes per thread, 256 threads
 constexpr int kTileBitsC128 = 12;  // 2^12 x 16 B = 64 KiB smem tile
 constexpr int kRegBitsC128 = 4;    // 16 amplitudes per thread, 256 threads

@@ -296,7 +296,7 @@ __device__ __forceinline__ void mid_op(E (&x)[L::NR], const KParams &p, unsigned
 }
 
 template <typename E, int TB, int RB, bool PRE, bool POST, int U>
-__global__ void __launch_bounds__(1 << (TB - RB), SV_TILE_MIN_BLOCKS) wht_tile_kernel(const KParams p) {
+__global__ void __launch_bounds__(1 << (TB - RB), (TB - RB >= 9) ? 1 : SV_TILE_MIN_BLOCKS) wht_tile_kernel(const KParams p) {
     using L = Layout<E, TB, RB>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     E *sm = reinterpret_cast<E *>(smem_raw);
