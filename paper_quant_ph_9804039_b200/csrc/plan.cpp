@@ -72,11 +72,28 @@ Plan make_plan(int n, int g, sv_dtype dtype) {
     SV_CHECK(nl - g >= T, SV_EINVAL,
              "shard too small for the sharded WHT: need n - 2*log2(world) >= " + std::to_string(T));
     p.groups.push_back(make_group(range_mask(0, T), T, nl));  // G1: contiguous
+    // Which groups host the elementwise ops.  The O- and F0-groups are visited
+    // once per iteration with both stage sets fused around the op; the others
+    // twice.  Fusing doubles a pass's on-chip work (stages + shared-memory
+    // relayouts), so the fused roles go to the groups with the FEWEST
+    // processed slots and the contiguous 13-slot G1 -- the cheapest pass to
+    // run unfused -- is visited twice.
+    auto nproc = [&](int i) { return __builtin_popcountll(p.groups[i].proc); };
     if (g == 0) {
         std::vector<int> rest;
         for (int s = T; s < nl; ++s) rest.push_back(s);
         for (uint64_t m : chunk(rest, Rs)) p.groups.push_back(make_group(m, T, nl));
-        for (int i = 0; i < (int)p.groups.size(); ++i) p.fwd.push_back(i);
+        const int ng = (int)p.groups.size();
+        std::vector<int> order;
+        for (int i = 1; i < ng; ++i) order.push_back(i);
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return nproc(a) < nproc(b); });
+        // order[0] = smallest strided group -> F0; order[1] (or G1) -> O
+        const int f0g = order[0];
+        const int og = ng >= 3 ? order[1] : 0;
+        p.fwd.push_back(og);
+        for (int i = 0; i < ng; ++i)
+            if (i != og && i != f0g) p.fwd.push_back(i);
+        p.fwd.push_back(f0g);
         return p;
     }
     // P > 1: U = top g local slots, processed once before the swap (they hold
@@ -89,11 +106,14 @@ Plan make_plan(int n, int g, sv_dtype dtype) {
     rest.resize(rest.size() - take);
     std::vector<int> l0 = rest;
     for (int s = nl - g; s < nl; ++s) l0.push_back(s);
-    p.fwd.push_back(0);
-    for (uint64_t m : chunk(l0, Rs)) {
-        p.groups.push_back(make_group(m, T, nl));
-        p.fwd.push_back((int)p.groups.size() - 1);
-    }
+    for (uint64_t m : chunk(l0, Rs)) p.groups.push_back(make_group(m, T, nl));
+    // O must run in the natural layout (before the swap): smallest L0 group
+    int og = 0;
+    for (int i = 1; i < (int)p.groups.size(); ++i)
+        if (og == 0 || nproc(i) < nproc(og)) og = i;
+    p.fwd.push_back(og);
+    for (int i = 0; i < (int)p.groups.size(); ++i)
+        if (i != og) p.fwd.push_back(i);
     p.fwd.push_back(-1);  // reorganisation (qubit swap)
     p.groups.push_back(make_group(l1, T, nl));
     p.fwd.push_back((int)p.groups.size() - 1);
@@ -177,10 +197,10 @@ std::vector<Step> schedule_wht(const Plan &plan, int k, bool with_oracle) {
                 i += 1;
             }
         }
-        // the oracle needs a contiguous tile (binary search of the sorted
-        // marked list); by construction it only meets groups[0]
+        // the oracle's per-tile marked lookup (sv_api.cu) is built for the
+        // O-group only; by construction O only meets plan.fwd[0]
         if (s.kind == STEP_PASS && s.mid == MID_ORACLE)
-            SV_CHECK(s.group == 0, SV_EINVAL, "internal: oracle fused into a strided tile");
+            SV_CHECK(s.group == plan.fwd[0], SV_EINVAL, "internal: oracle fused into a non-O group");
         steps.push_back(s);
     }
     return steps;

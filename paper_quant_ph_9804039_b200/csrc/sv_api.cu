@@ -42,7 +42,9 @@ struct sv_ctx {
     uint64_t nl_amps = 0;    // amplitudes per rank (2^{n-g})
     uint64_t *d_marked = nullptr;
     uint64_t marked_cap = 0;
-    unsigned int *d_tilemap = nullptr;  // one bit per contiguous 2^T tile of the resident state
+    unsigned int *d_tilemap = nullptr;  // one bit per tile of the O-group (holds a marked index)
+    uint64_t *d_okeys = nullptr;        // sorted (tile id << 16 | element) of the marked entries
+    uint64_t okeys_cap = 0;
     uint64_t n_marked = 0;   // resident (local) marked entries
     bool has_marked = false;
     double *d_partials = nullptr;  // 2 * kMaxGrid
@@ -201,7 +203,7 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle) {
         PassArgs a;
         a.in = s.in_recv ? c->recv : c->state;
         a.out = c->state;
-        a.marked = c->d_marked;
+        a.marked = c->d_okeys;  // O-group lookup keys (only read by oracle passes)
         a.n_marked = c->n_marked;
         a.tilemap = c->d_tilemap;
         a.f0_scale = ldexp(1.0, -c->n);
@@ -280,16 +282,42 @@ void store_marked(sv_ctx *c, const uint64_t *marked, uint64_t m) {
         c->marked_cap = cnt;
     }
     if (cnt) SV_CUDA(cudaMemcpyAsync(c->d_marked, loc.data(), cnt * 8, cudaMemcpyHostToDevice, c->stream));
-    // tile bitmap for the oracle-fused contiguous passes
+    // Per-tile lookup for the O-group's oracle-fused passes: a bitmap over its
+    // tiles and the sorted keys (tile id << 16 | tile element) of the marked
+    // entries -- tile id / element = the index's free / tile slot bits.
     std::vector<unsigned int> map;
+    std::vector<uint64_t> keys(cnt);
     if (!c->plan.whole) {
+        const int total_bits = c->emulated ? c->n : c->plan.nl;
+        const uint64_t tmask = c->plan.groups[c->plan.fwd[0]].tile;
+        const uint64_t fmask = ((total_bits >= 64) ? ~0ull : ((1ull << total_bits) - 1ull)) & ~tmask;
+        auto pext = [](uint64_t v, uint64_t m) {
+            uint64_t r = 0;
+            int k = 0;
+            for (int b = 0; b < 64; ++b)
+                if ((m >> b) & 1) r |= ((v >> b) & 1ull) << k++;
+            return r;
+        };
         const uint64_t ntiles = c->nres >> c->plan.T;
         map.assign((ntiles + 31) / 32, 0u);
-        for (uint64_t v : loc) map[(v >> c->plan.T) >> 5] |= 1u << ((v >> c->plan.T) & 31);
+        for (uint64_t j = 0; j < cnt; ++j) {
+            const uint64_t t = pext(loc[j], fmask);
+            keys[j] = (t << 16) | pext(loc[j], tmask);
+            map[t >> 5] |= 1u << (t & 31);
+        }
+        std::sort(keys.begin(), keys.end());
         if (!c->d_tilemap) dmalloc((void **)&c->d_tilemap, map.size() * 4, "tile bitmap");
         SV_CUDA(cudaMemcpyAsync(c->d_tilemap, map.data(), map.size() * 4, cudaMemcpyHostToDevice, c->stream));
+        if (cnt > c->okeys_cap) {
+            if (c->d_okeys) SV_CUDA(cudaFree(c->d_okeys));
+            c->d_okeys = nullptr;
+            c->okeys_cap = 0;
+            dmalloc((void **)&c->d_okeys, cnt * 8, "oracle keys");
+            c->okeys_cap = cnt;
+        }
+        if (cnt) SV_CUDA(cudaMemcpyAsync(c->d_okeys, keys.data(), cnt * 8, cudaMemcpyHostToDevice, c->stream));
     }
-    SV_CUDA(cudaStreamSynchronize(c->stream));  // loc / map are freed on return
+    SV_CUDA(cudaStreamSynchronize(c->stream));  // loc / map / keys are freed on return
     c->n_marked = cnt;
     c->has_marked = true;
 }
@@ -307,6 +335,7 @@ void destroy(sv_ctx *c) {
     cudaFree(c->recv);
     cudaFree(c->d_marked);
     cudaFree(c->d_tilemap);
+    cudaFree(c->d_okeys);
     cudaFree(c->d_partials);
     cudaFree(c->d_sums);
     cudaFree(c->d_counter);

@@ -86,6 +86,7 @@ struct Plan {
     int T = 0;        // tile bits
     bool whole = false;
     std::vector<Group> groups;   // groups[0] = contiguous slots [0, T)
+    // fwd[0] hosts the oracle O (natural layout), fwd.back() hosts F0
     std::vector<int> fwd;        // first transform: group indices, -1 = swap
 };
 

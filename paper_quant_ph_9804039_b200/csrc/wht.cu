@@ -44,12 +44,17 @@ struct Layout {
     static constexpr int NT = 1 << (TB - RB);             // threads
     static constexpr int NR = 1 << RB;                    // amplitudes per thread
     static constexpr int kTB = TB, kRB = RB;
-    static_assert(TB >= 2 * RB && TB <= 3 * RB, "three layouts must cover the tile");
+    // complex64: tile bit 0 is a register bit in EVERY layout, so each thread
+    // always holds adjacent pairs (e, e|1) = 16 bytes -> every shared and
+    // global access is 128-bit; the other RB-1 register bits cover 3(RB-1)
+    // tile bits.  complex128: one amplitude is already 16 bytes.
+    static_assert(VE == 2 ? (TB >= 2 * RB - 1 && TB <= 3 * RB - 2) : (TB >= 2 * RB && TB <= 3 * RB),
+                  "three layouts must cover the tile");
     static_assert(TB - RB >= 5, "need at least one warp");
 
     // i-th register bit (ascending) of layout ph (0 = A, 1 = B, 2 = C).
     __host__ __device__ static constexpr int reg_bit(int ph, int i) {
-        return VE == 2 ? (ph == 0 ? (i == 0 ? 0 : TB - RB + i) : ph == 1 ? 1 + i : TB - 2 * RB + 1 + i)
+        return VE == 2 ? (i == 0 ? 0 : ph == 0 ? TB - RB + i : ph == 1 ? i : TB - 2 * RB + 1 + i)
                        : (ph == 0 ? TB - RB + i : ph == 1 ? i : TB - 2 * RB + i);
     }
     __host__ __device__ static constexpr bool is_reg(int ph, int b) {
@@ -71,13 +76,13 @@ struct Layout {
     // Each tile bit's stage runs in exactly one layout: A and B are disjoint;
     // C runs only the bits B does not have.
     __host__ __device__ static constexpr bool owns(int ph, int b) {
-        return ph == 0 ? is_reg(0, b) : ph == 1 ? is_reg(1, b) : (is_reg(2, b) && !is_reg(1, b) && !is_reg(0, b));
+        return ph == 0 ? is_reg(0, b) : ph == 1 ? (is_reg(1, b) && !is_reg(0, b)) : (is_reg(2, b) && !is_reg(1, b) && !is_reg(0, b));
     }
     // XOR swizzle of the shared-memory index (linear over GF(2)): makes the
     // 8-lane (16 B) / 16-lane (8 B) wavefronts of every layout bank-conflict
     // free -- checked exhaustively by tests/test_layouts.py via sv_debug.
     __host__ __device__ static constexpr uint32_t swz(uint32_t e) {
-        return VE == 2 ? (e ^ (((e >> (RB + 1)) & 7u) << 1)) : (e ^ ((e >> RB) & 7u));
+        return VE == 2 ? (e ^ (((e >> RB) & 7u) << 1)) : (e ^ ((e >> RB) & 7u));
     }
     __host__ __device__ static constexpr uint32_t ereg(int ph, int j) {
         uint32_t e = 0;
@@ -161,6 +166,22 @@ __device__ __forceinline__ void run_stages(E (&x)[L::NR]) {
     }
 }
 
+// Read this thread's amplitudes of layout PR from the swizzled smem tile
+// (sr = swizzled thread part of the index).
+template <class L, int PR, typename E>
+__device__ __forceinline__ void smem_read(E (&x)[L::NR], const E *sm, uint32_t sr) {
+    if constexpr (L::VE == 2) {
+#pragma unroll
+        for (int v = 0; v < L::NR / 2; ++v) {
+            float4 q = *reinterpret_cast<const float4 *>(&sm[sr ^ L::swz(L::ereg(PR, 2 * v))]);
+            x[2 * v].x = q.x; x[2 * v].y = q.y; x[2 * v + 1].x = q.z; x[2 * v + 1].y = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < L::NR; ++j) x[j] = sm[sr ^ L::swz(L::ereg(PR, j))];
+    }
+}
+
 // Shared-memory layout change PW -> PR.  One barrier: each thread writes the
 // positions it read in the previous change (or, for the first write, nobody
 // has read yet), so no write can race a pending read.
@@ -168,7 +189,7 @@ template <class L, int PW, int PR, typename E>
 __device__ __forceinline__ void relayout(E (&x)[L::NR], E *sm, int tid) {
     const uint32_t sw = L::swz(L::ethr(PW, tid));
     const uint32_t sr = L::swz(L::ethr(PR, tid));
-    if constexpr (L::VE == 2 && PW == 0) {
+    if constexpr (L::VE == 2) {
 #pragma unroll
         for (int v = 0; v < L::NR / 2; ++v) {
             float4 q;
@@ -180,16 +201,26 @@ __device__ __forceinline__ void relayout(E (&x)[L::NR], E *sm, int tid) {
         for (int j = 0; j < L::NR; ++j) sm[sw ^ L::swz(L::ereg(PW, j))] = x[j];
     }
     __syncthreads();
-    if constexpr (L::VE == 2 && PR == 0) {
-#pragma unroll
-        for (int v = 0; v < L::NR / 2; ++v) {
-            float4 q = *reinterpret_cast<const float4 *>(&sm[sr ^ L::swz(L::ereg(PR, 2 * v))]);
-            x[2 * v].x = q.x; x[2 * v].y = q.y; x[2 * v + 1].x = q.z; x[2 * v + 1].y = q.w;
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < L::NR; ++j) x[j] = sm[sr ^ L::swz(L::ereg(PR, j))];
-    }
+    smem_read<L, PR>(x, sm, sr);
+}
+
+// Streaming 128-bit global load.  Every amplitude is read exactly once per
+// pass, so L1 allocation only costs: SV_LD_MODE 0 = default (ld.global),
+// 1 = ld.global.cg (L2 only), 2 = ld.global.nc.L1::no_allocate.
+#ifndef SV_LD_MODE
+#define SV_LD_MODE 1
+#endif
+__device__ __forceinline__ float4 ld_stream(const float4 *p) {
+#if SV_LD_MODE == 1
+    return __ldcg(p);
+#elif SV_LD_MODE == 2
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+#else
+    return *p;
+#endif
 }
 
 // Global offset (elements) of tile element e under the pass's slot map.
@@ -210,14 +241,14 @@ __device__ __forceinline__ void global_load(E (&x)[L::NR], const E *g, const KPa
 #pragma unroll
     for (int i = 0; i < 16; ++i)
         if (i < L::kRB) st[i] = 1ull << p.slot[L::reg_bit(PH, i)];
-    if constexpr (L::VE == 2 && PH == 0) {
+    if constexpr (L::VE == 2) {
 #pragma unroll
         for (int v = 0; v < L::NR / 2; ++v) {
             unsigned long long o = t;
 #pragma unroll
             for (int i = 1; i < 16; ++i)
                 if (i < L::kRB && (((2 * v) >> i) & 1)) o += st[i];
-            float4 q = *reinterpret_cast<const float4 *>(g + o);
+            float4 q = ld_stream(reinterpret_cast<const float4 *>(g + o));
             x[2 * v].x = q.x; x[2 * v].y = q.y; x[2 * v + 1].x = q.z; x[2 * v + 1].y = q.w;
         }
     } else {
@@ -227,7 +258,8 @@ __device__ __forceinline__ void global_load(E (&x)[L::NR], const E *g, const KPa
 #pragma unroll
             for (int i = 0; i < 16; ++i)
                 if (i < L::kRB && ((j >> i) & 1)) o += st[i];
-            x[j] = g[o];
+            const float4 q = ld_stream(reinterpret_cast<const float4 *>(g + o));
+            x[j] = *reinterpret_cast<const E *>(&q);
         }
     }
 }
@@ -239,7 +271,7 @@ __device__ __forceinline__ void global_store(const E (&x)[L::NR], E *g, const KP
 #pragma unroll
     for (int i = 0; i < 16; ++i)
         if (i < L::kRB) st[i] = 1ull << p.slot[L::reg_bit(PH, i)];
-    if constexpr (L::VE == 2 && PH == 0) {
+    if constexpr (L::VE == 2) {
 #pragma unroll
         for (int v = 0; v < L::NR / 2; ++v) {
             unsigned long long o = t;
@@ -275,10 +307,10 @@ __device__ __forceinline__ void mid_op(E (&x)[L::NR], const KParams &p, unsigned
         for (int j = 0; j < L::NR; ++j) scale(x[j], s);
         if (p.has_origin && base == 0 && tid == 0) { x[0].x = -x[0].x; x[0].y = -x[0].y; }
     } else if (p.mid == MID_ORACLE) {
-        // O: negate marked amplitudes (G3).  The tile is contiguous (slots
-        // 0..TB-1), so tile element e = m - base.
+        // O: negate marked amplitudes (G3).  Keys are (tile id << 16 | tile
+        // element e), e = the marked index's tile-slot bits (host-built).
         for (unsigned long long r = 0; r < mcnt; ++r) {
-            const uint32_t e = (uint32_t)(p.marked[mlo + r] - base);
+            const uint32_t e = (uint32_t)(p.marked[mlo + r] & 0xFFFFull);
             uint32_t t = 0, jj = 0;
 #pragma unroll
             for (int i = 0; i < 16; ++i)
@@ -295,57 +327,57 @@ __device__ __forceinline__ void mid_op(E (&x)[L::NR], const KParams &p, unsigned
     }
 }
 
-template <typename E, int TB, int RB, bool PRE, bool POST, int U>
-__global__ void __launch_bounds__(1 << (TB - RB), (TB - RB >= 9) ? 1 : SV_TILE_MIN_BLOCKS) wht_tile_kernel(const KParams p) {
-    using L = Layout<E, TB, RB>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    E *sm = reinterpret_cast<E *>(smem_raw);
-    __shared__ unsigned long long s_mlo, s_mcnt;
-    const int tid = threadIdx.x;
-
-    // tile base: scatter the tile id into the free slots (software pdep)
-    unsigned long long tile = blockIdx.x, base = 0, fm = p.free_mask;
+// Tile base: scatter the tile id into the free slots (software pdep).
+__device__ __forceinline__ unsigned long long tile_base(unsigned long long tile, unsigned long long fm) {
+    unsigned long long base = 0;
     while (fm) {
         const unsigned long long low = fm & (~fm + 1ull);
         if (tile & 1ull) base |= low;
         tile >>= 1;
         fm ^= low;
     }
+    return base;
+}
 
-    E x[L::NR];
-    global_load<L, 0>(x, reinterpret_cast<const E *>(p.in) + base, p, tid);
-    E *gout = reinterpret_cast<E *>(p.out) + base;
-
-    // Oracle tiles: one bitmap word says whether this tile holds a marked
-    // index (rare); only then does thread 0 binary-search the sorted list.
-    bool has_marked = false;
-    if (p.mid == MID_ORACLE) {
-        has_marked = (__ldg(&p.tilemap[blockIdx.x >> 5]) >> (blockIdx.x & 31)) & 1u;
-        if (has_marked && tid == 0) {
-            unsigned long long lo = 0, hi = p.n_marked;
-            while (lo < hi) {
-                unsigned long long md = (lo + hi) >> 1;
-                if (p.marked[md] < base) lo = md + 1; else hi = md;
-            }
-            unsigned long long a = lo;
-            hi = p.n_marked;
-            const unsigned long long end = base + (1ull << TB);
-            while (lo < hi) {
-                unsigned long long md = (lo + hi) >> 1;
-                if (p.marked[md] < end) lo = md + 1; else hi = md;
-            }
-            s_mlo = a;
-            s_mcnt = lo - a;
+// Oracle tiles: one bitmap word says whether this tile holds a marked index
+// (rare); only then does thread 0 binary-search the sorted keys (tile id << 16
+// | element) for this tile's range and publish it in shared memory.
+__device__ __forceinline__ bool oracle_lookup(const KParams &p, unsigned long long tile, int tid,
+                                              unsigned long long *s_mlo, unsigned long long *s_mcnt) {
+    const bool has = (__ldg(&p.tilemap[tile >> 5]) >> (tile & 31)) & 1u;
+    if (has && tid == 0) {
+        const unsigned long long first = tile << 16;
+        unsigned long long lo = 0, hi = p.n_marked;
+        while (lo < hi) {
+            unsigned long long md = (lo + hi) >> 1;
+            if (p.marked[md] < first) lo = md + 1; else hi = md;
         }
+        const unsigned long long a = lo;
+        hi = p.n_marked;
+        const unsigned long long end = first + (1ull << 16);
+        while (lo < hi) {
+            unsigned long long md = (lo + hi) >> 1;
+            if (p.marked[md] < end) lo = md + 1; else hi = md;
+        }
+        *s_mlo = a;
+        *s_mcnt = lo - a;
     }
+    return has;
+}
 
+// Everything after the tile is in registers (layout A): stage sets, the
+// elementwise op, relayouts through `sm`, and the coalesced global store.
+template <class L, bool PRE, bool POST, int U, typename E>
+__device__ __forceinline__ void tile_body(E (&x)[L::NR], E *sm, const KParams &p, unsigned long long base, E *gout,
+                                          int tid, bool has_marked, const unsigned long long *s_mlo,
+                                          const unsigned long long *s_mcnt) {
     if (PRE) {
         run_stages<L, 0, U>(x);
         relayout<L, 0, 1>(x, sm, tid);
         run_stages<L, 1, U>(x);
         relayout<L, 1, 2>(x, sm, tid);
         run_stages<L, 2, U>(x);
-        if (p.mid == MID_F0 || has_marked) mid_op<L, 2>(x, p, base, tid, s_mlo, s_mcnt);
+        if (p.mid == MID_F0 || has_marked) mid_op<L, 2>(x, p, base, tid, *s_mlo, *s_mcnt);
         if (POST) {
             run_stages<L, 2, U>(x);
             relayout<L, 2, 1>(x, sm, tid);
@@ -358,7 +390,7 @@ __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB >= 9) ? 1 : SV_TILE_M
         }
     } else {
         if (has_marked) __syncthreads();  // s_mlo / s_mcnt (uniform branch)
-        if (p.mid == MID_F0 || has_marked) mid_op<L, 0>(x, p, base, tid, s_mlo, s_mcnt);
+        if (p.mid == MID_F0 || has_marked) mid_op<L, 0>(x, p, base, tid, *s_mlo, *s_mcnt);
         if (POST) {
             run_stages<L, 0, U>(x);
             relayout<L, 0, 1>(x, sm, tid);
@@ -370,6 +402,21 @@ __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB >= 9) ? 1 : SV_TILE_M
             global_store<L, 0>(x, gout, p, tid);
         }
     }
+}
+
+// One CTA per tile: 128-bit loads straight into registers (layout A).
+template <typename E, int TB, int RB, bool PRE, bool POST, int U>
+__global__ void __launch_bounds__(1 << (TB - RB), (TB - RB >= 9) ? 1 : SV_TILE_MIN_BLOCKS) wht_tile_kernel(const KParams p) {
+    using L = Layout<E, TB, RB>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    E *sm = reinterpret_cast<E *>(smem_raw);
+    __shared__ unsigned long long s_mlo, s_mcnt;
+    const int tid = threadIdx.x;
+    const unsigned long long base = tile_base(blockIdx.x, p.free_mask);
+    E x[L::NR];
+    global_load<L, 0>(x, reinterpret_cast<const E *>(p.in) + base, p, tid);
+    const bool has_marked = (p.mid == MID_ORACLE) && oracle_lookup(p, blockIdx.x, tid, &s_mlo, &s_mcnt);
+    tile_body<L, PRE, POST, U>(x, sm, p, base, reinterpret_cast<E *>(p.out) + base, tid, has_marked, &s_mlo, &s_mcnt);
 }
 
 template <typename E, int TB, int RB, bool PRE, bool POST, int U>
@@ -426,10 +473,9 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
     }
     SV_CHECK(b == TB, SV_EINVAL, "internal: tile mask does not have T slots");
     SV_CHECK(kp.slot[0] == 0, SV_EINVAL, "internal: tile must contain slot 0");
-    if (a.mid == MID_ORACLE) {
-        for (int i = 0; i < TB; ++i) SV_CHECK(kp.slot[i] == i, SV_EINVAL, "internal: oracle needs a contiguous tile");
-        SV_CHECK(a.tilemap != nullptr, SV_EINVAL, "internal: oracle pass without tile bitmap");
-    }
+    if (a.mid == MID_ORACLE)
+        SV_CHECK(a.tilemap != nullptr && (a.n_marked == 0 || a.marked != nullptr), SV_EINVAL,
+                 "internal: oracle pass without its tile lookup");
     kp.proc = proc;
     // processed tile bits must be [u, TB) (see run_stages)
     int u = 0;

@@ -42,9 +42,9 @@ def test_shared_memory_bank_conflict_free(dtype):
     nt, nr = 1 << (T - R), 1 << R
     for ph in range(3):
         tab = layout(dtype, ph)
-        vec16 = dtype == sv.SV_C128 or ph == 0  # layout A of c64 moves 16-B pairs
+        vec16 = True  # c64 moves 16-B pairs (e, e|1) in every layout; c128 amplitudes are 16 B
         lanes_per_wave = 8 if vec16 else 16
-        regs = range(0, nr, 2) if (dtype == sv.SV_C64 and ph == 0) else range(nr)
+        regs = range(0, nr, 2) if dtype == sv.SV_C64 else range(nr)
         for w in range(nt // 32):
             for j in regs:
                 for q in range(0, 32, lanes_per_wave):
