@@ -31,6 +31,7 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     # name: (n, dtype, M, k, diffusion, seed, init, description)
     "c3": (28, "c64", 1, 64, "wht", 3, "uniform", "c3: n=28 complex64 (2 GiB), M=1, 64 WHT iterations"),
+    "c3m": (28, "c64", 1, 64, "mean", 3, "uniform", "c3 with the mean diffusion: n=28 complex64, M=1, 64 iterations"),
     "c4": (32, "c64", 256, 16, "wht", 4, "uniform",
            "c4: n=32 complex64 (32 GiB) sharded by top qubits, M=256 seeded, 16 WHT iterations"),
     "c5w": (34, "c64", 1024, 8, "wht", 5, "gaussian", "c5: n=34 complex64 (128 GiB), Gaussian start, M=1024, 8 WHT"),

@@ -18,10 +18,29 @@ REL64 = 2e-6  # complex64: max-abs error <= REL64 * max|a_ref|
 rng = np.random.default_rng(99)
 
 
+WORST = {"c64_rel": 0.0, "c64_abs": 0.0, "c128_abs": 0.0}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _report_worst_errors():
+    """Record the worst observed errors."""
+    yield
+    import json
+    import os
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    if os.path.isdir(out):
+        json.dump(WORST, open(os.path.join(out, "parity_error_stats.json"), "w"), indent=1)
+
+
 def assert_close(got, ref, dtype, what=""):
     got = np.asarray(got, dtype=np.complex128)
     err = float(np.max(np.abs(got - ref))) if ref.size else 0.0
     scale = float(np.max(np.abs(ref))) if ref.size else 0.0
+    if dtype == sv.SV_C64:
+        WORST["c64_abs"] = max(WORST["c64_abs"], err)
+        WORST["c64_rel"] = max(WORST["c64_rel"], err / scale if scale else 0.0)
+    else:
+        WORST["c128_abs"] = max(WORST["c128_abs"], err)
     assert err <= TOL[dtype], f"{what}: max-abs {err:.3e} > {TOL[dtype]:.0e}"
     if dtype == sv.SV_C64:
         assert err <= REL64 * scale + 1e-30, f"{what}: max-abs {err:.3e} > {REL64:.0e} x {scale:.3e}"
