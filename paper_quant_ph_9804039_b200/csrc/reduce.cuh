@@ -50,13 +50,5 @@ __device__ __forceinline__ void finalize(double re, double im, double *partials,
     }
 }
 
-// Chunk of vectors owned by block b (fixed for a fixed grid => deterministic).
-__device__ __forceinline__ void block_chunk(unsigned long long nvec, unsigned long long &lo, unsigned long long &hi) {
-    const unsigned long long per = (nvec + gridDim.x - 1) / gridDim.x;
-    lo = per * blockIdx.x;
-    hi = lo + per;
-    if (lo > nvec) lo = nvec;
-    if (hi > nvec) hi = nvec;
-}
 
 }  // namespace sv

@@ -45,6 +45,7 @@ struct sv_ctx {
     unsigned int *d_tilemap = nullptr;  // one bit per tile of the O-group (holds a marked index)
     uint64_t *d_okeys = nullptr;        // sorted (tile id << 16 | element) of the marked entries
     uint64_t okeys_cap = 0;
+    unsigned int *d_chunkmap = nullptr; // one bit per mean-kernel chunk (holds a marked index)
     uint64_t n_marked = 0;   // resident (local) marked entries
     bool has_marked = false;
     double *d_partials = nullptr;  // 2 * kMaxGrid
@@ -225,6 +226,7 @@ MeanArgs mean_args(sv_ctx *c, bool with_oracle) {
     m.inv_total = ldexp(1.0, -c->n);
     m.marked = with_oracle ? c->d_marked : nullptr;
     m.n_marked = with_oracle ? c->n_marked : 0;
+    m.chunkmap = c->d_chunkmap;
     m.partials = c->d_partials;
     m.counter = c->d_counter;
     return m;
@@ -317,7 +319,13 @@ void store_marked(sv_ctx *c, const uint64_t *marked, uint64_t m) {
         }
         if (cnt) SV_CUDA(cudaMemcpyAsync(c->d_okeys, keys.data(), cnt * 8, cudaMemcpyHostToDevice, c->stream));
     }
-    SV_CUDA(cudaStreamSynchronize(c->stream));  // loc / map / keys are freed on return
+    // chunk bitmap of the mean kernel
+    const uint64_t ce = mean_chunk_elems(c->dt);
+    std::vector<unsigned int> cmap(((c->nres + ce - 1) / ce + 31) / 32, 0u);
+    for (uint64_t v : loc) cmap[(v / ce) >> 5] |= 1u << ((v / ce) & 31);
+    if (!c->d_chunkmap) dmalloc((void **)&c->d_chunkmap, cmap.size() * 4, "chunk bitmap");
+    SV_CUDA(cudaMemcpyAsync(c->d_chunkmap, cmap.data(), cmap.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    SV_CUDA(cudaStreamSynchronize(c->stream));  // loc / map / keys / cmap are freed on return
     c->n_marked = cnt;
     c->has_marked = true;
 }
@@ -336,6 +344,7 @@ void destroy(sv_ctx *c) {
     cudaFree(c->d_marked);
     cudaFree(c->d_tilemap);
     cudaFree(c->d_okeys);
+    cudaFree(c->d_chunkmap);
     cudaFree(c->d_partials);
     cudaFree(c->d_sums);
     cudaFree(c->d_counter);

@@ -124,6 +124,7 @@ struct MeanArgs {
     double inv_total = 0.0;            // 1 / 2^n (global N)
     const uint64_t *marked = nullptr;  // sorted local indices
     uint64_t n_marked = 0;
+    const unsigned int *chunkmap = nullptr;  // bit per mean_chunk_elems() chunk: holds a marked index
     const double *sum_in = nullptr;    // complex sum of (O a) over all ranks
     double *sum_out = nullptr;         // local complex sum of (O a_new)
     double *partials = nullptr;        // 2 * grid doubles
@@ -131,6 +132,7 @@ struct MeanArgs {
 };
 // One wave of blocks (SM count x resident blocks), capped by the work.
 int mean_grid(uint64_t N, sv_dtype dt);
+uint64_t mean_chunk_elems(sv_dtype dt);  // amplitudes per chunk of the mean kernel
 // write = true: fused flip + invert-about-mean + next-sum; false: read-only
 // sum of (O a) (the first mu of an sv_iterate call).
 void launch_mean_grid(sv_dtype dt, const MeanArgs &a, int grid, bool write, cudaStream_t s);
