@@ -218,7 +218,9 @@ sv_status sv_profile_timeline(sv_ctx *ctx, int *kinds, double *ms, uint64_t cap,
 
 /* Tile element index and swizzled shared-memory slot held by thread `tid`,
  * register `reg` in register layout `phase` (0 = A, 1 = B, 2 = C) of the WHT
- * tile kernel for `dtype`.  Returns 0, or -1 for out-of-range arguments. */
+ * tile kernel for `dtype` (SV_C64 / SV_C128: the three-layout family; 2: the
+ * two-layout family of strided complex64 tiles, phases 0-1).  Returns 0, or
+ * -1 for out-of-range arguments. */
 int sv_debug_tile_layout(int dtype, int phase, int tid, int reg, int *tile_elem, int *smem_index);
 /* 1 if layout `phase` runs the butterfly stage of tile bit `bit`, else 0. */
 int sv_debug_tile_owner(int dtype, int phase, int bit);

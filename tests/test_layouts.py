@@ -67,3 +67,38 @@ def test_layout_a_is_coalesced(dtype):
         for j in range(0, 1 << R, step):
             addr = sorted(tab[(32 * w + l, j)][0] * eb for l in range(32))
             assert addr[-1] - addr[0] == 31 * 16 and len(set(addr)) == 32
+
+
+def test_strided_two_layout_family():
+    """Strided complex64 tiles (processed bits [U, 13), U >= 3): two layouts
+    of 8-byte amplitudes -- bijective, each processed bit owned once, carry
+    bits 0..2 never register bits, conflict-free half-warp wavefronts, and
+    layout A's warp loads cover whole 64-byte carry runs."""
+    T, R, eb, D = 13, 5, 8, 2
+    nt, nr = 1 << (T - R), 1 << R
+    e, s = ctypes.c_int(), ctypes.c_int()
+    tabs = []
+    for ph in range(2):
+        tab = {}
+        for t in range(nt):
+            for j in range(nr):
+                assert sv.lib.sv_debug_tile_layout(D, ph, t, j, ctypes.byref(e), ctypes.byref(s)) == 0
+                tab[(t, j)] = (e.value, s.value)
+        assert sorted(v[0] for v in tab.values()) == list(range(1 << T))
+        assert sorted(v[1] for v in tab.values()) == list(range(1 << T))
+        for w in range(nt // 32):
+            for j in range(nr):
+                for q in (0, 16):
+                    banks = []
+                    for l in range(q, q + 16):
+                        byte = tab[(32 * w + l, j)][1] * eb
+                        banks += [(byte // 4) % 32, (byte // 4 + 1) % 32]
+                    assert len(banks) == len(set(banks)), (ph, w, j, q)
+        tabs.append(tab)
+    for b in range(T):
+        owners = sum(sv.lib.sv_debug_tile_owner(D, ph, b) for ph in range(2))
+        assert owners == (1 if b >= 3 else 0)
+    for w in range(nt // 32):  # layout A: lanes 0..7 of a warp = one 64-B run
+        for j in range(nr):
+            elems = sorted(tabs[0][(32 * w + l, j)][0] for l in range(8))
+            assert elems == list(range(elems[0], elems[0] + 8)) and elems[0] % 8 == 0
