@@ -154,6 +154,18 @@ sv_status sv_marked_from_seed(int n, uint64_t m, uint64_t seed, uint64_t *out);
 sv_status sv_info(const sv_ctx *ctx, int *n, int *world, int *rank, uint64_t *local_len,
                   sv_dtype *dtype);
 
+/* Qubit-swap exchange mode (P > 1).  fused = 1: the pass before each swap
+ * stores every amplitude straight into its new owner's buffer -- peer memory
+ * over NVLink mapped with CUDA IPC, or the emulated shard -- and the swap is
+ * a cross-rank barrier (one-integer ncclAllReduce); the reorganisation of
+ * Fig. 8 then costs no extra HBM pass.  fused = 0: ncclAlltoAll
+ * of contiguous chunks into a receive buffer (emulation: device copies).
+ * Default: fused when available (SV_XCHG=nccl in the environment forces 0).
+ * SV_ESTATE if fused is requested but unavailable (1 rank, > 8 ranks, or the
+ * peers' buffers could not be mapped). */
+sv_status sv_set_exchange(sv_ctx *ctx, int fused);
+sv_status sv_get_exchange(const sv_ctx *ctx, int *fused);
+
 /* Block until all work enqueued on the context's stream is done. */
 sv_status sv_synchronize(sv_ctx *ctx);
 

@@ -65,6 +65,8 @@ _SIGS = {
     "sv_info": ([_ctxp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                  ctypes.POINTER(_u64), ctypes.POINTER(_i32)], _i32),
     "sv_synchronize": ([_ctxp], _i32),
+    "sv_set_exchange": ([_ctxp, _i32], _i32),
+    "sv_get_exchange": ([_ctxp, ctypes.POINTER(_i32)], _i32),
     "sv_nccl_unique_id": ([_vp, ctypes.c_size_t], _i32),
     "sv_plan_wht": ([_i32, _i32, _i32, _i32, _i32, ctypes.POINTER(sv_plan_step), _i32, ctypes.POINTER(_i32)], _i32),
     "sv_profile": ([_ctxp, _i32], _i32),
@@ -193,6 +195,16 @@ def sv_marked_from_seed(n: int, m: int, seed: int) -> np.ndarray:
     out = np.empty(m, dtype=np.uint64)
     _check(lib.sv_marked_from_seed(n, m, seed, out.ctypes.data if m else None), "sv_marked_from_seed")
     return out
+
+
+def sv_set_exchange(ctx: Ctx, fused: bool) -> None:
+    _check(lib.sv_set_exchange(ctx.ptr, int(fused)), "sv_set_exchange")
+
+
+def sv_get_exchange(ctx: Ctx) -> bool:
+    v = _i32()
+    _check(lib.sv_get_exchange(ctx.ptr, ctypes.byref(v)), "sv_get_exchange")
+    return bool(v.value)
 
 
 def sv_synchronize(ctx: Ctx) -> None:

@@ -203,6 +203,8 @@ std::vector<Step> schedule_wht(const Plan &plan, int k, bool with_oracle) {
             SV_CHECK(s.group == plan.fwd[0], SV_EINVAL, "internal: oracle fused into a non-O group");
         steps.push_back(s);
     }
+    for (size_t j = 0; j + 1 < steps.size(); ++j)
+        if (steps[j].kind == STEP_PASS && steps[j + 1].kind == STEP_SWAP) steps[j].pre_swap = 1;
     return steps;
 }
 

@@ -46,6 +46,13 @@ struct sv_ctx {
     uint64_t *d_okeys = nullptr;        // sorted (tile id << 16 | element) of the marked entries
     uint64_t okeys_cap = 0;
     unsigned int *d_chunkmap = nullptr; // one bit per mean-kernel chunk (holds a marked index)
+    // fused exchange: peer buffers (own buffers at index rank; CUDA IPC maps
+    // of the other ranks' state / recv), or the emulated shards
+    bool fused_xchg = false;
+    bool xchg_capable = false;
+    void *peer_state[8] = {};
+    void *peer_recv[8] = {};
+    int *d_barrier = nullptr;
     uint64_t n_marked = 0;   // resident (local) marked entries
     bool has_marked = false;
     double *d_partials = nullptr;  // 2 * kMaxGrid
@@ -180,6 +187,17 @@ void exchange(sv_ctx *c) {
     });
 }
 
+// Cross-rank ordering point after a fused exchange pass: every rank's
+// peer stores have landed before anyone reads its buffer.  Real ranks: a
+// one-integer ncclAllReduce on the stream (completes only after every rank's
+// exchange kernel has completed); emulation: stream order is enough.
+void xchg_barrier(sv_ctx *c) {
+    if (c->comm == nullptr) return;
+    run(c, SV_K_EXCHANGE, [&] {
+        SV_NCCL(ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclInt32, ncclSum, c->comm, c->stream));
+    });
+}
+
 void run_wht_schedule(sv_ctx *c, int k, bool with_oracle) {
     if (c->plan.whole) {
         if (with_oracle && k == 0) return;
@@ -191,9 +209,22 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle) {
     }
     const std::vector<Step> steps = schedule_wht(c->plan, k, with_oracle);
     const int total_bits = c->emulated ? c->n : c->plan.nl;
+    // cur = the buffer holding the state.  Unfused: passes write `state`, a
+    // swap is an all-to-all state -> recv.  Fused: the pass before a swap
+    // stores every element straight into its new owner's other buffer
+    // (peer memory over NVLink, or the emulated shard), a swap is only a
+    // barrier; passes after it continue in that buffer.
+    void *cur = c->state;
+    void *next = nullptr;
     for (const Step &s : steps) {
         if (s.kind == STEP_SWAP) {
-            exchange(c);
+            if (c->fused_xchg) {
+                xchg_barrier(c);
+                cur = next;
+            } else {
+                exchange(c);
+                cur = c->recv;
+            }
             continue;
         }
         if (s.kind == STEP_SCATTER) {
@@ -202,8 +233,22 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle) {
             continue;
         }
         PassArgs a;
-        a.in = s.in_recv ? c->recv : c->state;
-        a.out = c->state;
+        a.in = cur;
+        a.out = c->fused_xchg ? cur : c->state;
+        if (c->fused_xchg && s.pre_swap) {
+            const bool to_recv = (cur == c->state);
+            next = to_recv ? c->recv : c->state;
+            a.xchg_nl = c->plan.nl;
+            a.xchg_g = c->g;
+            a.xchg_rank = c->emulated ? -1 : c->rank;
+            for (int j = 0; j < (1 << c->g); ++j) {
+                if (c->emulated)
+                    a.xchg_dst[j] = (char *)next + (size_t)j * c->nl_amps * elem_bytes(c->dt);
+                else
+                    a.xchg_dst[j] = to_recv ? c->peer_recv[j] : c->peer_state[j];
+            }
+        }
+        if (!c->fused_xchg) cur = c->state;
         a.marked = c->d_okeys;  // O-group lookup keys (only read by oracle passes)
         a.n_marked = c->n_marked;
         a.tilemap = c->d_tilemap;
@@ -332,12 +377,74 @@ void store_marked(sv_ctx *c, const uint64_t *marked, uint64_t m) {
 
 void check_ctx(const sv_ctx *c) { SV_CHECK(c != nullptr, SV_EINVAL, "ctx is NULL"); }
 
+// Fused exchange plumbing.  Emulation: the shards are in one buffer.  Real
+// ranks: exchange CUDA IPC handles of every rank's state and receive buffer
+// over the library's own NCCL communicator and map them (NVLink peer access);
+// any failure leaves the NCCL all-to-all path in place.  SV_XCHG=nccl forces
+// the unfused path.
+void setup_peers(sv_ctx *c) {
+    if (c->world <= 1) return;
+    const char *env = getenv("SV_XCHG");
+    const bool want = !(env && strcmp(env, "nccl") == 0);
+    if (c->emulated) {
+        c->xchg_capable = c->world <= 8;
+        c->fused_xchg = want && c->xchg_capable;
+        return;
+    }
+    if (c->comm == nullptr || c->world > 8) return;
+    dmalloc((void **)&c->d_barrier, sizeof(int), "barrier");
+    SV_CUDA(cudaMemsetAsync(c->d_barrier, 0, sizeof(int), c->stream));
+    cudaIpcMemHandle_t h[2];
+    if (cudaIpcGetMemHandle(&h[0], c->state) != cudaSuccess || cudaIpcGetMemHandle(&h[1], c->recv) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    const size_t hb = sizeof(h);
+    char *d_all = nullptr;
+    dmalloc((void **)&d_all, hb * c->world, "ipc handles");
+    std::vector<char> all(hb * c->world);
+    try {
+        SV_CUDA(cudaMemcpyAsync(d_all + hb * c->rank, h, hb, cudaMemcpyHostToDevice, c->stream));
+        SV_NCCL(ncclAllGather(d_all + hb * c->rank, d_all, hb, ncclChar, c->comm, c->stream));
+        SV_CUDA(cudaMemcpyAsync(all.data(), d_all, hb * c->world, cudaMemcpyDeviceToHost, c->stream));
+        SV_CUDA(cudaStreamSynchronize(c->stream));
+    } catch (...) {
+        cudaFree(d_all);
+        throw;
+    }
+    SV_CUDA(cudaFree(d_all));
+    bool ok = true;
+    for (int j = 0; j < c->world; ++j) {
+        if (j == c->rank) {
+            c->peer_state[j] = c->state;
+            c->peer_recv[j] = c->recv;
+            continue;
+        }
+        cudaIpcMemHandle_t pj[2];
+        memcpy(pj, all.data() + hb * j, hb);
+        if (cudaIpcOpenMemHandle(&c->peer_state[j], pj[0], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+            cudaIpcOpenMemHandle(&c->peer_recv[j], pj[1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            ok = false;
+        }
+    }
+    c->xchg_capable = ok;
+    c->fused_xchg = want && ok;
+}
+
 void destroy(sv_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto &p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
     for (auto &p : c->pool) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+    if (!c->emulated)
+        for (int j = 0; j < 8; ++j) {
+            if (j == c->rank) continue;
+            if (c->peer_state[j]) cudaIpcCloseMemHandle(c->peer_state[j]);
+            if (c->peer_recv[j]) cudaIpcCloseMemHandle(c->peer_recv[j]);
+        }
+    cudaFree(c->d_barrier);
     if (c->comm) ncclCommDestroy(c->comm);
     cudaFree(c->state);
     cudaFree(c->recv);
@@ -402,6 +509,7 @@ sv_status sv_init(sv_ctx **out, int n, uint64_t seed, sv_dtype dtype, sv_init_ki
             memcpy(&id, dist->nccl_id, sizeof(id));
             SV_NCCL(ncclCommInitRank(&c->comm, world, id, c->rank));
         }
+        setup_peers(c);
         do_init(c, seed, init);
         *out = c;
     });
@@ -540,6 +648,22 @@ sv_status sv_info(const sv_ctx *c, int *n, int *world, int *rank, uint64_t *loca
         if (rank) *rank = c->rank;
         if (local_len) *local_len = c->nres;
         if (dtype) *dtype = c->dt;
+    });
+}
+
+sv_status sv_set_exchange(sv_ctx *c, int fused) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CHECK(!fused || c->xchg_capable, SV_ESTATE, "fused exchange unavailable (1 rank, > 8 ranks or no peer access)");
+        c->fused_xchg = fused != 0;
+    });
+}
+
+sv_status sv_get_exchange(const sv_ctx *c, int *fused) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CHECK(fused != nullptr, SV_EINVAL, "fused is NULL");
+        *fused = c->fused_xchg ? 1 : 0;
     });
 }
 

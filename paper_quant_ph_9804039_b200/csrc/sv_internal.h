@@ -78,6 +78,7 @@ struct Step {
     int group = -1;
     int pre = 0, mid = MID_NONE, post = 0;
     int in_recv = 0;
+    int pre_swap = 0;   // the next step is a qubit swap (its store can BE the exchange)
 };
 
 struct Plan {
@@ -112,6 +113,12 @@ struct PassArgs {
     uint64_t tile_mask = 0;             // slots of one tile
     uint64_t proc_mask = 0;             // processed slots (subset of tile_mask)
     int total_bits = 0;                 // index bits of the launched buffer
+    // fused qubit-swap exchange: the pass's store sends every element to its
+    // new owner (xchg_nl > 0 enables; see global_store_xchg in wht.cu)
+    int xchg_nl = 0;                    // local index bits per rank
+    int xchg_g = 0;                     // rank bits
+    int xchg_rank = -1;                 // own rank; -1 = emulation (rank = index >> nl)
+    void *xchg_dst[8] = {};             // destination buffer base of each rank
 };
 
 void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s);

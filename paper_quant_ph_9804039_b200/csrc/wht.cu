@@ -159,7 +159,21 @@ struct KParams {
     unsigned int proc;       // processed tile bits
     unsigned long long free_mask;  // slots not in the tile; tile id bits scatter into them
     signed char slot[16];          // tile bit -> slot
+    // fused qubit-swap exchange (global_store_xchg): 0 = plain store
+    int xchg, xnl, xg, xrank;      // local index bits, rank bits, own rank (-1: emulated)
+    void *xdst[8];                 // destination buffer of each rank
 };
+
+// Publish the exchange destinations in shared memory (constant indices only:
+// a runtime-indexed kernel-parameter array would be copied to local memory).
+template <typename E>
+__device__ __forceinline__ void load_xdst(const KParams &p, int tid, E **s_dst) {
+    if (p.xchg) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (tid == i) s_dst[i] = reinterpret_cast<E *>(p.xdst[i]);
+    }
+}
 
 template <typename E>
 __device__ __forceinline__ void bfly(E &x, E &y) {
@@ -342,6 +356,64 @@ __device__ __forceinline__ void global_store(const E (&x)[L::NR], E *g, const KP
     }
 }
 
+// Store that IS the qubit-swap exchange (the paper's reorganisation, Fig. 8,
+// P:4631-4646, fused into the pass that precedes it): element with local
+// index i of rank r belongs to rank j = i's top-g local bits and lands in
+// rank j's destination buffer at r*B + (i mod B), B = N_l / P.  dst[j] is a
+// peer pointer (NVLink, CUDA IPC) on a real multi-GPU run, or rank j's shard
+// of the one buffer in single-GPU emulation (rank r = launched index >> nl).
+template <class L, int PH, typename E>
+__device__ __forceinline__ void global_store_xchg(const E (&x)[L::NR], unsigned long long base, const KParams &p,
+                                                  int tid, E *const *sdst) {
+    const unsigned long long t = base + goff_thr<L, PH>(p, tid);
+    unsigned long long st[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+        if (i < L::kRB) st[i] = 1ull << p.slot[L::reg_bit(PH, i)];
+    const unsigned long long nlm = (1ull << p.xnl) - 1ull;
+    const unsigned long long bm = (1ull << (p.xnl - p.xg)) - 1ull;
+    const unsigned long long pm = (1ull << p.xg) - 1ull;
+    auto dst = [&](unsigned long long idx) {
+        const unsigned long long loc = idx & nlm;
+        const unsigned long long r = p.xrank >= 0 ? (unsigned long long)p.xrank : (idx >> p.xnl);
+        return sdst[(loc >> (p.xnl - p.xg)) & pm] + (r << (p.xnl - p.xg)) + (loc & bm);
+    };
+    if constexpr (L::VE == 2) {
+#pragma unroll
+        for (int v = 0; v < L::NR / 2; ++v) {
+            unsigned long long o = t;
+#pragma unroll
+            for (int i = 1; i < 16; ++i)
+                if (i < L::kRB && (((2 * v) >> i) & 1)) o += st[i];
+            float4 q;
+            q.x = x[2 * v].x; q.y = x[2 * v].y; q.z = x[2 * v + 1].x; q.w = x[2 * v + 1].y;
+            *reinterpret_cast<float4 *>(dst(o)) = q;  // pair (e, e|1) never straddles ranks
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < L::NR; ++j) {
+            unsigned long long o = t;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                if (i < L::kRB && ((j >> i) & 1)) o += st[i];
+            *dst(o) = x[j];
+        }
+    }
+}
+
+// Final store of a pass: plain (in place / to the next pass's buffer) or
+// through the exchange.
+template <class L, int PH, typename E>
+__device__ __forceinline__ void pass_store(const E (&x)[L::NR], E *gout, unsigned long long base, const KParams &p,
+                                           int tid, E *const *sdst) {
+    if (p.xchg) {
+        __syncthreads();  // sdst published (uniform branch)
+        global_store_xchg<L, PH>(x, base, p, tid, sdst);
+    } else {
+        global_store<L, PH>(x, gout, p, tid);
+    }
+}
+
 // Elementwise op between the two stage sets, in register layout PH.
 template <class L, int PH, typename E>
 __device__ __forceinline__ void mid_op(E (&x)[L::NR], const KParams &p, unsigned long long base, int tid,
@@ -417,7 +489,7 @@ __device__ __forceinline__ bool oracle_lookup(const KParams &p, unsigned long lo
 // elementwise op, relayouts through `sm`, and the coalesced global store.
 template <class L, bool PRE, bool POST, int U, typename E>
 __device__ __forceinline__ void tile_body(E (&x)[L::NR], E *sm, const KParams &p, unsigned long long base, E *gout,
-                                          int tid, bool has_marked, const unsigned long long *s_mlo,
+                                          int tid, E *const *sdst, bool has_marked, const unsigned long long *s_mlo,
                                           const unsigned long long *s_mcnt) {
     if (PRE) {
         run_stages<L, 0, U>(x);
@@ -432,9 +504,9 @@ __device__ __forceinline__ void tile_body(E (&x)[L::NR], E *sm, const KParams &p
             run_stages<L, 1, U>(x);
             relayout<L, 1, 0>(x, sm, tid);
             run_stages<L, 0, U>(x);
-            global_store<L, 0>(x, gout, p, tid);
+            pass_store<L, 0>(x, gout, base, p, tid, sdst);
         } else {
-            global_store<L, 2>(x, gout, p, tid);
+            pass_store<L, 2>(x, gout, base, p, tid, sdst);
         }
     } else {
         if (has_marked) __syncthreads();  // s_mlo / s_mcnt (uniform branch)
@@ -445,9 +517,9 @@ __device__ __forceinline__ void tile_body(E (&x)[L::NR], E *sm, const KParams &p
             run_stages<L, 1, U>(x);
             relayout<L, 1, 2>(x, sm, tid);
             run_stages<L, 2, U>(x);
-            global_store<L, 2>(x, gout, p, tid);
+            pass_store<L, 2>(x, gout, base, p, tid, sdst);
         } else {
-            global_store<L, 0>(x, gout, p, tid);
+            pass_store<L, 0>(x, gout, base, p, tid, sdst);
         }
     }
 }
@@ -456,7 +528,7 @@ __device__ __forceinline__ void tile_body(E (&x)[L::NR], E *sm, const KParams &p
 // the op in B, B -> A stages; without processed bits in B it stays in A.
 template <class L, bool PRE, bool POST, int U, typename E>
 __device__ __forceinline__ void tile_body2(E (&x)[L::NR], E *sm, const KParams &p, unsigned long long base, E *gout,
-                                           int tid, bool has_marked, const unsigned long long *s_mlo,
+                                           int tid, E *const *sdst, bool has_marked, const unsigned long long *s_mlo,
                                            const unsigned long long *s_mcnt) {
     constexpr bool kNeedB = U < L::kTB - L::kRB;
     constexpr int kLast = kNeedB ? 1 : 0;
@@ -475,9 +547,9 @@ __device__ __forceinline__ void tile_body2(E (&x)[L::NR], E *sm, const KParams &
                 relayout<L, 1, 0>(x, sm, tid);
                 run_stages<L, 0, U>(x);
             }
-            global_store<L, 0>(x, gout, p, tid);
+            pass_store<L, 0>(x, gout, base, p, tid, sdst);
         } else {
-            global_store<L, kLast>(x, gout, p, tid);
+            pass_store<L, kLast>(x, gout, base, p, tid, sdst);
         }
     } else {
         if (has_marked) __syncthreads();
@@ -489,7 +561,7 @@ __device__ __forceinline__ void tile_body2(E (&x)[L::NR], E *sm, const KParams &
                 run_stages<L, 1, U>(x);
             }
         }
-        global_store<L, POST ? kLast : 0>(x, gout, p, tid);
+        pass_store<L, POST ? kLast : 0>(x, gout, base, p, tid, sdst);
     }
 }
 
@@ -500,12 +572,14 @@ __global__ void __launch_bounds__(1 << (TB - RB), SV_TILE_MIN_BLOCKS) wht_tile2_
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float2 *sm = reinterpret_cast<float2 *>(smem_raw);
     __shared__ unsigned long long s_mlo, s_mcnt;
+    __shared__ float2 *s_dst[8];
+    load_xdst(p, threadIdx.x, s_dst);
     const int tid = threadIdx.x;
     const unsigned long long base = tile_base(blockIdx.x, p.free_mask);
     float2 x[L::NR];
     global_load<L, 0>(x, reinterpret_cast<const float2 *>(p.in) + base, p, tid);
     const bool has_marked = (p.mid == MID_ORACLE) && oracle_lookup(p, blockIdx.x, tid, &s_mlo, &s_mcnt);
-    tile_body2<L, PRE, POST, U>(x, sm, p, base, reinterpret_cast<float2 *>(p.out) + base, tid, has_marked, &s_mlo,
+    tile_body2<L, PRE, POST, U>(x, sm, p, base, reinterpret_cast<float2 *>(p.out) + base, tid, s_dst, has_marked, &s_mlo,
                                 &s_mcnt);
 }
 
@@ -516,12 +590,14 @@ __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB >= 9) ? 1 : SV_TILE_M
     extern __shared__ __align__(16) unsigned char smem_raw[];
     E *sm = reinterpret_cast<E *>(smem_raw);
     __shared__ unsigned long long s_mlo, s_mcnt;
+    __shared__ E *s_dst[8];
+    load_xdst(p, threadIdx.x, s_dst);
     const int tid = threadIdx.x;
     const unsigned long long base = tile_base(blockIdx.x, p.free_mask);
     E x[L::NR];
     global_load<L, 0>(x, reinterpret_cast<const E *>(p.in) + base, p, tid);
     const bool has_marked = (p.mid == MID_ORACLE) && oracle_lookup(p, blockIdx.x, tid, &s_mlo, &s_mcnt);
-    tile_body<L, PRE, POST, U>(x, sm, p, base, reinterpret_cast<E *>(p.out) + base, tid, has_marked, &s_mlo, &s_mcnt);
+    tile_body<L, PRE, POST, U>(x, sm, p, base, reinterpret_cast<E *>(p.out) + base, tid, s_dst, has_marked, &s_mlo, &s_mcnt);
 }
 
 template <typename E, int TB, int RB, bool PRE, bool POST, int U>
@@ -567,6 +643,15 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
     kp.f0_scale = a.f0_scale;
     kp.mid = a.mid;
     kp.has_origin = a.has_origin;
+    kp.xchg = a.xchg_nl > 0 ? 1 : 0;
+    if (kp.xchg) {
+        SV_CHECK(a.xchg_g >= 1 && a.xchg_g <= 3 && a.xchg_nl - a.xchg_g >= 1, SV_EINVAL,
+                 "internal: fused exchange supports 2..8 ranks");
+        kp.xnl = a.xchg_nl;
+        kp.xg = a.xchg_g;
+        kp.xrank = a.xchg_rank;
+        for (int i = 0; i < 8; ++i) kp.xdst[i] = i < (1 << a.xchg_g) ? a.xchg_dst[i] : nullptr;
+    }
     int b = 0, f = 0;
     unsigned int proc = 0;
     kp.free_mask = 0;

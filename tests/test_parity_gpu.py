@@ -272,9 +272,12 @@ def test_c5_semantics_small_gaussian(dtype):
 # --------------------------------------------------------------------------- #
 # sharded schedule, emulated on one GPU                                        #
 # --------------------------------------------------------------------------- #
+@pytest.mark.parametrize("fused", [True, False], ids=["fused-xchg", "alltoall"])
 @pytest.mark.parametrize("dtype", DT, ids=DT_IDS)
 @pytest.mark.parametrize("n,world", [(17, 2), (19, 4), (20, 8), (22, 8), (21, 2)])
-def test_emulated_sharding_matches_oracle(dtype, n, world):
+def test_emulated_sharding_matches_oracle(dtype, n, world, fused):
+    """The sharded schedule on one GPU (P shards in one buffer): qubit swaps as
+    the fused store-to-new-owner pass, or as an all-to-all of chunks."""
     T = 13 if dtype == sv.SV_C64 else 12
     if n - 2 * (world.bit_length() - 1) < T:
         pytest.skip("shard too small")
@@ -283,6 +286,8 @@ def test_emulated_sharding_matches_oracle(dtype, n, world):
     k = 3
     with ctx_with(a, dtype, world=world) as c:
         assert sv.sv_info(c)["world"] == world
+        assert sv.sv_get_exchange(c)  # fused by default in emulation
+        sv.sv_set_exchange(c, fused)
         sv.sv_set_marked(c, marked)
         sv.sv_iterate(c, k, sv.SV_DIFFUSE_WHT)
         got = sv.sv_get_amplitudes(c)

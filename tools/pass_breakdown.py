@@ -37,7 +37,10 @@ def main():
     plan = sv.sv_plan_wht(a.n, a.world, dt, a.k, True)
     agg = collections.OrderedDict()
     it = iter(tl)
+    fused = a.world > 1 and sv.sv_get_exchange(ctx)
     for st in plan:
+        if st["kind"] == 1 and fused:
+            continue  # emulated fused exchange: the swap is inside the preceding pass
         kind, ms = next(it)
         if st["kind"] == 0:
             key = "tile=%#x proc=%#x pre=%d mid=%d post=%d" % (st["tile_mask"], st["proc_mask"], st["pre"], st["mid"],
