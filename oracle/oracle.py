@@ -76,6 +76,11 @@ def lib():
         L.or_norm_sq.restype = ctypes.c_double
         L.or_dense_hadamard.argtypes = [i32, vp]
         L.or_dense_hadamard.restype = i32
+        L.or_noise_delta.argtypes = [u64, u64, i32, i32, ctypes.c_double]
+        L.or_noise_delta.restype = ctypes.c_double
+        L.or_noisy_transform.argtypes = [i32, vp, u64, u64, i32, ctypes.c_double]
+        L.or_f0.argtypes = [i32, vp]
+        L.or_iterate_noisy.argtypes = [i32, vp, vp, u64, i32, ctypes.c_double, u64, u64]
         L.or_reorganize.argtypes = [i32, i32, vp, vp]
         L.or_wht_sharded.argtypes = [i32, i32, vp]
         L.or_wht_sharded.restype = i32
@@ -222,4 +227,25 @@ def reorganize(a: np.ndarray, g: int) -> np.ndarray:
     ptrs = (ctypes.c_void_p * P)(*[a.ctypes.data + r * Nl * a.itemsize for r in range(P)])
     tmp = np.empty_like(a)
     lib().or_reorganize(n, g, ptrs, _ptr(tmp))
+    return a
+
+
+# ---- operational angle errors (NEXT-1; readings G19, G20) ----------------------
+def noise_delta(seed: int, t: int, w: int, q: int, sigma: float) -> float:
+    return float(lib().or_noise_delta(seed, t, w, q, sigma))
+
+
+def noisy_transform(a: np.ndarray, seed: int, t: int, w: int, sigma: float) -> np.ndarray:
+    lib().or_noisy_transform(_nbits(a), _ptr(_state(a)), seed, t, w, sigma)
+    return a
+
+
+def f0(a: np.ndarray) -> np.ndarray:
+    lib().or_f0(_nbits(a), _ptr(_state(a)))
+    return a
+
+
+def iterate_noisy(a: np.ndarray, marked: np.ndarray, k: int, sigma: float, seed: int, t0: int = 0) -> np.ndarray:
+    marked = np.ascontiguousarray(marked, dtype=np.uint64)
+    lib().or_iterate_noisy(_nbits(a), _ptr(_state(a)), _ptr(marked), marked.size, k, sigma, seed, t0)
     return a

@@ -254,6 +254,67 @@ void or_iterate(int n, cplx *a, const uint64_t *marked, uint64_t m, int k,
 }
 
 /* ------------------------------------------------------------------------ */
+/* Operational errors                                  */
+/* ------------------------------------------------------------------------ */
+
+/* "Imperfections in the laser apparatus result in deviations in the angle of
+ * rotation" (section 2.0; operational errors, section 1.4,
+ * P:2609-2614).  Reading G19: every Hadamard of a transform is the
+ * reflection-rotation U(phi) = [[cos phi, sin phi], [sin phi, -cos phi]]
+ * (Fig. 3's [w x; y z] with w = cos, x = y = sin, z = -cos), phi = pi/4 +
+ * delta; ONE delta per (iteration t, transform w in {0,1}, qubit q), i.e. one
+ * laser operation per qubit acting on all V/2 pairs.
+ * Reading G20: delta = sigma * z, z standard normal by Box-Muller from the
+ * counter hash: c = (2t + w) * 64 + q, u_j = ((hash64(key ^ (2c + j)) >> 11)
+ * + 0.5) 2^-53, z = sqrt(-2 ln u_0) cos(2 pi u_1), key = hash64(seed ^ "NOIS").
+ * With unitary (normalised) transforms F0 = 2|0><0| - I carries no 2^-n. */
+#define OR_TAG_NOISE 0x4E4F495300000000ULL /* "NOIS" */
+
+double or_noise_delta(uint64_t seed, uint64_t t, int w, int q, double sigma)
+{
+    uint64_t key = or_hash64(seed ^ OR_TAG_NOISE);
+    uint64_t c = (2ULL * t + (uint64_t)w) * 64ULL + (uint64_t)q;
+    uint64_t h0 = or_hash64(key ^ (2ULL * c));
+    uint64_t h1 = or_hash64(key ^ (2ULL * c + 1ULL));
+    double u0 = ((double)(h0 >> 11) + 0.5) * 0x1.0p-53;
+    double u1 = ((double)(h1 >> 11) + 0.5) * 0x1.0p-53;
+    return sigma * (sqrt(-2.0 * log(u0)) * cos(6.283185307179586 * u1));
+}
+
+/* One noisy transform: for q = 0..n-1 apply U(pi/4 + delta(t, w, q)). */
+void or_noisy_transform(int n, cplx *a, uint64_t seed, uint64_t t, int w, double sigma)
+{
+    int q;
+    for (q = 0; q < n; ++q) {
+        double phi = 0.78539816339744831 + or_noise_delta(seed, t, w, q, sigma);
+        double cs = cos(phi), sn = sin(phi);
+        or_apply_2x2(n, a, q, cs, sn, sn, -cs);
+    }
+}
+
+/* F0 = 2|0><0| - I without scale. */
+void or_f0(int n, cplx *a)
+{
+    uint64_t N = 1ULL << n, i;
+    for (i = 1; i < N; ++i) a[i] = -a[i];
+}
+
+/* k noisy Grover iterations (global iteration numbers t0 .. t0+k-1):
+ * O, noisy transform w = 0, F0, noisy transform w = 1. */
+void or_iterate_noisy(int n, cplx *a, const uint64_t *marked, uint64_t m, int k, double sigma,
+                      uint64_t seed, uint64_t t0)
+{
+    int it;
+    for (it = 0; it < k; ++it) {
+        uint64_t t = t0 + (uint64_t)it;
+        or_oracle_flip(a, marked, m);
+        or_noisy_transform(n, a, seed, t, 0, sigma);
+        or_f0(n, a);
+        or_noisy_transform(n, a, seed, t, 1, sigma);
+    }
+}
+
+/* ------------------------------------------------------------------------ */
 /* Readouts                                                                 */
 /* ------------------------------------------------------------------------ */
 

@@ -318,3 +318,65 @@ def test_reorganisation_moves_fraction_one_minus_inv_p(n, g):
     assert np.array_equal(pos[stay], src[stay])
     # applied twice it is the identity
     np.testing.assert_array_equal(orc.reorganize(b.copy(), g), a)
+
+
+# --------------------------------------------------------------------------- #
+# Operational angle errors (NEXT-1, readings G19/G20)                          #
+# --------------------------------------------------------------------------- #
+def test_noisy_sigma0_is_ideal_grover():
+    """sigma = 0: U(pi/4) is the normalised Hadamard, so the noisy iteration
+    is the ideal one (closed form)."""
+    n, m, k = 10, 1, 25
+    marked = orc.marked_from_seed(n, m, 1)
+    a = orc.iterate_noisy(orc.init_uniform(n), marked, k, 0.0, 7)
+    np.testing.assert_allclose(a, orc.iterate(orc.init_uniform(n), marked, k, orc.WHT), rtol=0, atol=1e-13)
+    assert orc.marked_mass(a, marked) == pytest.approx(cf.p_success_uniform(n, m, k), abs=1e-13)
+
+
+@pytest.mark.parametrize("n", [1, 3, 5])
+def test_noisy_iteration_equals_dense_kron_product(n):
+    """Each noisy transform is the Kronecker product of its n per-qubit 2x2s
+    (qubit q = bit q: kron order q = n-1 ... 0), built with numpy.kron."""
+    N = 1 << n
+    sigma, seed, t0, k = 0.2, 99, 5, 3
+    a0 = crandn(N)
+    a0 /= np.linalg.norm(a0)
+    marked = orc.marked_from_seed(n, max(1, N // 3), 4)
+    O = np.eye(N)
+    O[marked, marked] = -1.0
+    F0 = -np.eye(N)
+    F0[0, 0] = 1.0
+
+    def transform(t, w):
+        M = np.ones((1, 1))
+        for q in reversed(range(n)):
+            phi = math.pi / 4 + orc.noise_delta(seed, t, w, q, sigma)
+            U = np.array([[math.cos(phi), math.sin(phi)], [math.sin(phi), -math.cos(phi)]])
+            M = np.kron(M, U)
+        return M
+
+    ref = a0.copy()
+    for t in range(t0, t0 + k):
+        ref = transform(t, 1) @ F0 @ transform(t, 0) @ O @ ref
+    got = orc.iterate_noisy(a0.copy(), marked, k, sigma, seed, t0)
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-12)
+
+
+def test_noisy_unitary_deterministic_and_noise_statistics():
+    n = 12
+    a0 = orc.init_gaussian(n, 3)
+    marked = orc.marked_from_seed(n, 5, 3)
+    a = orc.iterate_noisy(a0.copy(), marked, 6, 0.3, 11)
+    assert orc.norm_sq(a) == pytest.approx(1.0, abs=1e-12)
+    np.testing.assert_array_equal(orc.iterate_noisy(a0.copy(), marked, 6, 0.3, 11), a)
+    # splitting the iterations across calls with t0 gives the same state
+    b = orc.iterate_noisy(a0.copy(), marked, 2, 0.3, 11, 0)
+    orc.iterate_noisy(b, marked, 4, 0.3, 11, 2)
+    np.testing.assert_array_equal(b, a)
+    z = np.array([orc.noise_delta(5, t, w, q, 1.0) for t in range(256) for w in (0, 1) for q in range(64)])
+    assert abs(z.mean()) < 6 / math.sqrt(z.size) and abs(z.var() - 1) < 6 * math.sqrt(2 / z.size)
+    # more angle error -> further from the ideal state (monotone in expectation)
+    ideal = orc.iterate(a0.copy(), marked, 6, orc.WHT)
+    d = [np.mean([np.linalg.norm(orc.iterate_noisy(a0.copy(), marked, 6, s, sd) - ideal) for sd in range(8)])
+         for s in (1e-3, 1e-2, 1e-1)]
+    assert d[0] < d[1] < d[2]
