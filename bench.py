@@ -36,6 +36,10 @@ CONFIGS = {
            "c4: n=32 complex64 (32 GiB) sharded by top qubits, M=256 seeded, 16 WHT iterations"),
     "c5w": (34, "c64", 1024, 8, "wht", 5, "gaussian", "c5: n=34 complex64 (128 GiB), Gaussian start, M=1024, 8 WHT"),
     "c5m": (34, "c64", 1024, 8, "mean", 5, "gaussian", "c5: n=34 complex64 (128 GiB), Gaussian start, M=1024, 8 mean"),
+    # NEXT-1: operational angle errors (sigma = 0.01 rad per Hadamard), same sizes as c3 / c4
+    "c3n": (28, "c64", 1, 64, "wht-noisy", 3, "uniform", "c3 with angle errors sigma=0.01: n=28 complex64, M=1, 64 iterations"),
+    "c4n": (32, "c64", 256, 16, "wht-noisy", 4, "uniform",
+            "c4 with angle errors sigma=0.01: n=32 complex64, M=256, 16 iterations"),
 }
 METRIC = "grover_amp_updates_per_s"
 UNIT = "amplitude-updates/s"
@@ -183,7 +187,15 @@ def run_ours(args):
     torch.cuda.set_device(local)
     n, dts, M, k, diff, seed, init, desc = CONFIGS[args.config]
     dtype = sv.SV_C64 if dts == "c64" else sv.SV_C128
-    dflag = sv.SV_DIFFUSE_WHT if diff == "wht" else sv.SV_DIFFUSE_MEAN
+    dflag = sv.SV_DIFFUSE_MEAN if diff == "mean" else sv.SV_DIFFUSE_WHT
+    noisy = diff == "wht-noisy"
+    sigma = 0.01
+
+    def iterate():
+        if noisy:
+            sv.sv_iterate_noisy(ctx, k, sigma, seed, 0)
+        else:
+            sv.sv_iterate(ctx, k, dflag)
     ikind = sv.SV_INIT_UNIFORM if init == "uniform" else sv.SV_INIT_GAUSSIAN
     # a dedicated (non-default) stream shared by libsv and the timing events
     stream = torch.cuda.Stream()
@@ -194,7 +206,7 @@ def run_ours(args):
 
     def step():
         sv.sv_reset(ctx, seed, ikind)
-        sv.sv_iterate(ctx, k, dflag)
+        iterate()
 
     for _ in range(args.warmup):
         step()
@@ -222,7 +234,7 @@ def run_ours(args):
     value = N_amp * k * args.steps / (t_ms / 1e3)
 
     # roofline of the dominant kernel: the WHT tile pass (or the mean pass)
-    kname = "wht_tile" if diff == "wht" else "mean"
+    kname = "mean" if diff == "mean" else "wht_tile"
     launches, kms = prof[kname]
     local_bytes = (N_amp // world) * (8 if dtype == sv.SV_C64 else 16)
     algo_bytes = 2 * local_bytes  # one read + one write of the local state per pass
@@ -247,7 +259,7 @@ def run_ours(args):
         host_marked = pinned.numpy().view(np.uint64)
         sv.sv_set_marked(ctx, host_marked)          # H2D copy of the step's input
         sv.sv_reset(ctx, seed, ikind)
-        sv.sv_iterate(ctx, k, dflag)
+        iterate()
         p_success = sv.sv_measure_marked_mass(ctx)  # D2H read of the step's result
     e2e_s = svd.max_over_ranks(time.perf_counter() - t0)
     e2e = {"value": N_amp * k * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(M * 8),

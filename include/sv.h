@@ -124,6 +124,19 @@ sv_status sv_diffuse(sv_ctx *ctx, sv_diffusion diffusion);
  * Errors: SV_EINVAL (k < 0), SV_ESTATE (no marked set was ever given). */
 sv_status sv_iterate(sv_ctx *ctx, int k, sv_diffusion diffusion);
 
+/* k Grover iterations with operational angle errors:
+ * "imperfections in the laser apparatus result in deviations in the angle of
+ * rotation" (section 2.0; section 1.4).  Reading G19:
+ * every Hadamard of the WHT diffusion becomes U(phi) = [[cos phi, sin phi],
+ * [sin phi, -cos phi]] (Fig. 3's [w x; y z]), phi = pi/4 + delta, one delta
+ * per (iteration t, transform w, qubit q) shared by all V/2 pairs of that
+ * qubit; F0 = 2|0><0| - I (no 2^-n: the transforms are unitary); O exact.
+ * Reading G20: delta = sigma * z, z ~ N(0,1) from a counter hash of
+ * (seed, t, w, q); iterations are numbered t0, t0+1, ... so a run can be
+ * split over calls.  sigma = 0 is the ideal iteration (up to rounding).
+ * Errors: SV_EINVAL (k < 0, sigma not in [0, 10)), SV_ESTATE (no marked set). */
+sv_status sv_iterate_noisy(sv_ctx *ctx, int k, double sigma, uint64_t seed, uint64_t t0);
+
 /* p_i = re^2 + im^2 in fp64 ("the probability of each state is defined as the
  * square of this complex amplitude") for the context's resident
  * indices (local shard; whole state in emulation), in local index order.

@@ -57,6 +57,7 @@ _SIGS = {
     "sv_apply_oracle": ([_ctxp, _vp, _u64], _i32),
     "sv_diffuse": ([_ctxp, _i32], _i32),
     "sv_iterate": ([_ctxp, _i32, _i32], _i32),
+    "sv_iterate_noisy": ([_ctxp, _i32, ctypes.c_double, _u64, _u64], _i32),
     "sv_probabilities": ([_ctxp, _vp, _u64, _i32], _i32),
     "sv_measure_marked_mass": ([_ctxp, _dp], _i32),
     "sv_get_amplitudes": ([_ctxp, _vp, _u64, _u64], _i32),
@@ -151,6 +152,10 @@ def sv_diffuse(ctx: Ctx, diffusion: int = SV_DIFFUSE_WHT) -> None:
 
 def sv_iterate(ctx: Ctx, k: int, diffusion: int = SV_DIFFUSE_WHT) -> None:
     _check(lib.sv_iterate(ctx.ptr, k, diffusion), "sv_iterate")
+
+
+def sv_iterate_noisy(ctx: Ctx, k: int, sigma: float, seed: int, t0: int = 0) -> None:
+    _check(lib.sv_iterate_noisy(ctx.ptr, k, sigma, seed, t0), "sv_iterate_noisy")
 
 
 def sv_info(ctx: Ctx) -> dict:

@@ -52,6 +52,17 @@ uint64_t perm_seeded(int n, uint64_t seed, uint64_t x) {
     return x;
 }
 
+// Angle error of qubit q in transform w of iteration t (G20):
+// sigma * sqrt(-2 ln u0) cos(2 pi u1) from the counter hashes of
+// c = (2t + w) * 64 + q under key hash64(seed ^ "NOIS").
+double noise_delta(uint64_t seed, uint64_t t, int w, int q, double sigma) {
+    const uint64_t key = hash64(seed ^ 0x4E4F495300000000ull);
+    const uint64_t c = (2ull * t + (uint64_t)w) * 64ull + (uint64_t)q;
+    const double u0 = ((double)(hash64(key ^ (2ull * c)) >> 11) + 0.5) * 0x1.0p-53;
+    const double u1 = ((double)(hash64(key ^ (2ull * c + 1ull)) >> 11) + 0.5) * 0x1.0p-53;
+    return sigma * (sqrt(-2.0 * log(u0)) * cos(6.283185307179586 * u1));
+}
+
 // Box-Muller on two counter hashes (G8): u = ((h >> 11) + 0.5) 2^-53.
 __device__ __forceinline__ void gauss_draw(uint64_t key, uint64_t i, double &re, double &im) {
     const uint64_t h0 = mix64((key ^ (2ull * i)) + 0x9E3779B97F4A7C15ull);

@@ -124,7 +124,8 @@ namespace {
 enum ItemKind { VISIT, OP, SWAP };
 struct Item {
     ItemKind kind;
-    int arg;  // group index or MidOp
+    int arg;      // group index or MidOp
+    int tr = -1;  // VISIT: transform index within the call (2 x iteration + w)
 };
 }  // namespace
 
@@ -139,23 +140,24 @@ std::vector<Step> schedule_wht(const Plan &plan, int k, bool with_oracle) {
         return steps;
     }
     std::vector<Item> items;
-    auto transform = [&](bool forward) {
+    auto transform = [&](bool forward, int tr) {
         if (forward)
-            for (int gi : plan.fwd) items.push_back(gi < 0 ? Item{SWAP, 0} : Item{VISIT, gi});
+            for (int gi : plan.fwd) items.push_back(gi < 0 ? Item{SWAP, 0} : Item{VISIT, gi, tr});
         else
             for (auto it = plan.fwd.rbegin(); it != plan.fwd.rend(); ++it)
-                items.push_back(*it < 0 ? Item{SWAP, 0} : Item{VISIT, *it});
+                items.push_back(*it < 0 ? Item{SWAP, 0} : Item{VISIT, *it, tr});
     };
     int reps = with_oracle ? k : 1;
     for (int it = 0; it < reps; ++it) {
         if (with_oracle) items.push_back({OP, MID_ORACLE});
-        transform(true);
+        transform(true, 2 * it);
         items.push_back({OP, MID_F0});
-        transform(false);
+        transform(false, 2 * it + 1);
     }
     // Fuse: visit(G) op visit(G) -> one pass; op visit(G) / visit(G) op at the
     // ends -> one pass; everything else one pass per visit.
     bool after_swap = false;
+    int layout = 0;
     size_t i = 0, L = items.size();
     while (i < L) {
         Step s;
@@ -164,19 +166,23 @@ std::vector<Step> schedule_wht(const Plan &plan, int k, bool with_oracle) {
             s.kind = STEP_SWAP;
             steps.push_back(s);
             after_swap = true;
+            layout ^= 1;
             ++i;
             continue;
         }
         s.kind = STEP_PASS;
         s.in_recv = after_swap ? 1 : 0;
+        s.layout = layout;
         after_swap = false;
         if (a.kind == VISIT) {
             s.group = a.arg;
             s.pre = 1;
+            s.tr_pre = a.tr;
             if (i + 2 < L && items[i + 1].kind == OP && items[i + 2].kind == VISIT &&
                 items[i + 2].arg == a.arg) {
                 s.mid = items[i + 1].arg;
                 s.post = 1;
+                s.tr_post = items[i + 2].tr;
                 i += 3;
             } else if (i + 1 < L && items[i + 1].kind == OP &&
                        (i + 2 == L || items[i + 2].kind != VISIT)) {
@@ -190,6 +196,7 @@ std::vector<Step> schedule_wht(const Plan &plan, int k, bool with_oracle) {
                 s.group = items[i + 1].arg;
                 s.mid = a.arg;
                 s.post = 1;
+                s.tr_post = items[i + 1].tr;
                 i += 2;
             } else {
                 s.kind = STEP_SCATTER;

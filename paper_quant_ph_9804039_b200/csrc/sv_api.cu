@@ -53,6 +53,8 @@ struct sv_ctx {
     void *peer_state[8] = {};
     void *peer_recv[8] = {};
     int *d_barrier = nullptr;
+    double *d_coefs = nullptr;          // angle-error coefficients of the one-CTA kernel
+    size_t coefs_cap = 0;
     uint64_t n_marked = 0;   // resident (local) marked entries
     bool has_marked = false;
     double *d_partials = nullptr;  // 2 * kMaxGrid
@@ -198,12 +200,44 @@ void xchg_barrier(sv_ctx *c) {
     });
 }
 
-void run_wht_schedule(sv_ctx *c, int k, bool with_oracle) {
+// Operational angle errors (NEXT-1, G19/G20): iteration numbers t0 ..
+struct Noise {
+    double sigma;
+    uint64_t seed;
+    uint64_t t0;
+};
+
+// (cos, sin) of U(pi/4 + delta) for logical qubit q in transform tr of the call
+static void noisy_coef(const Noise &nz, int tr, int q, double out[2]) {
+    const double phi = 0.78539816339744831 + noise_delta(nz.seed, nz.t0 + (uint64_t)(tr / 2), tr % 2, q, nz.sigma);
+    out[0] = cos(phi);
+    out[1] = sin(phi);
+}
+
+void run_wht_schedule(sv_ctx *c, int k, bool with_oracle, const Noise *noise = nullptr) {
     if (c->plan.whole) {
         if (with_oracle && k == 0) return;
+        const int reps = with_oracle ? k : 1;
+        const double *coefs = nullptr;
+        if (noise) {  // per (iteration, transform, qubit) coefficients for the one-CTA kernel
+            std::vector<double> h((size_t)reps * 2 * c->n * 2);
+            for (int it = 0; it < reps; ++it)
+                for (int w = 0; w < 2; ++w)
+                    for (int q = 0; q < c->n; ++q) noisy_coef(*noise, 2 * it + w, q, &h[((size_t)(2 * it + w) * c->n + q) * 2]);
+            if (h.size() > c->coefs_cap) {
+                if (c->d_coefs) SV_CUDA(cudaFree(c->d_coefs));
+                c->d_coefs = nullptr;
+                c->coefs_cap = 0;
+                dmalloc((void **)&c->d_coefs, h.size() * sizeof(double), "angle-error coefficients");
+                c->coefs_cap = h.size();
+            }
+            SV_CUDA(cudaMemcpyAsync(c->d_coefs, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+            SV_CUDA(cudaStreamSynchronize(c->stream));
+            coefs = c->d_coefs;
+        }
         run(c, SV_K_WHT_WHOLE, [&] {
-            launch_whole_state(c->dt, c->state, c->n, with_oracle ? k : 1, with_oracle ? 1 : 0, SV_DIFFUSE_WHT,
-                               c->d_marked, c->n_marked, c->stream);
+            launch_whole_state(c->dt, c->state, c->n, reps, with_oracle ? 1 : 0, SV_DIFFUSE_WHT, c->d_marked,
+                               c->n_marked, c->stream, coefs);
         });
         return;
     }
@@ -252,7 +286,20 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle) {
         a.marked = c->d_okeys;  // O-group lookup keys (only read by oracle passes)
         a.n_marked = c->n_marked;
         a.tilemap = c->d_tilemap;
-        a.f0_scale = ldexp(1.0, -c->n);
+        a.f0_scale = noise ? 1.0 : ldexp(1.0, -c->n);  // unitary transforms carry no 2^-n
+        if (noise) {
+            a.noisy = 1;
+            const uint64_t proc = c->plan.groups[s.group].proc;
+            const int u0 = c->plan.nl - c->g;  // first top-g local slot
+            for (int sl = 0; sl < 64; ++sl) {
+                if (!((proc >> sl) & 1)) continue;
+                // logical qubit of this slot: in the swapped layout the top-g
+                // local slots hold the rank qubits nl .. n-1
+                const int q = (s.layout == 1 && sl >= u0) ? c->plan.nl + (sl - u0) : sl;
+                if (s.pre) noisy_coef(*noise, s.tr_pre, q, a.coef[0][sl]);
+                if (s.post) noisy_coef(*noise, s.tr_post, q, a.coef[1][sl]);
+            }
+        }
         a.mid = s.mid;
         a.has_origin = origin_here(c) ? 1 : 0;
         a.pre = s.pre;
@@ -445,6 +492,7 @@ void destroy(sv_ctx *c) {
             if (c->peer_recv[j]) cudaIpcCloseMemHandle(c->peer_recv[j]);
         }
     cudaFree(c->d_barrier);
+    cudaFree(c->d_coefs);
     if (c->comm) ncclCommDestroy(c->comm);
     cudaFree(c->state);
     cudaFree(c->recv);
@@ -552,6 +600,19 @@ sv_status sv_diffuse(sv_ctx *c, sv_diffusion d) {
         if (d == SV_DIFFUSE_WHT) run_wht_schedule(c, 1, false);
         else if (d == SV_DIFFUSE_MEAN) run_mean(c, 1, false);
         else throw Error{SV_EINVAL, "unknown diffusion"};
+    });
+}
+
+sv_status sv_iterate_noisy(sv_ctx *c, int k, double sigma, uint64_t seed, uint64_t t0) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CHECK(k >= 0, SV_EINVAL, "k must be >= 0");
+        SV_CHECK(sigma >= 0.0 && sigma < 10.0, SV_EINVAL, "sigma must be in [0, 10)");
+        SV_CHECK(c->n <= 64, SV_EINVAL, "internal: qubit index range");
+        SV_CHECK(c->has_marked, SV_ESTATE, "sv_iterate_noisy before any marked set");
+        SV_CUDA(cudaSetDevice(c->device));
+        const Noise nz{sigma, seed, t0};
+        run_wht_schedule(c, k, true, &nz);
     });
 }
 

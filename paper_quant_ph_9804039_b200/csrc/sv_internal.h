@@ -79,6 +79,9 @@ struct Step {
     int pre = 0, mid = MID_NONE, post = 0;
     int in_recv = 0;
     int pre_swap = 0;   // the next step is a qubit swap (its store can BE the exchange)
+    int tr_pre = -1;    // transform (2 x iteration + w, within the call) of the pre stages
+    int tr_post = -1;   // ... of the post stages
+    int layout = 0;     // 0 = natural; 1 = top-g local slots hold the rank qubits
 };
 
 struct Plan {
@@ -119,11 +122,15 @@ struct PassArgs {
     int xchg_g = 0;                     // rank bits
     int xchg_rank = -1;                 // own rank; -1 = emulation (rank = index >> nl)
     void *xchg_dst[8] = {};             // destination buffer base of each rank
+    // angle-error stages (NEXT-1): coef[half][slot] = (cos, sin) of U(phi)
+    // for the stages before (half 0) / after (half 1) the elementwise op
+    int noisy = 0;
+    double coef[2][64][2] = {};
 };
 
 void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s);
 void launch_whole_state(sv_dtype dt, void *state, int n, int k, int with_oracle, int diffusion,
-                        const uint64_t *marked, uint64_t m, cudaStream_t s);
+                        const uint64_t *marked, uint64_t m, cudaStream_t s, const double *coefs = nullptr);
 
 struct MeanArgs {
     void *a = nullptr;
@@ -162,5 +169,7 @@ uint64_t splitmix64_next(uint64_t &state);
 uint64_t hash64(uint64_t x);
 uint64_t gauss_key(uint64_t seed);
 uint64_t perm_seeded(int n, uint64_t seed, uint64_t x);
+// Angle error of qubit q in transform w of iteration t (G20).
+double noise_delta(uint64_t seed, uint64_t t, int w, int q, double sigma);
 
 }  // namespace sv
