@@ -159,7 +159,10 @@ def run_reference(args):
     for i in range(args.warmup + args.steps):
         a = orc.init_uniform(n_s)
         t0 = time.perf_counter()
-        orc.iterate(a, marked, k_s, orc.WHT if diff == "wht" else orc.MEAN)
+        if diff == "wht-noisy":
+            orc.iterate_noisy(a, marked, k_s, 0.01, seed, 0)
+        else:
+            orc.iterate(a, marked, k_s, orc.MEAN if diff == "mean" else orc.WHT)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
