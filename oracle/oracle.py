@@ -81,6 +81,9 @@ def lib():
         L.or_noisy_transform.argtypes = [i32, vp, u64, u64, i32, ctypes.c_double]
         L.or_f0.argtypes = [i32, vp]
         L.or_iterate_noisy.argtypes = [i32, vp, vp, u64, i32, ctypes.c_double, u64, u64]
+        L.or_sample_uniform.argtypes = [u64, u64]
+        L.or_sample_uniform.restype = ctypes.c_double
+        L.or_sample.argtypes = [i32, vp, u64, u64, vp, vp]
         L.or_reorganize.argtypes = [i32, i32, vp, vp]
         L.or_wht_sharded.argtypes = [i32, i32, vp]
         L.or_wht_sharded.restype = i32
@@ -200,6 +203,18 @@ def probabilities(a: np.ndarray) -> np.ndarray:
 def marked_mass(a: np.ndarray, marked: np.ndarray) -> float:
     marked = np.ascontiguousarray(marked, dtype=np.uint64)
     return float(lib().or_marked_mass(_ptr(_state(a)), _ptr(marked), marked.size))
+
+
+def sample_uniform(seed: int, s: int) -> float:
+    return float(lib().or_sample_uniform(seed, s))
+
+
+def sample(a: np.ndarray, shots: int, seed: int) -> tuple[np.ndarray, np.ndarray]:
+    """Seeded whole-register measurement (G21): (indices, inclusive CDF)."""
+    out = np.empty(shots, dtype=np.uint64)
+    cdf = np.empty(a.size, dtype=np.float64)
+    lib().or_sample(_nbits(a), _ptr(_state(a)), shots, seed, _ptr(out), _ptr(cdf))
+    return out, cdf
 
 
 def norm_sq(a: np.ndarray) -> float:

@@ -326,6 +326,42 @@ void or_probabilities(int n, const cplx *a, double *p)
     for (i = 0; i < N; ++i) p[i] = creal(a[i]) * creal(a[i]) + cimag(a[i]) * cimag(a[i]);
 }
 
+/* Seeded measurement of the whole register.  "This
+ * measurement operation forces the state to one of the two values ... we must
+ * describe the possible states ... in terms of their probability of
+ * occurrence", probability = |a|^2.  Reading G21:
+ * shot s draws u_s = ((hash64(key ^ s) >> 11) + 0.5) 2^-53, key =
+ * hash64(seed ^ "SAMP"), and returns the smallest index i whose inclusive
+ * cumulative probability C_i exceeds u_s * C_{N-1} (inverse CDF, normalised
+ * by the total so a norm drift cannot push u past the end). */
+#define OR_TAG_SAMPLE 0x53414D5000000000ULL /* "SAMP" */
+
+double or_sample_uniform(uint64_t seed, uint64_t s)
+{
+    uint64_t key = or_hash64(seed ^ OR_TAG_SAMPLE);
+    return ((double)(or_hash64(key ^ s) >> 11) + 0.5) * 0x1.0p-53;
+}
+
+/* cdf (N entries, caller-owned) receives the inclusive prefix sums. */
+void or_sample(int n, const cplx *a, uint64_t shots, uint64_t seed, uint64_t *out, double *cdf)
+{
+    uint64_t N = 1ULL << n, i, s;
+    long double acc = 0.0L;
+    for (i = 0; i < N; ++i) {
+        acc += (long double)(creal(a[i]) * creal(a[i]) + cimag(a[i]) * cimag(a[i]));
+        cdf[i] = (double)acc;
+    }
+    for (s = 0; s < shots; ++s) {
+        double target = or_sample_uniform(seed, s) * cdf[N - 1];
+        uint64_t lo = 0, hi = N - 1;   /* smallest i with cdf[i] > target */
+        while (lo < hi) {
+            uint64_t md = (lo + hi) >> 1;
+            if (cdf[md] > target) hi = md; else lo = md + 1;
+        }
+        out[s] = lo;
+    }
+}
+
 double or_marked_mass(const cplx *a, const uint64_t *marked, uint64_t m)
 {
     long double s = 0.0L;

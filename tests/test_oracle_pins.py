@@ -321,6 +321,54 @@ def test_reorganisation_moves_fraction_one_minus_inv_p(n, g):
 
 
 # --------------------------------------------------------------------------- #
+# Seeded measurement (NEXT-3, reading G21)                                     #
+# --------------------------------------------------------------------------- #
+def test_sample_fig1_superposition_and_basis_state():
+    """Fig. 1(b): the 1-qubit superposition measures 0 or 1 with probability
+    1/2 each -> index 0 exactly when u < 1/2; a basis state
+    always measures its own index."""
+    shots = 4096
+    idx, _ = orc.sample(orc.init_uniform(1), shots, 3)
+    u = np.array([orc.sample_uniform(3, s) for s in range(shots)])
+    np.testing.assert_array_equal(idx, (u >= 0.5).astype(np.uint64))
+    assert abs(idx.mean() - 0.5) < 6 * 0.5 / math.sqrt(shots)
+    a = np.zeros(1 << 7, np.complex128)
+    a[77] = 1j
+    idx, _ = orc.sample(a, 100, 1)
+    assert set(idx.tolist()) == {77}
+
+
+def test_sample_is_numpy_inverse_cdf():
+    """Inverse CDF with numpy's cumsum + searchsorted (library routines)."""
+    n, shots, seed = 9, 20000, 11
+    a = crandn(1 << n)
+    a /= np.linalg.norm(a)
+    idx, cdf = orc.sample(a, shots, seed)
+    p = np.abs(a) ** 2
+    c = np.cumsum(p)
+    np.testing.assert_allclose(cdf, c, rtol=0, atol=1e-14)
+    u = np.array([orc.sample_uniform(seed, s) for s in range(shots)])
+    ref = np.searchsorted(c, u * c[-1], side="right")
+    bad = np.nonzero(idx != ref)[0]
+    for s in bad:  # only a rounding-level boundary may differ
+        assert abs(c[min(idx[s], ref[s])] - u[s] * c[-1]) < 1e-14
+    # frequencies follow |a|^2 (chi-square, 6-sigma bound on the statistic)
+    counts = np.bincount(idx.astype(np.int64), minlength=1 << n)
+    expected = p * shots
+    chi2 = np.sum((counts - expected) ** 2 / expected)
+    dof = (1 << n) - 1
+    assert chi2 < dof + 6 * math.sqrt(2 * dof)
+
+
+def test_sample_grover_state_finds_the_marked_index():
+    n, m = 10, 1
+    marked = orc.marked_from_seed(n, m, 1)
+    a = orc.iterate(orc.init_uniform(n), marked, cf.optimal_iterations(n, m), orc.WHT)
+    idx, _ = orc.sample(a, 10000, 2)
+    assert np.mean(idx == marked[0]) > 0.998  # P_success = 0.99946
+
+
+# --------------------------------------------------------------------------- #
 # Operational angle errors (NEXT-1, readings G19/G20)                          #
 # --------------------------------------------------------------------------- #
 def test_noisy_sigma0_is_ideal_grover():
