@@ -145,6 +145,17 @@ sv_status sv_iterate_noisy(sv_ctx *ctx, int k, double sigma, uint64_t seed, uint
  *   SV_ETOOBIG above). */
 sv_status sv_probabilities(sv_ctx *ctx, double *out, uint64_t len, int out_on_device);
 
+/* Seeded measurement of the whole register, `shots` times, without collapsing
+ * the state: "this measurement operation forces the state
+ * to one of the two values ... in terms of their probability of occurrence"
+ * (P:2273-2276), probability |a_i|^2.  Reading G21: shot s uses
+ * u_s = ((SplitMix64(key ^ s) >> 11) + 0.5) 2^-53, key = SplitMix64(seed ^
+ * "SAMP"), and returns the smallest GLOBAL index whose inclusive cumulative
+ * probability exceeds u_s times the total (fp64, fixed summation order:
+ * deterministic).  out: shots indices (host, guarded at 2^26, or device);
+ * identical on every rank.  Errors: SV_EINVAL (out NULL), SV_ETOOBIG. */
+sv_status sv_sample(sv_ctx *ctx, uint64_t shots, uint64_t seed, uint64_t *out, int out_on_device);
+
 /* out (host) = sum over the marked set of |a_m|^2, fp64, allreduced over
  * ranks (identical on every rank).  SV_ESTATE if no marked set. */
 sv_status sv_measure_marked_mass(sv_ctx *ctx, double *out);

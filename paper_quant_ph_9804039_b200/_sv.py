@@ -60,6 +60,7 @@ _SIGS = {
     "sv_iterate_noisy": ([_ctxp, _i32, ctypes.c_double, _u64, _u64], _i32),
     "sv_probabilities": ([_ctxp, _vp, _u64, _i32], _i32),
     "sv_measure_marked_mass": ([_ctxp, _dp], _i32),
+    "sv_sample": ([_ctxp, _u64, _u64, _vp, _i32], _i32),
     "sv_get_amplitudes": ([_ctxp, _vp, _u64, _u64], _i32),
     "sv_set_amplitudes": ([_ctxp, _vp, _u64, _u64], _i32),
     "sv_marked_from_seed": ([_i32, _u64, _u64, _vp], _i32),
@@ -175,6 +176,16 @@ def sv_probabilities(ctx: Ctx, out_device_ptr: int | None = None, length: int | 
     p = np.empty(ll, dtype=np.float64)
     _check(lib.sv_probabilities(ctx.ptr, p.ctypes.data, ll, 0), "sv_probabilities")
     return p
+
+
+def sv_sample(ctx: Ctx, shots: int, seed: int, out_device_ptr: int | None = None) -> np.ndarray | None:
+    """Seeded whole-register measurement (G21): `shots` global indices."""
+    if out_device_ptr is not None:
+        _check(lib.sv_sample(ctx.ptr, shots, seed, out_device_ptr, 1), "sv_sample")
+        return None
+    out = np.empty(shots, dtype=np.uint64)
+    _check(lib.sv_sample(ctx.ptr, shots, seed, out.ctypes.data if shots else None, 0), "sv_sample")
+    return out
 
 
 def sv_measure_marked_mass(ctx: Ctx) -> float:

@@ -1,0 +1,177 @@
+// sample.cu -- seeded whole-register measurement on the device (SURVEY 8(f)
+// NEXT-3).  "This measurement operation forces the state to one of the two
+// values" with "the probability of each state ... the square of this complex
+// amplitude".  Reading G21: shot s draws u_s from a counter hash
+// and returns the smallest index whose inclusive cumulative probability
+// exceeds u_s times the total.
+//
+// Device plan (three launches, fp64, fixed order => deterministic):
+//   1. chunk_sum_kernel: one warp per 4096-amplitude chunk, 128 rows of 32
+//      lanes, row sums by a fixed xor-butterfly, accumulated in row order
+//      (HBM-bound read of the state);
+//   2. chunk_scan_kernel: one block, exclusive prefix of the chunk sums;
+//   3. sample_kernel: one warp per shot, binary search over the chunk
+//      prefixes, then the chunk's rows in the SAME order as kernel 1 until the
+//      running sum passes the target; the crossing lane comes from an
+//      inclusive warp scan of the row.
+#include <cuda_runtime.h>
+
+#include "sv_internal.h"
+
+namespace sv {
+
+constexpr int kSampChunk = 4096;  // amplitudes per chunk
+constexpr int kRows = kSampChunk / 32;
+
+__device__ __forceinline__ uint64_t smix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+template <typename E>
+__device__ __forceinline__ double prob(const E *a, uint64_t i, uint64_t N) {
+    if (i >= N) return 0.0;
+    const E v = a[i];
+    const double re = (double)v.x, im = (double)v.y;
+    return __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+}
+
+__device__ __forceinline__ double warp_xor_sum(double v) {
+    for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+template <typename E>
+__global__ void __launch_bounds__(256) chunk_sum_kernel(const E *a, uint64_t N, double *sums, uint64_t nchunks) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t wpb = blockDim.x / 32;
+    for (uint64_t c = blockIdx.x * wpb + threadIdx.x / 32; c < nchunks; c += (uint64_t)gridDim.x * wpb) {
+        double acc = 0.0;
+        const uint64_t base = c * kSampChunk;
+        for (int r = 0; r < kRows; ++r) acc = __dadd_rn(acc, warp_xor_sum(prob(a, base + r * 32 + lane, N)));
+        if (lane == 0) sums[c] = acc;
+    }
+}
+
+// In place: sums -> exclusive prefix; total -> *total.  1024 threads, each a
+// contiguous segment (sequential), then a sequential scan of the 1024
+// segment totals by thread 0.
+__global__ void __launch_bounds__(1024) chunk_scan_kernel(double *sums, uint64_t nchunks, double *total) {
+    __shared__ double seg[1024];
+    const uint64_t per = (nchunks + blockDim.x - 1) / blockDim.x;
+    const uint64_t lo = threadIdx.x * per, hi = lo + per < nchunks ? lo + per : nchunks;
+    double s = 0.0;
+    for (uint64_t i = lo; i < hi; ++i) s = __dadd_rn(s, sums[i]);
+    seg[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double run = 0.0;
+        for (unsigned t = 0; t < blockDim.x; ++t) {
+            const double v = seg[t];
+            seg[t] = run;
+            run = __dadd_rn(run, v);
+        }
+        *total = run;
+    }
+    __syncthreads();
+    double run = seg[threadIdx.x];
+    for (uint64_t i = lo; i < hi; ++i) {
+        const double v = sums[i];
+        sums[i] = run;
+        run = __dadd_rn(run, v);
+    }
+}
+
+// g = {global total, this rank's cumulative offset, this rank's total}: a
+// shot whose target falls outside [offset, offset + total) belongs to another
+// rank and is written as 0 (the host then sums the lists over ranks).
+__global__ void rank_window_kernel(const double *totals, int world, int rank, double *g) {
+    double all = 0.0, off = 0.0;
+    for (int r = 0; r < world; ++r) {
+        if (r == rank) off = all;
+        all = __dadd_rn(all, totals[r]);
+    }
+    g[0] = all;
+    g[1] = off;
+    g[2] = totals[rank];
+}
+
+template <typename E>
+__global__ void __launch_bounds__(256) sample_kernel(const E *a, uint64_t N, const double *prefix, uint64_t nchunks,
+                                                     const double *g, uint64_t key, uint64_t shots,
+                                                     uint64_t index_base, int last_rank, uint64_t *out) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t wpb = blockDim.x / 32;
+    for (uint64_t s = blockIdx.x * wpb + threadIdx.x / 32; s < shots; s += (uint64_t)gridDim.x * wpb) {
+        const double u = ((double)(smix64((key ^ s) + 0x9E3779B97F4A7C15ull) >> 11) + 0.5) * 0x1.0p-53;
+        const double target = __dsub_rn(u * g[0], g[1]);
+        if (target < 0.0 || (!last_rank && target >= g[2])) {
+            if (lane == 0) out[s] = 0;  // another rank's shot
+            continue;
+        }
+        // last chunk whose exclusive prefix is <= target
+        uint64_t lo = 0, hi = nchunks - 1;
+        while (lo < hi) {
+            const uint64_t md = (lo + hi + 1) >> 1;
+            if (prefix[md] <= target) lo = md; else hi = md - 1;
+        }
+        const uint64_t base = lo * kSampChunk;
+        double run = prefix[lo];
+        uint64_t pick = (base + kSampChunk <= N ? base + kSampChunk : N) - 1;
+        uint64_t last_nz = base;
+        for (int r = 0; r < kRows; ++r) {
+            const uint64_t i = base + r * 32 + lane;
+            const double p = prob(a, i, N);
+            const double row = warp_xor_sum(p);
+            const unsigned nzm = __ballot_sync(0xffffffffu, p > 0.0);
+            if (nzm) last_nz = base + r * 32 + (31 - __clz(nzm));
+            if (__dadd_rn(run, row) > target) {
+                double inc = p;  // inclusive scan of the row (fixed order)
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double v = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc = __dadd_rn(inc, v);
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, __dadd_rn(run, inc) > target && p > 0.0);
+                pick = m ? base + r * 32 + (__ffs(m) - 1) : last_nz;
+                break;
+            }
+            run = __dadd_rn(run, row);
+            if (r == kRows - 1) pick = last_nz;  // rounding: target sits on the chunk's upper edge
+        }
+        if (lane == 0) out[s] = index_base + pick;
+    }
+}
+
+uint64_t sample_chunks(uint64_t N) { return (N + kSampChunk - 1) / kSampChunk; }
+
+void launch_sample_prefix(sv_dtype dt, const void *a, uint64_t N, double *scratch, double *rank_total,
+                          cudaStream_t s) {
+    const uint64_t nch = sample_chunks(N);
+    const unsigned g1 = (unsigned)((nch + 7) / 8 < 148 * 64 ? (nch + 7) / 8 : 148 * 64);
+    if (dt == SV_C64) chunk_sum_kernel<float2><<<g1, 256, 0, s>>>((const float2 *)a, N, scratch, nch);
+    else chunk_sum_kernel<double2><<<g1, 256, 0, s>>>((const double2 *)a, N, scratch, nch);
+    SV_CUDA(cudaGetLastError());
+    chunk_scan_kernel<<<1, 1024, 0, s>>>(scratch, nch, rank_total);
+    SV_CUDA(cudaGetLastError());
+}
+
+void launch_sample_draw(sv_dtype dt, const void *a, uint64_t N, const double *scratch, const double *totals,
+                        int world, int rank, double *g, uint64_t key, uint64_t shots, uint64_t index_base,
+                        uint64_t *out, cudaStream_t s) {
+    rank_window_kernel<<<1, 1, 0, s>>>(totals, world, rank, g);
+    SV_CUDA(cudaGetLastError());
+    if (shots == 0) return;
+    const uint64_t nch = sample_chunks(N);
+    const unsigned g3 = (unsigned)((shots + 7) / 8 < 148 * 64 ? (shots + 7) / 8 : 148 * 64);
+    const int last = rank == world - 1 ? 1 : 0;
+    if (dt == SV_C64)
+        sample_kernel<float2><<<g3, 256, 0, s>>>((const float2 *)a, N, scratch, nch, g, key, shots, index_base, last,
+                                                 out);
+    else
+        sample_kernel<double2><<<g3, 256, 0, s>>>((const double2 *)a, N, scratch, nch, g, key, shots, index_base,
+                                                  last, out);
+    SV_CUDA(cudaGetLastError());
+}
+
+}  // namespace sv

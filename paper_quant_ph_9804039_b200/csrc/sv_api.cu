@@ -55,6 +55,9 @@ struct sv_ctx {
     int *d_barrier = nullptr;
     double *d_coefs = nullptr;          // angle-error coefficients of the one-CTA kernel
     size_t coefs_cap = 0;
+    double *d_samp = nullptr;           // sampler: chunk prefixes + rank totals + window
+    uint64_t *d_shots = nullptr;        // sampler: device output for host-returning calls
+    uint64_t shots_cap = 0;
     uint64_t n_marked = 0;   // resident (local) marked entries
     bool has_marked = false;
     double *d_partials = nullptr;  // 2 * kMaxGrid
@@ -493,6 +496,8 @@ void destroy(sv_ctx *c) {
         }
     cudaFree(c->d_barrier);
     cudaFree(c->d_coefs);
+    cudaFree(c->d_samp);
+    cudaFree(c->d_shots);
     if (c->comm) ncclCommDestroy(c->comm);
     cudaFree(c->state);
     cudaFree(c->recv);
@@ -650,6 +655,55 @@ sv_status sv_probabilities(sv_ctx *c, double *out, uint64_t len, int on_device) 
             throw;
         }
         SV_CUDA(cudaFree(tmp));
+    });
+}
+
+sv_status sv_sample(sv_ctx *c, uint64_t shots, uint64_t seed, uint64_t *out, int out_on_device) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CHECK(out != nullptr || shots == 0, SV_EINVAL, "out is NULL");
+        SV_CHECK(out_on_device || shots <= (1ull << 26), SV_ETOOBIG, "host sample list above 2^26 shots");
+        SV_CUDA(cudaSetDevice(c->device));
+        const uint64_t nch = sample_chunks(c->nres);
+        const int world = c->comm ? c->world : 1;
+        const int rank = c->comm ? c->rank : 0;
+        if (!c->d_samp) dmalloc((void **)&c->d_samp, (nch + 8 + 3) * sizeof(double), "sampler scratch");
+        double *totals = c->d_samp + nch;  // [world]
+        double *g = totals + 8;             // window {global total, offset, rank total}
+        uint64_t *dout = out;
+        if (!out_on_device) {
+            if (shots > c->shots_cap) {
+                if (c->d_shots) SV_CUDA(cudaFree(c->d_shots));
+                c->d_shots = nullptr;
+                c->shots_cap = 0;
+                dmalloc((void **)&c->d_shots, std::max<uint64_t>(shots, 1) * 8, "sample list");
+                c->shots_cap = shots;
+            }
+            dout = c->d_shots;
+        }
+        const uint64_t key = hash64(seed ^ 0x53414D5000000000ull);  // "SAMP" (G21)
+        run(c, SV_K_READOUT, [&] {
+            launch_sample_prefix(c->dt, c->state, c->nres, c->d_samp, totals + rank, c->stream);
+        });
+        if (c->comm) {  // every rank's total, in rank order
+            run(c, SV_K_ALLREDUCE, [&] {
+                SV_NCCL(ncclAllGather(totals + rank, totals, 1, ncclFloat64, c->comm, c->stream));
+            });
+        }
+        const uint64_t base = c->comm ? (uint64_t)c->rank * c->nl_amps : 0;
+        run(c, SV_K_READOUT, [&] {
+            launch_sample_draw(c->dt, c->state, c->nres, c->d_samp, totals, world, rank, g, key, shots, base, dout,
+                               c->stream);
+        });
+        if (c->comm && shots) {  // each shot is owned by one rank; the others wrote 0
+            run(c, SV_K_ALLREDUCE, [&] {
+                SV_NCCL(ncclAllReduce(dout, dout, shots, ncclUint64, ncclSum, c->comm, c->stream));
+            });
+        }
+        if (!out_on_device && shots) {
+            SV_CUDA(cudaMemcpyAsync(out, dout, shots * 8, cudaMemcpyDeviceToHost, c->stream));
+            SV_CUDA(cudaStreamSynchronize(c->stream));
+        }
     });
 }
 

@@ -164,6 +164,14 @@ void launch_probabilities(sv_dtype dt, const void *a, double *p, uint64_t N, cud
 void launch_marked_mass(sv_dtype dt, const void *a, const uint64_t *marked, uint64_t m, double *out,
                         cudaStream_t s);
 
+// Seeded whole-register measurement (sample.cu; NEXT-3, G21).
+uint64_t sample_chunks(uint64_t N);
+void launch_sample_prefix(sv_dtype dt, const void *a, uint64_t N, double *scratch, double *rank_total,
+                          cudaStream_t s);
+void launch_sample_draw(sv_dtype dt, const void *a, uint64_t N, const double *scratch, const double *totals,
+                        int world, int rank, double *g, uint64_t key, uint64_t shots, uint64_t index_base,
+                        uint64_t *out, cudaStream_t s);
+
 // Seeded generators (host side of the library; G6, G8).
 uint64_t splitmix64_next(uint64_t &state);
 uint64_t hash64(uint64_t x);
