@@ -49,7 +49,13 @@ __global__ void __launch_bounds__(256) chunk_sum_kernel(const E *a, uint64_t N, 
     for (uint64_t c = blockIdx.x * wpb + threadIdx.x / 32; c < nchunks; c += (uint64_t)gridDim.x * wpb) {
         double acc = 0.0;
         const uint64_t base = c * kSampChunk;
-        for (int r = 0; r < kRows; ++r) acc = __dadd_rn(acc, warp_xor_sum(prob(a, base + r * 32 + lane, N)));
+        for (int r0 = 0; r0 < kRows; r0 += 8) {
+            double p[8];  // 8 rows of loads in flight, then the same row order
+#pragma unroll
+            for (int r = 0; r < 8; ++r) p[r] = prob(a, base + (r0 + r) * 32 + lane, N);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) acc = __dadd_rn(acc, warp_xor_sum(p[r]));
+        }
         if (lane == 0) sums[c] = acc;
     }
 }
