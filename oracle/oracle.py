@@ -81,6 +81,9 @@ def lib():
         L.or_noisy_transform.argtypes = [i32, vp, u64, u64, i32, ctypes.c_double]
         L.or_f0.argtypes = [i32, vp]
         L.or_iterate_noisy.argtypes = [i32, vp, vp, u64, i32, ctypes.c_double, u64, u64]
+        L.or_decay_site.argtypes = [i32, u64, u64, i32, i32]
+        L.or_decay_site.restype = i32
+        L.or_iterate_decoherent.argtypes = [i32, vp, vp, u64, i32, ctypes.c_double, ctypes.c_double, u64, u64, vp]
         L.or_sample_uniform.argtypes = [u64, u64]
         L.or_sample_uniform.restype = ctypes.c_double
         L.or_sample.argtypes = [i32, vp, u64, u64, vp, vp]
@@ -203,6 +206,21 @@ def probabilities(a: np.ndarray) -> np.ndarray:
 def marked_mass(a: np.ndarray, marked: np.ndarray) -> float:
     marked = np.ascontiguousarray(marked, dtype=np.uint64)
     return float(lib().or_marked_mass(_ptr(_state(a)), _ptr(marked), marked.size))
+
+
+def decay_site(n: int, seed: int, t: int, w: int, q: int) -> int:
+    return int(lib().or_decay_site(n, seed, t, w, q))
+
+
+def iterate_decoherent(a: np.ndarray, marked: np.ndarray, k: int, sigma: float, rate: float, seed: int,
+                       t0: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """k iterations with angle errors and the decoherence step after every
+    laser operation (readings G19, G20, G22); returns (state, survival[k])."""
+    marked = np.ascontiguousarray(marked, dtype=np.uint64)
+    surv = np.empty(k, dtype=np.float64)
+    lib().or_iterate_decoherent(_nbits(a), _ptr(_state(a)), _ptr(marked), marked.size, k, sigma, rate, seed, t0,
+                                _ptr(surv) if k else None)
+    return a, surv
 
 
 def sample_uniform(seed: int, s: int) -> float:

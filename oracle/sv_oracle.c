@@ -315,6 +315,65 @@ void or_iterate_noisy(int n, cplx *a, const uint64_t *marked, uint64_t m, int k,
 }
 
 /* ------------------------------------------------------------------------ */
+/* Decoherence                                         */
+/* ------------------------------------------------------------------------ */
+
+/* "The decoherence step adds two additional operations for every laser
+ * operation, and requires two messages to accumulate and redistribute the
+ * sum" (Eq. 3 text).  Reading G22 (the
+ * channel is not given; SPEC S:207-215's choice): after every laser operation
+ * (the 2x2 on qubit q), (1) a contraction of a randomly selected site s: the
+ * amplitudes with bit s = 1 are scaled by sqrt(1 - rate); (2) a global
+ * renormalisation by the accumulated sum sum_i |a_i|^2 (the paper's global
+ * sum).  s = hash64(key ^ c) mod n, c = (2t + w) * 64 + q, key = hash64(seed
+ * ^ "DECO").  survival[t] = product over iteration t's laser operations of the
+ * pre-renormalisation sums.  This follows the paper literally: one global sum
+ * per laser operation. */
+#define OR_TAG_DECO 0x4445434F00000000ULL /* "DECO" */
+
+double or_norm_sq(int n, const cplx *a);
+
+int or_decay_site(int n, uint64_t seed, uint64_t t, int w, int q)
+{
+    uint64_t key = or_hash64(seed ^ OR_TAG_DECO);
+    uint64_t c = (2ULL * t + (uint64_t)w) * 64ULL + (uint64_t)q;
+    return (int)(or_hash64(key ^ c) % (uint64_t)n);
+}
+
+static double or_contract_renormalise(int n, cplx *a, int s, double rate)
+{
+    uint64_t N = 1ULL << n, i, bit = 1ULL << s;
+    double c = sqrt(1.0 - rate), sum, inv;
+    for (i = 0; i < N; ++i)
+        if (i & bit) a[i] = a[i] * c;
+    sum = or_norm_sq(n, a);
+    inv = 1.0 / sqrt(sum);
+    for (i = 0; i < N; ++i) a[i] = a[i] * inv;
+    return sum;
+}
+
+void or_iterate_decoherent(int n, cplx *a, const uint64_t *marked, uint64_t m, int k, double sigma,
+                           double rate, uint64_t seed, uint64_t t0, double *survival)
+{
+    int it, w, q;
+    for (it = 0; it < k; ++it) {
+        uint64_t t = t0 + (uint64_t)it;
+        double surv = 1.0;
+        or_oracle_flip(a, marked, m);
+        for (w = 0; w < 2; ++w) {
+            if (w == 1) or_f0(n, a);
+            for (q = 0; q < n; ++q) {
+                double phi = 0.78539816339744831 + or_noise_delta(seed, t, w, q, sigma);
+                double cs = cos(phi), sn = sin(phi);
+                or_apply_2x2(n, a, q, cs, sn, sn, -cs);                         /* the laser operation */
+                surv *= or_contract_renormalise(n, a, or_decay_site(n, seed, t, w, q), rate);
+            }
+        }
+        if (survival) survival[it] = surv;
+    }
+}
+
+/* ------------------------------------------------------------------------ */
 /* Readouts                                                                 */
 /* ------------------------------------------------------------------------ */
 

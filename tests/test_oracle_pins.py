@@ -369,6 +369,83 @@ def test_sample_grover_state_finds_the_marked_index():
 
 
 # --------------------------------------------------------------------------- #
+# Decoherence step (NEXT-2, reading G22)                                       #
+# --------------------------------------------------------------------------- #
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_decoherent_iteration_equals_dense_brute_force(n):
+    """Every laser op as a dense matrix: the 2x2 on qubit q (numpy.kron), the
+    contraction diag(1, sqrt(1-r)) on the drawn site, then division by the
+    norm; survival = product of the pre-renormalisation sums.  n = 1 is
+    SPEC's example: the sum after a contraction is |alpha|^2 + (1-r)|beta|^2."""
+    N = 1 << n
+    sigma, rate, seed, t0, k = 0.1, 0.05, 21, 3, 2
+    a0 = crandn(N)
+    a0 /= np.linalg.norm(a0)
+    marked = orc.marked_from_seed(n, max(1, N // 4), 2)
+    O = np.eye(N)
+    O[marked, marked] = -1.0
+
+    def on_qubit(U, q):
+        return np.kron(np.kron(np.eye(1 << (n - q - 1)), U), np.eye(1 << q))
+
+    ref = a0.copy()
+    surv_ref = []
+    for t in range(t0, t0 + k):
+        ref = O @ ref
+        surv = 1.0
+        for w in (0, 1):
+            if w == 1:
+                ref = -ref
+                ref[0] = -ref[0]
+            for q in range(n):
+                phi = math.pi / 4 + orc.noise_delta(seed, t, w, q, sigma)
+                ref = on_qubit(np.array([[math.cos(phi), math.sin(phi)], [math.sin(phi), -math.cos(phi)]]), q) @ ref
+                s = orc.decay_site(n, seed, t, w, q)
+                ref = on_qubit(np.diag([1.0, math.sqrt(1 - rate)]), s) @ ref
+                nrm = float(np.sum(np.abs(ref) ** 2))
+                surv *= nrm
+                ref = ref / math.sqrt(nrm)
+        surv_ref.append(surv)
+    got, surv = orc.iterate_decoherent(a0.copy(), marked, k, sigma, rate, seed, t0)
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(surv, surv_ref, rtol=1e-12)
+
+
+def test_decoherence_single_qubit_survival_closed_form():
+    """contraction of |1> by sqrt(1-r) on alpha|0> + beta|1> leaves
+    sum |alpha|^2 + (1-r)|beta|^2.  With sigma = 0 and M = 0 the first laser op
+    maps |0> to the superposition (Fig. 1(b)): sum = 1/2 + (1-r)/2."""
+    r = 0.3
+    a = orc.init_zero_state(1)
+    _, surv = orc.iterate_decoherent(a, np.zeros(0, np.uint64), 1, 0.0, r, 1)
+    # op 1: H|0> = (1,1)/sqrt2 -> contraction -> 1/2 + (1-r)/2
+    s1 = 0.5 + (1 - r) / 2
+    # op 2 acts on the renormalised (1, sqrt(1-r))/sqrt(s1 * 2) after F0 and H
+    v = np.array([1.0, math.sqrt(1 - r)]) / math.sqrt(2 * s1)
+    v = np.array([v[0], -v[1]])
+    h = np.array([[1, 1], [1, -1]]) / math.sqrt(2)
+    v = h @ v
+    s2 = v[0] ** 2 + (1 - r) * v[1] ** 2
+    assert surv[0] == pytest.approx(s1 * s2, rel=1e-14)
+
+
+def test_decoherence_rate0_is_noisy_iteration_and_norm_is_kept():
+    n = 11
+    a0 = orc.init_gaussian(n, 4)
+    marked = orc.marked_from_seed(n, 3, 4)
+    got, surv = orc.iterate_decoherent(a0.copy(), marked, 4, 0.05, 0.0, 9, 2)
+    np.testing.assert_allclose(got, orc.iterate_noisy(a0.copy(), marked, 4, 0.05, 9, 2), rtol=0, atol=1e-13)
+    np.testing.assert_allclose(surv, 1.0, atol=1e-13)
+    got, surv = orc.iterate_decoherent(a0.copy(), marked, 4, 0.05, 0.02, 9, 2)
+    assert orc.norm_sq(got) == pytest.approx(1.0, abs=1e-12)
+    assert np.all((surv > 0) & (surv < 1))
+    _, surv2 = orc.iterate_decoherent(a0.copy(), marked, 4, 0.05, 0.04, 9, 2)
+    assert np.all(surv2 < surv)
+    sites = {orc.decay_site(n, 9, t, w, q) for t in range(20) for w in (0, 1) for q in range(n)}
+    assert sites == set(range(n))
+
+
+# --------------------------------------------------------------------------- #
 # Operational angle errors (NEXT-1, readings G19/G20)                          #
 # --------------------------------------------------------------------------- #
 def test_noisy_sigma0_is_ideal_grover():
