@@ -137,6 +137,22 @@ sv_status sv_iterate(sv_ctx *ctx, int k, sv_diffusion diffusion);
  * Errors: SV_EINVAL (k < 0, sigma not in [0, 10)), SV_ESTATE (no marked set). */
 sv_status sv_iterate_noisy(sv_ctx *ctx, int k, double sigma, uint64_t seed, uint64_t t0);
 
+/* k noisy Grover iterations with the decoherence step:
+ * "the decoherence step adds two additional operations for every laser
+ * operation, and requires two messages to accumulate and redistribute the
+ * sum" (Eq. 3 text).  Reading G22: after every laser
+ * operation (the 2x2 on qubit q of a transform) the amplitudes with bit d = 1
+ * of a drawn site d are contracted by sqrt(1 - rate), then the register is
+ * renormalised by the global sum |a|^2.  Angle errors as sv_iterate_noisy
+ * (sigma = 0: none).  The renormalisations are global scalars, so they are
+ * applied once per iteration from one deterministic fp64 reduction
+ * (allreduced over ranks); survival[t] (host, k entries, may be NULL) = the
+ * product of iteration t's pre-renormalisation sums.  The state is left
+ * normalised.  Errors: SV_EINVAL (k < 0, sigma, rate not in [0, 1)),
+ * SV_ESTATE (no marked set). */
+sv_status sv_iterate_decoherent(sv_ctx *ctx, int k, double sigma, double rate, uint64_t seed, uint64_t t0,
+                                double *survival);
+
 /* p_i = re^2 + im^2 in fp64 ("the probability of each state is defined as the
  * square of this complex amplitude") for the context's resident
  * indices (local shard; whole state in emulation), in local index order.

@@ -58,6 +58,7 @@ _SIGS = {
     "sv_diffuse": ([_ctxp, _i32], _i32),
     "sv_iterate": ([_ctxp, _i32, _i32], _i32),
     "sv_iterate_noisy": ([_ctxp, _i32, ctypes.c_double, _u64, _u64], _i32),
+    "sv_iterate_decoherent": ([_ctxp, _i32, ctypes.c_double, ctypes.c_double, _u64, _u64, _vp], _i32),
     "sv_probabilities": ([_ctxp, _vp, _u64, _i32], _i32),
     "sv_measure_marked_mass": ([_ctxp, _dp], _i32),
     "sv_sample": ([_ctxp, _u64, _u64, _vp, _i32], _i32),
@@ -157,6 +158,13 @@ def sv_iterate(ctx: Ctx, k: int, diffusion: int = SV_DIFFUSE_WHT) -> None:
 
 def sv_iterate_noisy(ctx: Ctx, k: int, sigma: float, seed: int, t0: int = 0) -> None:
     _check(lib.sv_iterate_noisy(ctx.ptr, k, sigma, seed, t0), "sv_iterate_noisy")
+
+
+def sv_iterate_decoherent(ctx: Ctx, k: int, sigma: float, rate: float, seed: int, t0: int = 0) -> np.ndarray:
+    """k iterations with angle errors + the decoherence step (G22); returns survival[k]."""
+    surv = np.zeros(max(k, 1), dtype=np.float64)
+    _check(lib.sv_iterate_decoherent(ctx.ptr, k, sigma, rate, seed, t0, surv.ctypes.data), "sv_iterate_decoherent")
+    return surv[:k]
 
 
 def sv_info(ctx: Ctx) -> dict:

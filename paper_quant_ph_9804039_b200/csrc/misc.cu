@@ -63,6 +63,14 @@ double noise_delta(uint64_t seed, uint64_t t, int w, int q, double sigma) {
     return sigma * (sqrt(-2.0 * log(u0)) * cos(6.283185307179586 * u1));
 }
 
+// Decoherence site after laser operation q of transform w, iteration t (G22):
+// hash64(hash64(seed ^ "DECO") ^ c) mod n, c = (2t + w) * 64 + q.
+int decay_site(int n, uint64_t seed, uint64_t t, int w, int q) {
+    const uint64_t key = hash64(seed ^ 0x4445434F00000000ull);
+    const uint64_t c = (2ull * t + (uint64_t)w) * 64ull + (uint64_t)q;
+    return (int)(hash64(key ^ c) % (uint64_t)n);
+}
+
 // Box-Muller on two counter hashes (G8): u = ((h >> 11) + 0.5) 2^-53.
 __device__ __forceinline__ void gauss_draw(uint64_t key, uint64_t i, double &re, double &im) {
     const uint64_t h0 = mix64((key ^ (2ull * i)) + 0x9E3779B97F4A7C15ull);
@@ -154,6 +162,60 @@ void launch_gauss_write(sv_dtype dt, void *a, uint64_t key, uint64_t off, uint64
                         cudaStream_t s) {
     if (dt == SV_C64) gauss_write_kernel<float2><<<grid_for(N), kThreads, 0, s>>>((float2 *)a, key, off, N, norm);
     else gauss_write_kernel<double2><<<grid_for(N), kThreads, 0, s>>>((double2 *)a, key, off, N, norm);
+    SV_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------------- //
+// Renormalisation (decoherence, G22): the paper's "accumulate and           //
+// redistribute a sum" (Eq. 3)                                   //
+// ------------------------------------------------------------------------- //
+template <typename E>
+__global__ void __launch_bounds__(kThreads) norm2_kernel(const E *a, uint64_t N, double *partials,
+                                                          unsigned int *counter, double *out) {
+    __shared__ double red[2 * (kThreads / 32)];
+    double s = 0.0, dummy = 0.0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x) {
+        const E v = a[i];
+        s += (double)v.x * (double)v.x + (double)v.y * (double)v.y;
+    }
+    block_sum2(s, dummy, red);
+    finalize(s, dummy, partials, counter, out, red);
+}
+
+void launch_norm2(sv_dtype dt, const void *a, uint64_t N, double *partials, unsigned int *counter, double *sum,
+                  cudaStream_t s) {
+    unsigned int g = grid_for(N, 8);
+    if (g > 4096) g = 4096;  // partials capacity
+    if (dt == SV_C64) norm2_kernel<float2><<<g, kThreads, 0, s>>>((const float2 *)a, N, partials, counter, sum);
+    else norm2_kernel<double2><<<g, kThreads, 0, s>>>((const double2 *)a, N, partials, counter, sum);
+    SV_CUDA(cudaGetLastError());
+}
+
+__global__ void norm_finalize_kernel(const double *sum, double *scale_out, double *survival) {
+    if (scale_out) *scale_out = 1.0 / sqrt(sum[0]);
+    if (survival) *survival = sum[0];
+}
+
+void launch_norm_finalize(const double *sum, double *scale_out, double *survival, cudaStream_t s) {
+    norm_finalize_kernel<<<1, 1, 0, s>>>(sum, scale_out, survival);
+    SV_CUDA(cudaGetLastError());
+}
+
+template <typename E>
+__global__ void scale_kernel(E *a, uint64_t N, const double *scale) {
+    using R = decltype(E{}.x);
+    const R sc = (R)scale[0];
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x) {
+        E v = a[i];
+        v.x *= sc;
+        v.y *= sc;
+        a[i] = v;
+    }
+}
+
+void launch_scale(sv_dtype dt, void *a, uint64_t N, const double *scale, cudaStream_t s) {
+    if (dt == SV_C64) scale_kernel<float2><<<grid_for(N), kThreads, 0, s>>>((float2 *)a, N, scale);
+    else scale_kernel<double2><<<grid_for(N), kThreads, 0, s>>>((double2 *)a, N, scale);
     SV_CUDA(cudaGetLastError());
 }
 

@@ -55,6 +55,8 @@ struct sv_ctx {
     int *d_barrier = nullptr;
     double *d_coefs = nullptr;          // angle-error coefficients of the one-CTA kernel
     size_t coefs_cap = 0;
+    double *d_deco = nullptr;           // decoherence: {sum, scale, survival[k]}
+    size_t deco_cap = 0;
     double *d_samp = nullptr;           // sampler: chunk prefixes + rank totals + window
     uint64_t *d_shots = nullptr;        // sampler: device output for host-returning calls
     uint64_t shots_cap = 0;
@@ -203,30 +205,62 @@ void xchg_barrier(sv_ctx *c) {
     });
 }
 
-// Operational angle errors (NEXT-1, G19/G20): iteration numbers t0 ..
+// General per-qubit 2x2 transforms (NEXT-1 angle errors G19/G20, NEXT-2
+// decoherence G22); iteration numbers t0 ...
 struct Noise {
     double sigma;
+    double rate;                      // decoherence rate per laser operation (0 = none)
     uint64_t seed;
     uint64_t t0;
+    const double *scale_first = nullptr;  // device scalar folded into the first pass's load
 };
 
-// (cos, sin) of U(pi/4 + delta) for logical qubit q in transform tr of the call
-static void noisy_coef(const Noise &nz, int tr, int q, double out[2]) {
-    const double phi = 0.78539816339744831 + noise_delta(nz.seed, nz.t0 + (uint64_t)(tr / 2), tr % 2, q, nz.sigma);
-    out[0] = cos(phi);
-    out[1] = sin(phi);
+// [w x; y z] of logical qubit q in transform tr (= 2 x iteration + w) of the
+// call, for all q.  Angle errors: U(pi/4 + delta) = [[c, s], [s, -c]].
+// Decoherence: the laser operations of a transform run q = 0..n-1, each
+// followed by a contraction diag(1, sqrt(1-rate)) of a drawn site d_q.  Such a
+// contraction commutes with every 2x2 except its own site's, so on qubit s it
+// sits BEFORE U_s if it follows an earlier operation (q < s) and AFTER U_s
+// otherwise: M_s = diag(1, post_s) U_s diag(1, pre_s) with pre_s / post_s the
+// products of those factors.  The renormalisations are scalars (applied once
+// per iteration by the caller).
+static void transform_coefs(const Noise &nz, int tr, int n, std::vector<double> &m) {
+    const uint64_t t = nz.t0 + (uint64_t)(tr / 2);
+    const int w = tr % 2;
+    m.assign((size_t)n * 4, 0.0);
+    std::vector<double> pre(n, 1.0), post(n, 1.0);
+    if (nz.rate > 0.0) {
+        const double cf = sqrt(1.0 - nz.rate);
+        for (int q = 0; q < n; ++q) {
+            const int d = decay_site(n, nz.seed, t, w, q);
+            if (q < d) pre[d] *= cf;
+            else post[d] *= cf;
+        }
+    }
+    for (int q = 0; q < n; ++q) {
+        const double phi = 0.78539816339744831 + noise_delta(nz.seed, t, w, q, nz.sigma);
+        const double cs = cos(phi), sn = sin(phi);
+        m[4 * q + 0] = cs;
+        m[4 * q + 1] = sn * pre[q];
+        m[4 * q + 2] = post[q] * sn;
+        m[4 * q + 3] = -post[q] * cs * pre[q];
+    }
 }
 
-void run_wht_schedule(sv_ctx *c, int k, bool with_oracle, const Noise *noise = nullptr) {
+void run_wht_schedule(sv_ctx *c, int k, bool with_oracle, const Noise *noise = nullptr, double *survival = nullptr) {
+    std::vector<std::vector<double>> tcoef;  // per transform of the call
+    if (noise) {
+        const int ntr = 2 * (with_oracle ? k : 1);
+        tcoef.resize(ntr);
+        for (int tr = 0; tr < ntr; ++tr) transform_coefs(*noise, tr, c->n, tcoef[tr]);
+    }
     if (c->plan.whole) {
         if (with_oracle && k == 0) return;
         const int reps = with_oracle ? k : 1;
         const double *coefs = nullptr;
         if (noise) {  // per (iteration, transform, qubit) coefficients for the one-CTA kernel
-            std::vector<double> h((size_t)reps * 2 * c->n * 2);
-            for (int it = 0; it < reps; ++it)
-                for (int w = 0; w < 2; ++w)
-                    for (int q = 0; q < c->n; ++q) noisy_coef(*noise, 2 * it + w, q, &h[((size_t)(2 * it + w) * c->n + q) * 2]);
+            std::vector<double> h;
+            for (const auto &v : tcoef) h.insert(h.end(), v.begin(), v.end());
             if (h.size() > c->coefs_cap) {
                 if (c->d_coefs) SV_CUDA(cudaFree(c->d_coefs));
                 c->d_coefs = nullptr;
@@ -240,10 +274,11 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle, const Noise *noise = n
         }
         run(c, SV_K_WHT_WHOLE, [&] {
             launch_whole_state(c->dt, c->state, c->n, reps, with_oracle ? 1 : 0, SV_DIFFUSE_WHT, c->d_marked,
-                               c->n_marked, c->stream, coefs);
+                               c->n_marked, c->stream, coefs, survival);
         });
         return;
     }
+    bool first_pass = true;
     const std::vector<Step> steps = schedule_wht(c->plan, k, with_oracle);
     const int total_bits = c->emulated ? c->n : c->plan.nl;
     // cur = the buffer holding the state.  Unfused: passes write `state`, a
@@ -299,10 +334,14 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle, const Noise *noise = n
                 // logical qubit of this slot: in the swapped layout the top-g
                 // local slots hold the rank qubits nl .. n-1
                 const int q = (s.layout == 1 && sl >= u0) ? c->plan.nl + (sl - u0) : sl;
-                if (s.pre) noisy_coef(*noise, s.tr_pre, q, a.coef[0][sl]);
-                if (s.post) noisy_coef(*noise, s.tr_post, q, a.coef[1][sl]);
+                for (int e = 0; e < 4; ++e) {
+                    if (s.pre) a.coef[0][sl][e] = tcoef[s.tr_pre][4 * q + e];
+                    if (s.post) a.coef[1][sl][e] = tcoef[s.tr_post][4 * q + e];
+                }
             }
+            if (first_pass) a.scale_in = noise->scale_first;
         }
+        first_pass = false;
         a.mid = s.mid;
         a.has_origin = origin_here(c) ? 1 : 0;
         a.pre = s.pre;
@@ -497,6 +536,7 @@ void destroy(sv_ctx *c) {
     cudaFree(c->d_barrier);
     cudaFree(c->d_coefs);
     cudaFree(c->d_samp);
+    cudaFree(c->d_deco);
     cudaFree(c->d_shots);
     if (c->comm) ncclCommDestroy(c->comm);
     cudaFree(c->state);
@@ -616,8 +656,51 @@ sv_status sv_iterate_noisy(sv_ctx *c, int k, double sigma, uint64_t seed, uint64
         SV_CHECK(c->n <= 64, SV_EINVAL, "internal: qubit index range");
         SV_CHECK(c->has_marked, SV_ESTATE, "sv_iterate_noisy before any marked set");
         SV_CUDA(cudaSetDevice(c->device));
-        const Noise nz{sigma, seed, t0};
+        const Noise nz{sigma, 0.0, seed, t0};
         run_wht_schedule(c, k, true, &nz);
+    });
+}
+
+sv_status sv_iterate_decoherent(sv_ctx *c, int k, double sigma, double rate, uint64_t seed, uint64_t t0,
+                                double *survival) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CHECK(k >= 0, SV_EINVAL, "k must be >= 0");
+        SV_CHECK(sigma >= 0.0 && sigma < 10.0, SV_EINVAL, "sigma must be in [0, 10)");
+        SV_CHECK(rate >= 0.0 && rate < 1.0, SV_EINVAL, "rate must be in [0, 1)");
+        SV_CHECK(c->n <= 64, SV_EINVAL, "internal: qubit index range");
+        SV_CHECK(c->has_marked, SV_ESTATE, "sv_iterate_decoherent before any marked set");
+        SV_CUDA(cudaSetDevice(c->device));
+        if (k == 0) return;
+        if ((size_t)k + 2 > c->deco_cap) {
+            if (c->d_deco) SV_CUDA(cudaFree(c->d_deco));
+            c->d_deco = nullptr;
+            c->deco_cap = 0;
+            dmalloc((void **)&c->d_deco, ((size_t)k + 2) * sizeof(double), "survival");
+            c->deco_cap = (size_t)k + 2;
+        }
+        double *sum = c->d_deco, *scale = c->d_deco + 1, *surv = c->d_deco + 2;
+        if (c->plan.whole) {  // one CTA: renormalises inside, once per iteration
+            const Noise nz{sigma, rate, seed, t0};
+            run_wht_schedule(c, k, true, &nz, surv);
+        } else {
+            // The renormalisations are global scalars, so the per-operation
+            // factors of an iteration collapse into one: after each iteration
+            // accumulate sum |a|^2 (Eq. 3's global sum, allreduced across
+            // ranks) and fold 1/sqrt(sum) into the next iteration's first load.
+            for (int it = 0; it < k; ++it) {
+                const Noise nz{sigma, rate, seed, t0 + (uint64_t)it, it == 0 ? nullptr : scale};
+                run_wht_schedule(c, 1, true, &nz);
+                run(c, SV_K_REDUCE, [&] { launch_norm2(c->dt, c->state, c->nres, c->d_partials, c->d_counter, sum, c->stream); });
+                allreduce_sum(c, sum, 1);
+                run(c, SV_K_REDUCE, [&] { launch_norm_finalize(sum, scale, surv + it, c->stream); });
+            }
+            run(c, SV_K_INIT, [&] { launch_scale(c->dt, c->state, c->nres, scale, c->stream); });
+        }
+        if (survival) {
+            SV_CUDA(cudaMemcpyAsync(survival, surv, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            SV_CUDA(cudaStreamSynchronize(c->stream));
+        }
     });
 }
 

@@ -122,15 +122,18 @@ struct PassArgs {
     int xchg_g = 0;                     // rank bits
     int xchg_rank = -1;                 // own rank; -1 = emulation (rank = index >> nl)
     void *xchg_dst[8] = {};             // destination buffer base of each rank
-    // angle-error stages (NEXT-1): coef[half][slot] = (cos, sin) of U(phi)
-    // for the stages before (half 0) / after (half 1) the elementwise op
+    // general 2x2 stages (NEXT-1 angle errors, NEXT-2 decoherence):
+    // coef[half][slot] = [w x; y z] for the stages before (half 0) / after
+    // (half 1) the elementwise op
     int noisy = 0;
-    double coef[2][64][2] = {};
+    double coef[2][64][4] = {};
+    const double *scale_in = nullptr;   // device scalar multiplied into the loaded tile
 };
 
 void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s);
 void launch_whole_state(sv_dtype dt, void *state, int n, int k, int with_oracle, int diffusion,
-                        const uint64_t *marked, uint64_t m, cudaStream_t s, const double *coefs = nullptr);
+                        const uint64_t *marked, uint64_t m, cudaStream_t s, const double *coefs = nullptr,
+                        double *survival = nullptr);
 
 struct MeanArgs {
     void *a = nullptr;
@@ -179,5 +182,13 @@ uint64_t gauss_key(uint64_t seed);
 uint64_t perm_seeded(int n, uint64_t seed, uint64_t x);
 // Angle error of qubit q in transform w of iteration t (G20).
 double noise_delta(uint64_t seed, uint64_t t, int w, int q, double sigma);
+// Decoherence site after laser operation q of transform w, iteration t (G22).
+int decay_site(int n, uint64_t seed, uint64_t t, int w, int q);
+// Renormalisation (G22): sum |a|^2 -> *sum (deterministic), then
+// scale_out = 1/sqrt(sum), survival = sum (either pointer may be null).
+void launch_norm2(sv_dtype dt, const void *a, uint64_t N, double *partials, unsigned int *counter, double *sum,
+                  cudaStream_t s);
+void launch_norm_finalize(const double *sum, double *scale_out, double *survival, cudaStream_t s);
+void launch_scale(sv_dtype dt, void *a, uint64_t N, const double *scale, cudaStream_t s);
 
 }  // namespace sv

@@ -22,6 +22,7 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
     kp.f0_scale = a.f0_scale;
     kp.mid = a.mid;
     kp.has_origin = a.has_origin;
+    kp.scale_in = a.scale_in;
     kp.xchg = a.xchg_nl > 0 ? 1 : 0;
     if (kp.xchg) {
         SV_CHECK(a.xchg_g >= 1 && a.xchg_g <= 3 && a.xchg_nl - a.xchg_g >= 1, SV_EINVAL,
@@ -39,10 +40,8 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
             SV_CHECK(b < 16, SV_EINVAL, "internal: tile too large");
             if ((a.proc_mask >> sl) & 1) proc |= 1u << b;
             if (a.noisy)
-                for (int h = 0; h < 2; ++h) {
-                    kp.coef[h][b][0] = a.coef[h][sl][0];
-                    kp.coef[h][b][1] = a.coef[h][sl][1];
-                }
+                for (int h = 0; h < 2; ++h)
+                    for (int e = 0; e < 4; ++e) kp.coef[h][b][e] = a.coef[h][sl][e];
             kp.slot[b++] = (signed char)sl;
         } else {
             kp.free_mask |= 1ull << sl;
@@ -68,14 +67,16 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
 // ------------------------------------------------------------------------- //
 // Whole state in one CTA (n <= T): k iterations without leaving shared memory //
 // ------------------------------------------------------------------------- //
-// coefs != nullptr: angle-error transforms (NEXT-1, G19); coefs[((it*2 + w)*n
-// + q)*2 + {0,1}] = (cos, sin) of qubit q's U(phi) in transform w of
-// iteration it; F0 then carries no 2^{-n} (f0_scale = 1).
+// coefs != nullptr: general 2x2 transforms (NEXT-1 angle errors, NEXT-2
+// decoherence); coefs[((it*2 + w)*n + q)*4 + {0..3}] = [w x; y z] of qubit q
+// in transform w of iteration it; F0 then carries no 2^{-n} (f0_scale = 1).
+// survival != nullptr: renormalise after every iteration (G22) and record the
+// pre-renormalisation sum |a|^2 of iteration it in survival[it].
 template <typename E>
 __global__ void __launch_bounds__(512) whole_state_kernel(E *a, int n, int k, int with_oracle, int diffusion,
                                                           const unsigned long long *marked,
                                                           unsigned long long m, double f0_scale,
-                                                          const double *coefs) {
+                                                          const double *coefs, double *survival) {
     using R = typename RealOf<E>::T;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     E *s = reinterpret_cast<E *>(smem_raw);
@@ -86,10 +87,10 @@ __global__ void __launch_bounds__(512) whole_state_kernel(E *a, int n, int k, in
     auto transform = [&](int it, int w) {
         for (int q = 0; q < n; ++q) {
             const unsigned int bit = 1u << q;
-            const double *cq = coefs ? coefs + ((size_t)(2 * it + w) * n + q) * 2 : nullptr;
+            const double *cq = coefs ? coefs + ((size_t)(2 * it + w) * n + q) * 4 : nullptr;
             for (unsigned int pr = tid; pr < N / 2; pr += nt) {
                 const unsigned int i = ((pr >> q) << (q + 1)) | (pr & (bit - 1));
-                if (cq) bfly_rot(s[i], s[i | bit], cq[0], cq[1]);
+                if (cq) bfly_gen(s[i], s[i | bit], cq);
                 else bfly(s[i], s[i | bit]);
             }
             __syncthreads();
@@ -114,6 +115,21 @@ __global__ void __launch_bounds__(512) whole_state_kernel(E *a, int n, int k, in
             }
             __syncthreads();
             transform(it, 1);
+            if (survival) {  // fixed-order block sum of |a|^2, then scale to norm 1
+                double sq = 0.0, dummy = 0.0;
+                for (unsigned int i = tid; i < N; i += nt)
+                    sq += (double)s[i].x * (double)s[i].x + (double)s[i].y * (double)s[i].y;
+                for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+                if ((tid & 31) == 0) red[2 * (tid >> 5)] = sq;
+                __syncthreads();
+                double tot = 0.0;
+                for (unsigned int w = 0; w < nt / 32; ++w) tot += red[2 * w];
+                (void)dummy;
+                if (tid == 0) survival[it] = tot;
+                const R inv = (R)(1.0 / sqrt(tot));
+                for (unsigned int i = tid; i < N; i += nt) { s[i].x *= inv; s[i].y *= inv; }
+                __syncthreads();
+            }
         } else {
             // fixed-order block reduction in fp64 (deterministic)
             double re = 0.0, im = 0.0;
@@ -137,7 +153,7 @@ __global__ void __launch_bounds__(512) whole_state_kernel(E *a, int n, int k, in
 }
 
 void launch_whole_state(sv_dtype dt, void *state, int n, int k, int with_oracle, int diffusion,
-                        const uint64_t *marked, uint64_t m, cudaStream_t s, const double *coefs) {
+                        const uint64_t *marked, uint64_t m, cudaStream_t s, const double *coefs, double *survival) {
     const unsigned int N = 1u << n;
     const int threads = N >= 1024 ? 512 : (N / 2 >= 32 ? (int)(N / 2) : 32);
     const double f0 = coefs ? 1.0 : ldexp(1.0, -n);
@@ -147,12 +163,12 @@ void launch_whole_state(sv_dtype dt, void *state, int n, int k, int with_oracle,
         const int smem = (int)(N * sizeof(float2));
         SV_CUDA(cudaFuncSetAttribute(whole_state_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         whole_state_kernel<float2>
-            <<<1, threads, smem, s>>>((float2 *)state, n, k, with_oracle, diffusion, mk, m, f0, coefs);
+            <<<1, threads, smem, s>>>((float2 *)state, n, k, with_oracle, diffusion, mk, m, f0, coefs, survival);
     } else {
         const int smem = (int)(N * sizeof(double2));
         SV_CUDA(cudaFuncSetAttribute(whole_state_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         whole_state_kernel<double2>
-            <<<1, threads, smem, s>>>((double2 *)state, n, k, with_oracle, diffusion, mk, m, f0, coefs);
+            <<<1, threads, smem, s>>>((double2 *)state, n, k, with_oracle, diffusion, mk, m, f0, coefs, survival);
     }
     SV_CUDA(cudaGetLastError());
 }

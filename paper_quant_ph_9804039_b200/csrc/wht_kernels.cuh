@@ -165,9 +165,10 @@ struct KParams {
     // fused qubit-swap exchange (global_store_xchg): 0 = plain store
     int xchg, xnl, xg, xrank;      // local index bits, rank bits, own rank (-1: emulated)
     void *xdst[8];                 // destination buffer of each rank
-    // angle-error stages (NEXT-1): per half (0 = before the op, 1 = after) and
-    // tile bit, (cos phi, sin phi) of U(phi) = [[c, s], [s, -c]]
-    double coef[2][16][2];
+    // general 2x2 stages (NEXT-1/2): per half (0 = before the op, 1 = after)
+    // and tile bit, [w x; y z] row-major
+    double coef[2][16][4];
+    const double *scale_in;        // != nullptr: multiply the loaded tile by *scale_in (renormalisation)
 };
 
 // Publish the exchange destinations in shared memory (constant indices only:
@@ -202,33 +203,37 @@ __device__ __forceinline__ void bfly<float2>(float2 &x, float2 &y) {
     y = *reinterpret_cast<float2 *>(&d);
 }
 
-// Angle-error stage (G19): (u, v) -> (c u + s v, s u - c v).
+// General real 2x2 stage (Fig. 3's [w x; y z]):
+// (u, v) -> (w u + x v, y u + z v).  Angle errors (G19) use
+// [[cos, sin], [sin, -cos]]; with decoherence (G22) the per-qubit matrix also
+// carries the contractions of the laser operations around it.
 template <typename E>
-__device__ __forceinline__ void bfly_rot(E &x, E &y, double cd, double sd) {
+__device__ __forceinline__ void bfly_gen(E &x, E &y, const double *m) {
     using R = decltype(E{}.x);
-    const R c = (R)cd, s = (R)sd;
+    const R w = (R)m[0], xx = (R)m[1], yy = (R)m[2], z = (R)m[3];
     E t = x;
-    x.x = c * t.x + s * y.x;
-    x.y = c * t.y + s * y.y;
-    y.x = s * t.x - c * y.x;
-    y.y = s * t.y - c * y.y;
+    x.x = w * t.x + xx * y.x;
+    x.y = w * t.y + xx * y.y;
+    y.x = yy * t.x + z * y.x;
+    y.y = yy * t.y + z * y.y;
 }
 
 template <>
-__device__ __forceinline__ void bfly_rot<float2>(float2 &x, float2 &y, double cd, double sd) {
-    const float c = (float)cd, s = (float)sd;
-    const float2 cc = make_float2(c, c), ss = make_float2(s, s), nc = make_float2(-c, -c);
+__device__ __forceinline__ void bfly_gen<float2>(float2 &x, float2 &y, const double *m) {
+    const float w = (float)m[0], xx = (float)m[1], yy = (float)m[2], z = (float)m[3];
+    const float2 W = make_float2(w, w), X = make_float2(xx, xx), Y = make_float2(yy, yy), Z = make_float2(z, z);
     const unsigned long long a = *reinterpret_cast<unsigned long long *>(&x);
     const unsigned long long b = *reinterpret_cast<unsigned long long *>(&y);
-    const unsigned long long C = *reinterpret_cast<const unsigned long long *>(&cc);
-    const unsigned long long S = *reinterpret_cast<const unsigned long long *>(&ss);
-    const unsigned long long NC = *reinterpret_cast<const unsigned long long *>(&nc);
+    const unsigned long long w2 = *reinterpret_cast<const unsigned long long *>(&W);
+    const unsigned long long x2 = *reinterpret_cast<const unsigned long long *>(&X);
+    const unsigned long long y2 = *reinterpret_cast<const unsigned long long *>(&Y);
+    const unsigned long long z2 = *reinterpret_cast<const unsigned long long *>(&Z);
     unsigned long long t, u;
     asm("mul.rn.f32x2 %0, %2, %4;\n\t"
         "fma.rn.f32x2 %0, %3, %5, %0;\n\t"
-        "mul.rn.f32x2 %1, %2, %5;\n\t"
-        "fma.rn.f32x2 %1, %3, %6, %1;"
-        : "=&l"(t), "=&l"(u) : "l"(a), "l"(b), "l"(C), "l"(S), "l"(NC));
+        "mul.rn.f32x2 %1, %2, %6;\n\t"
+        "fma.rn.f32x2 %1, %3, %7, %1;"
+        : "=&l"(t), "=&l"(u) : "l"(a), "l"(b), "l"(w2), "l"(x2), "l"(y2), "l"(z2));
     x = *reinterpret_cast<float2 *>(&t);
     y = *reinterpret_cast<float2 *>(&u);
 }
@@ -262,7 +267,7 @@ __device__ __forceinline__ void run_stages(E (&x)[L::NR], const KParams &p) {
                 for (int j = 0; j < L::NR; ++j)
                     if (!(j & (1 << i))) {
                         if constexpr (NOISY)
-                            bfly_rot(x[j], x[j | (1 << i)], p.coef[HALF][b][0], p.coef[HALF][b][1]);
+                            bfly_gen(x[j], x[j | (1 << i)], p.coef[HALF][b]);
                         else
                             bfly(x[j], x[j | (1 << i)]);
                     }
@@ -489,6 +494,14 @@ __device__ __forceinline__ void mid_op(E (&x)[L::NR], const KParams &p, unsigned
     }
 }
 
+// Renormalisation folded into the load (decoherence, G22): x *= s.
+template <typename E, int NR>
+__device__ __forceinline__ void apply_scale(E (&x)[NR], double s) {
+    using R = decltype(E{}.x);
+#pragma unroll
+    for (int j = 0; j < NR; ++j) scale(x[j], (R)s);
+}
+
 // Tile base: scatter the tile id into the free slots (software pdep).
 __device__ __forceinline__ unsigned long long tile_base(unsigned long long tile, unsigned long long fm) {
     unsigned long long base = 0;
@@ -620,6 +633,7 @@ __global__ void __launch_bounds__(1 << (TB - RB), SV_TILE_MIN_BLOCKS) wht_tile2_
     const unsigned long long base = tile_base(blockIdx.x, p.free_mask);
     float2 x[L::NR];
     global_load<L, 0>(x, reinterpret_cast<const float2 *>(p.in) + base, p, tid);
+    if (p.scale_in) apply_scale(x, *p.scale_in);
     const bool has_marked = (p.mid == MID_ORACLE) && oracle_lookup(p, blockIdx.x, tid, &s_mlo, &s_mcnt);
     tile_body2<L, PRE, POST, U, NOISY>(x, sm, p, base, reinterpret_cast<float2 *>(p.out) + base, tid, s_dst, has_marked, &s_mlo,
                                 &s_mcnt);
@@ -638,6 +652,7 @@ __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB >= 9) ? 1 : SV_TILE_M
     const unsigned long long base = tile_base(blockIdx.x, p.free_mask);
     E x[L::NR];
     global_load<L, 0>(x, reinterpret_cast<const E *>(p.in) + base, p, tid);
+    if (p.scale_in) apply_scale(x, *p.scale_in);
     const bool has_marked = (p.mid == MID_ORACLE) && oracle_lookup(p, blockIdx.x, tid, &s_mlo, &s_mcnt);
     tile_body<L, PRE, POST, U, NOISY>(x, sm, p, base, reinterpret_cast<E *>(p.out) + base, tid, s_dst, has_marked, &s_mlo, &s_mcnt);
 }
