@@ -40,6 +40,9 @@ CONFIGS = {
     "c3n": (28, "c64", 1, 64, "wht-noisy", 3, "uniform", "c3 with angle errors sigma=0.01: n=28 complex64, M=1, 64 iterations"),
     "c4n": (32, "c64", 256, 16, "wht-noisy", 4, "uniform",
             "c4 with angle errors sigma=0.01: n=32 complex64, M=256, 16 iterations"),
+    # NEXT-2: angle errors + decoherence step (rate 1e-3 per laser operation)
+    "c3d": (28, "c64", 1, 64, "wht-decoherent", 3, "uniform",
+            "c3 with angle errors sigma=0.01 and decoherence rate=1e-3: n=28 complex64, M=1, 64 iterations"),
 }
 METRIC = "grover_amp_updates_per_s"
 UNIT = "amplitude-updates/s"
@@ -161,6 +164,8 @@ def run_reference(args):
         t0 = time.perf_counter()
         if diff == "wht-noisy":
             orc.iterate_noisy(a, marked, k_s, 0.01, seed, 0)
+        elif diff == "wht-decoherent":
+            orc.iterate_decoherent(a, marked, k_s, 0.01, 1e-3, seed, 0)
         else:
             orc.iterate(a, marked, k_s, orc.MEAN if diff == "mean" else orc.WHT)
         dt = time.perf_counter() - t0
@@ -192,11 +197,13 @@ def run_ours(args):
     dtype = sv.SV_C64 if dts == "c64" else sv.SV_C128
     dflag = sv.SV_DIFFUSE_MEAN if diff == "mean" else sv.SV_DIFFUSE_WHT
     noisy = diff == "wht-noisy"
-    sigma = 0.01
+    sigma, rate = 0.01, 1e-3
 
     def iterate():
         if noisy:
             sv.sv_iterate_noisy(ctx, k, sigma, seed, 0)
+        elif diff == "wht-decoherent":
+            sv.sv_iterate_decoherent(ctx, k, sigma, rate, seed, 0)
         else:
             sv.sv_iterate(ctx, k, dflag)
     ikind = sv.SV_INIT_UNIFORM if init == "uniform" else sv.SV_INIT_GAUSSIAN
