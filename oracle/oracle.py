@@ -90,6 +90,11 @@ def lib():
         L.or_reorganize.argtypes = [i32, i32, vp, vp]
         L.or_wht_sharded.argtypes = [i32, i32, vp]
         L.or_wht_sharded.restype = i32
+        L.or_apply_controlled_2x2.argtypes = [i32, vp, i32, u64] + [_C128] * 4
+        L.or_apply_gates.argtypes = [i32, vp, vp, u64]
+        L.or_apply_gates.restype = i32
+        L.or_apply_gates_sharded.argtypes = [i32, i32, vp, u64, vp]
+        L.or_apply_gates_sharded.restype = i32
         _lib = L
     return _lib
 
@@ -282,3 +287,41 @@ def iterate_noisy(a: np.ndarray, marked: np.ndarray, k: int, sigma: float, seed:
     marked = np.ascontiguousarray(marked, dtype=np.uint64)
     lib().or_iterate_noisy(_nbits(a), _ptr(_state(a)), _ptr(marked), marked.size, k, sigma, seed, t0)
     return a
+
+
+# --------------------------------------------------------------------------- #
+# NEXT-4: gate circuits (or_apply_gates; section 2.1, Fig. 3)     #
+# --------------------------------------------------------------------------- #
+# Layout of or_gate (80 bytes): int32 target, int32 reserved, uint64 controls,
+# double m[8] = w, x, y, z as (re, im) pairs of [w x; y z].
+GATE_DTYPE = np.dtype([("target", "<i4"), ("reserved", "<i4"), ("controls", "<u8"), ("m", "<f8", (8,))])
+
+
+def _gates(gates) -> np.ndarray:
+    g = np.ascontiguousarray(gates, dtype=GATE_DTYPE)
+    assert g.dtype.itemsize == 80
+    return g
+
+
+def apply_controlled_2x2(a: np.ndarray, q: int, controls: int, w, x, y, z) -> np.ndarray:
+    lib().or_apply_controlled_2x2(_nbits(a), _ptr(_state(a)), q, controls,
+                                  *(_C128(v.real, v.imag) for v in map(complex, (w, x, y, z))))
+    return a
+
+
+def apply_gates(a: np.ndarray, gates) -> np.ndarray:
+    """or_apply_gates: the gates in order on the full vector (raises on an invalid gate)."""
+    g = _gates(gates)
+    if lib().or_apply_gates(_nbits(a), _ptr(_state(a)), _ptr(g), g.size) != 0:
+        raise ValueError("invalid gate (target/control out of range or control == target)")
+    return a
+
+
+def apply_gates_sharded(a: np.ndarray, gates, g_bits: int) -> int:
+    """or_apply_gates_sharded: the same circuit over 2^g shards with Fig. 8
+    reorganisations; returns the reorganisation count."""
+    g = _gates(gates)
+    r = lib().or_apply_gates_sharded(_nbits(a), g_bits, _ptr(g), g.size, _ptr(_state(a)))
+    if r < 0:
+        raise ValueError("invalid gate or g")
+    return r

@@ -519,3 +519,122 @@ int or_wht_sharded(int n, int g, cplx *a_global)
     free(sh);
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-4: circuits of general (controlled) 2x2 gates                       */
+/* ------------------------------------------------------------------------ */
+
+/* One gate.  Section 2.1: "we describe each operation with a
+ * VxV transformation matrix.  Because each gate only operates on a small
+ * number of bits, these matrices are simply 2x2 or 4x4 matrices replicated
+ * many times."  A gate here is Fig. 3's general 2x2 [w x; y z] on qubit
+ * `target`, replicated over the V/2 pairs, and
+ * applied only to the pairs whose `controls` qubits are all 1 (a controlled
+ * 2x2 is the 4x4 of a two-bit gate, e.g. a controlled-NOT; reading G23).
+ * m = {w.re, w.im, x.re, x.im, y.re, y.im, z.re, z.im}.  80 bytes. */
+typedef struct {
+    int32_t target;
+    int32_t reserved;
+    uint64_t controls; /* bit q set: qubit q must be 1 */
+    double m[8];
+} or_gate;
+
+/* The V/2-pair loop of P:3080-3084, restricted to the pairs whose control
+ * bits are all set. */
+void or_apply_controlled_2x2(int n, cplx *a, int q, uint64_t controls, cplx w, cplx x, cplx y, cplx z)
+{
+    uint64_t N = 1ULL << n, bit = 1ULL << q, i;
+    for (i = 0; i < N; ++i) {
+        if (i & bit) continue;
+        if ((i & controls) != controls) continue;
+        {
+            cplx a0 = a[i], a1 = a[i | bit];
+            a[i] = w * a0 + x * a1;
+            a[i | bit] = y * a0 + z * a1;
+        }
+    }
+}
+
+static int or_gate_valid(int n, const or_gate *g)
+{
+    uint64_t all = (n >= 64) ? ~0ULL : ((1ULL << n) - 1ULL);
+    if (g->target < 0 || g->target >= n) return 0;
+    if (g->controls & ~all) return 0;
+    if ((g->controls >> g->target) & 1ULL) return 0;
+    return 1;
+}
+
+/* Apply gates[0..count) in order.  Returns 0, or -1 (nothing applied) if a
+ * gate has a target outside [0, n), a control >= n, or controls its own
+ * target. */
+int or_apply_gates(int n, cplx *a, const or_gate *g, uint64_t count)
+{
+    uint64_t j;
+    for (j = 0; j < count; ++j)
+        if (!or_gate_valid(n, &g[j])) return -1;
+    for (j = 0; j < count; ++j)
+        or_apply_controlled_2x2(n, a, g[j].target, g[j].controls, g[j].m[0] + I * g[j].m[1],
+                                g[j].m[2] + I * g[j].m[3], g[j].m[4] + I * g[j].m[5], g[j].m[6] + I * g[j].m[7]);
+    return 0;
+}
+
+/* The same circuit over P = 2^g shards, the paper's way (section 3.1,
+ * P:4097-4113): shard r holds the states whose parallel bits concatenate to
+ * r; "all of the processors can run in parallel operating only on local
+ * data as long as they do not use any of the QU-bits in the set N.  When the
+ * computation needs to operate on one of the bits in N, a new set is picked
+ * and the simulator redistributes the data" (Fig. 8, or_reorganize).  The
+ * new set is always the top g local positions, so the physical layout is
+ * either natural or swapped (positions [nl-g, nl) <-> [nl, n)); a control on
+ * a parallel bit is decided by the shard number.  The natural layout is
+ * restored at the end.  Must equal or_apply_gates on the concatenated
+ * vector.  Returns the number of reorganisations, or -1. */
+int or_apply_gates_sharded(int n, int g, const or_gate *gates, uint64_t count, cplx *a_global)
+{
+    uint64_t P = 1ULL << g, Nl, r, j;
+    int nl = n - g, swapped = 0, reorgs = 0, q;
+    cplx **sh;
+    cplx *tmp;
+    if (g < 0 || 2 * g > n) return -1;
+    for (j = 0; j < count; ++j)
+        if (!or_gate_valid(n, &gates[j])) return -1;
+    Nl = 1ULL << nl;
+    sh = (cplx **)malloc(sizeof(cplx *) * P);
+    tmp = (cplx *)malloc(sizeof(cplx) * P * Nl);
+    for (r = 0; r < P; ++r) sh[r] = a_global + r * Nl;
+    for (j = 0; j < count; ++j) {
+        const or_gate *gt = &gates[j];
+        int pt;
+        /* physical position of logical qubit q */
+#define OR_PHYS(q) ((!swapped) ? (q) : ((q) >= nl ? (q) - g : ((q) >= nl - g ? (q) + g : (q))))
+        pt = OR_PHYS(gt->target);
+        if (pt >= nl) {
+            or_reorganize(n, g, sh, tmp);
+            swapped ^= 1;
+            ++reorgs;
+            pt = OR_PHYS(gt->target);
+        }
+        for (r = 0; r < P; ++r) {
+            uint64_t local_c = 0;
+            int ok = 1;
+            for (q = 0; q < n; ++q) {
+                int pq;
+                if (!((gt->controls >> q) & 1ULL)) continue;
+                pq = OR_PHYS(q);
+                if (pq < nl) local_c |= 1ULL << pq;
+                else if (!((r >> (pq - nl)) & 1ULL)) ok = 0; /* parallel bit of shard r is 0 */
+            }
+            if (!ok) continue;
+            or_apply_controlled_2x2(nl, sh[r], pt, local_c, gt->m[0] + I * gt->m[1], gt->m[2] + I * gt->m[3],
+                                    gt->m[4] + I * gt->m[5], gt->m[6] + I * gt->m[7]);
+        }
+#undef OR_PHYS
+    }
+    if (swapped) {
+        or_reorganize(n, g, sh, tmp);
+        ++reorgs;
+    }
+    free(tmp);
+    free(sh);
+    return reorgs;
+}
