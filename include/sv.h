@@ -206,6 +206,60 @@ sv_status sv_info(const sv_ctx *ctx, int *n, int *world, int *rank, uint64_t *lo
 sv_status sv_set_exchange(sv_ctx *ctx, int fused);
 sv_status sv_get_exchange(const sv_ctx *ctx, int *fused);
 
+/* ---- NEXT-4: circuits of general (controlled) 2x2 gates ------------------- */
+
+/* One gate (80 bytes).  Section 2.1: "we describe each
+ * operation with a VxV transformation matrix.  Because each gate only
+ * operates on a small number of bits, these matrices are simply 2x2 or 4x4
+ * matrices replicated many times."  The gate is Fig. 3's general 2x2
+ * [w x; y z] on qubit `target`, applied as V/2 independent pair
+ * transformations: for every index i with bit `target` = 0 and
+ * (i & controls) == controls, (a_i, a_j) <- (w a_i + x a_j, y a_i + z a_j),
+ * j = i | 2^target.  A controlled 2x2 is the 4x4 of a two-bit gate (G23).
+ *   m = {w.re, w.im, x.re, x.im, y.re, y.im, z.re, z.im} (fp64; rounded to
+ *   fp32 for SV_C64 states); reserved must be 0. */
+typedef struct {
+    int32_t target;
+    int32_t reserved;
+    uint64_t controls;
+    double m[8];
+} sv_gate;
+
+/* Apply gates[0..count) to the state, in order (gates may be regrouped only
+ * where they commute: different targets, neither controlled by the other's
+ * target).  The host planner packs consecutive runs of gates on up to T
+ * local qubits into one tile pass each (one HBM read + write per pass, all of
+ * the pass's gates on-chip); a gate on a parallel (rank) qubit first triggers
+ * the qubit swap of section 3.1 / Fig. 8 ("when the computation needs to
+ * operate on one of the bits in N, a new set is picked and the simulator
+ * redistributes the data"); the natural layout is restored
+ * before the call returns.  n <= T (13 for c64, 12 for c128) runs all gates
+ * in one CTA's shared memory.  gates: host array, copied.
+ * Errors: SV_EINVAL (target not in [0, n), control >= n, control == target,
+ * reserved != 0, gates NULL with count > 0). */
+sv_status sv_apply_gates(sv_ctx *ctx, const sv_gate *gates, uint64_t count);
+
+/* One step of a gate-circuit schedule: kind 0 = tile pass (tile_mask / proc_mask
+ * as in sv_plan_step, in PHYSICAL slots of the shard; its gates are
+ * order[first .. first + count)), kind 1 = qubit-swap exchange (physical
+ * slots [nl - g, nl) <-> the g rank bits), kind 2 = whole state in one CTA. */
+typedef struct {
+    int kind;
+    int tile_bits;
+    uint64_t tile_mask;
+    uint64_t proc_mask;
+    uint64_t first;
+    uint64_t count;
+} sv_gate_plan_step;
+
+/* The schedule sv_apply_gates enqueues on every rank for an n-qubit state over
+ * world = 2^g ranks (host only, no device).  Writes at most cap steps
+ * (*nsteps = total) and, if order != NULL, the execution order of the gate
+ * indices (count entries).  The layout is natural again after the last step.
+ * Errors: as sv_apply_gates, plus invalid (n, world, dtype). */
+sv_status sv_plan_gates(int n, int world, sv_dtype dtype, const sv_gate *gates, uint64_t count,
+                        sv_gate_plan_step *out, int cap, int *nsteps, uint64_t *order);
+
 /* Block until all work enqueued on the context's stream is done. */
 sv_status sv_synchronize(sv_ctx *ctx);
 
@@ -250,7 +304,8 @@ typedef enum {
     SV_K_READOUT = 6,    /* probabilities / marked mass              */
     SV_K_EXCHANGE = 7,   /* qubit-swap all-to-all (NCCL or emulated) */
     SV_K_ALLREDUCE = 8,  /* scalar NCCL allreduce                    */
-    SV_K_COUNT = 9
+    SV_K_GATE_TILE = 9,  /* gate-circuit tile pass (NEXT-4)          */
+    SV_K_COUNT = 10
 } sv_kernel_kind;
 
 /* enable != 0: bracket every launch with CUDA events and count launches per

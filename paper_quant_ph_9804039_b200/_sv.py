@@ -20,8 +20,11 @@ SV_C64, SV_C128 = 0, 1
 SV_INIT_UNIFORM, SV_INIT_GAUSSIAN, SV_INIT_ZERO_STATE = 0, 1, 2
 SV_DIFFUSE_WHT, SV_DIFFUSE_MEAN = 0, 1
 (SV_K_WHT_TILE, SV_K_WHT_WHOLE, SV_K_MEAN, SV_K_REDUCE, SV_K_INIT, SV_K_ORACLE, SV_K_READOUT,
- SV_K_EXCHANGE, SV_K_ALLREDUCE, SV_K_COUNT) = range(10)
-KERNEL_KIND_NAMES = ["wht_tile", "wht_whole", "mean", "reduce", "init", "oracle", "readout", "exchange", "allreduce"]
+ SV_K_EXCHANGE, SV_K_ALLREDUCE, SV_K_GATE_TILE, SV_K_COUNT) = range(11)
+KERNEL_KIND_NAMES = ["wht_tile", "wht_whole", "mean", "reduce", "init", "oracle", "readout", "exchange", "allreduce",
+                     "gate_tile"]
+# sv_gate (80 bytes): int32 target, int32 reserved, uint64 controls, double m[8] = [w x; y z] as (re, im)
+GATE_DTYPE = np.dtype([("target", "<i4"), ("reserved", "<i4"), ("controls", "<u8"), ("m", "<f8", (8,))])
 
 NP_DTYPE = {SV_C64: np.complex64, SV_C128: np.complex128}
 
@@ -41,6 +44,11 @@ class sv_plan_step(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int), ("pre", ctypes.c_int), ("mid", ctypes.c_int), ("post", ctypes.c_int),
                 ("in_recv", ctypes.c_int), ("tile_bits", ctypes.c_int), ("tile_mask", ctypes.c_uint64),
                 ("proc_mask", ctypes.c_uint64)]
+
+
+class sv_gate_plan_step(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("tile_bits", ctypes.c_int), ("tile_mask", ctypes.c_uint64),
+                ("proc_mask", ctypes.c_uint64), ("first", ctypes.c_uint64), ("count", ctypes.c_uint64)]
 
 
 if not os.path.exists(LIB_PATH):
@@ -72,6 +80,9 @@ _SIGS = {
     "sv_get_exchange": ([_ctxp, ctypes.POINTER(_i32)], _i32),
     "sv_nccl_unique_id": ([_vp, ctypes.c_size_t], _i32),
     "sv_plan_wht": ([_i32, _i32, _i32, _i32, _i32, ctypes.POINTER(sv_plan_step), _i32, ctypes.POINTER(_i32)], _i32),
+    "sv_apply_gates": ([_ctxp, _vp, _u64], _i32),
+    "sv_plan_gates": ([_i32, _i32, _i32, _vp, _u64, ctypes.POINTER(sv_gate_plan_step), _i32, ctypes.POINTER(_i32),
+                       _vp], _i32),
     "sv_profile": ([_ctxp, _i32], _i32),
     "sv_profile_read": ([_ctxp, _i32, ctypes.POINTER(_u64), _dp], _i32),
     "sv_profile_timeline": ([_ctxp, _vp, _vp, _u64, ctypes.POINTER(_u64)], _i32),
@@ -247,6 +258,30 @@ def sv_plan_wht(n: int, world: int, dtype: int, k: int, with_oracle: bool) -> li
     arr = (sv_plan_step * max(cnt.value, 1))()
     _check(lib.sv_plan_wht(n, world, dtype, k, int(with_oracle), arr, cnt.value, ctypes.byref(cnt)), "sv_plan_wht")
     return [{f: getattr(arr[i], f) for f, _ in sv_plan_step._fields_} for i in range(cnt.value)]
+
+
+def _gates(gates) -> np.ndarray:
+    g = np.ascontiguousarray(gates, dtype=GATE_DTYPE)
+    assert g.dtype.itemsize == 80
+    return g
+
+
+def sv_apply_gates(ctx: Ctx, gates) -> None:
+    g = _gates(gates)
+    _check(lib.sv_apply_gates(ctx.ptr, g.ctypes.data if g.size else None, g.size), "sv_apply_gates")
+
+
+def sv_plan_gates(n: int, world: int, dtype: int, gates) -> tuple[list[dict], np.ndarray]:
+    g = _gates(gates)
+    gp = g.ctypes.data if g.size else None
+    cnt = _i32()
+    _check(lib.sv_plan_gates(n, world, dtype, gp, g.size, None, 0, ctypes.byref(cnt), None), "sv_plan_gates")
+    arr = (sv_gate_plan_step * max(cnt.value, 1))()
+    order = np.zeros(max(g.size, 1), dtype=np.uint64)
+    _check(lib.sv_plan_gates(n, world, dtype, gp, g.size, arr, cnt.value, ctypes.byref(cnt), order.ctypes.data),
+           "sv_plan_gates")
+    steps = [{f: getattr(arr[i], f) for f, _ in sv_gate_plan_step._fields_} for i in range(cnt.value)]
+    return steps, order[:g.size]
 
 
 def sv_profile(ctx: Ctx, enable: bool) -> None:

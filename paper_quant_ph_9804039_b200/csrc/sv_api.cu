@@ -56,6 +56,8 @@ struct sv_ctx {
     double *d_coefs = nullptr;          // angle-error coefficients of the one-CTA kernel
     size_t coefs_cap = 0;
     double *d_deco = nullptr;           // decoherence: {sum, scale, survival[k]}
+    unsigned char *d_gprog = nullptr;   // gate circuits: op programs of every pass of a call
+    size_t gprog_cap = 0;
     size_t deco_cap = 0;
     double *d_samp = nullptr;           // sampler: chunk prefixes + rank totals + window
     uint64_t *d_shots = nullptr;        // sampler: device output for host-returning calls
@@ -353,6 +355,95 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle, const Noise *noise = n
     }
 }
 
+// Gate circuit (NEXT-4): the planned passes (gate_plan.cpp) and qubit swaps.
+// All passes' op programs are built on the host and uploaded once, then the
+// passes run back to back on the stream.  Buffers as in run_wht_schedule:
+// unfused, a swap is an all-to-all state -> recv and the next pass reads recv
+// and writes state; fused, the pass before a swap stores every element into
+// its new owner's other buffer and the swap is a barrier.
+void run_gates(sv_ctx *c, const sv_gate *gates, uint64_t count) {
+    const GatePlan gp = plan_gates(c->n, c->g, c->dt, gates, count);
+    if (gp.steps.empty()) return;
+    const int total_bits = c->emulated ? c->n : gp.nl;
+    auto args = [&](const GateStep &st) {
+        GatePassArgs a;
+        a.tile_mask = st.tile;
+        a.total_bits = total_bits;
+        a.g = gp.g;
+        a.rank = c->rank;
+        a.emulated = c->emulated ? 1 : 0;
+        a.swapped = st.swapped;
+        a.n = gp.n;
+        a.nl = gp.nl;
+        a.gates = gates;
+        a.order = gp.order.data() + st.first;
+        a.count = st.count;
+        return a;
+    };
+    std::vector<unsigned char> prog;
+    std::vector<std::pair<size_t, uint64_t>> where(gp.steps.size(), {0, 0});
+    for (size_t i = 0; i < gp.steps.size(); ++i) {
+        const GateStep &st = gp.steps[i];
+        if (st.kind == GSTEP_SWAP) continue;
+        const size_t off = (prog.size() + 15) & ~(size_t)15;
+        where[i] = {off, build_gate_ops(c->dt, args(st), st.kind == GSTEP_WHOLE, prog)};
+    }
+    if (prog.size() > c->gprog_cap) {
+        if (c->d_gprog) SV_CUDA(cudaFree(c->d_gprog));
+        c->d_gprog = nullptr;
+        c->gprog_cap = 0;
+        dmalloc((void **)&c->d_gprog, prog.size(), "gate program");
+        c->gprog_cap = prog.size();
+    }
+    if (!prog.empty())
+        SV_CUDA(cudaMemcpyAsync(c->d_gprog, prog.data(), prog.size(), cudaMemcpyHostToDevice, c->stream));
+    void *cur = c->state, *next = nullptr;
+    for (size_t i = 0; i < gp.steps.size(); ++i) {
+        const GateStep &st = gp.steps[i];
+        if (st.kind == GSTEP_SWAP) {
+            if (c->fused_xchg && next != nullptr) {
+                xchg_barrier(c);
+                cur = next;
+                next = nullptr;
+            } else {  // unfused, or a swap with no pass before it to carry it
+                if (cur != c->state)
+                    SV_CUDA(cudaMemcpyAsync(c->state, cur, c->nres * elem_bytes(c->dt), cudaMemcpyDeviceToDevice,
+                                            c->stream));
+                exchange(c);
+                cur = c->recv;
+            }
+            continue;
+        }
+        GatePassArgs a = args(st);
+        const void *ops = c->d_gprog + where[i].first;
+        if (st.kind == GSTEP_WHOLE) {
+            a.in = c->state;
+            run(c, SV_K_GATE_TILE, [&] { launch_gate_whole(c->dt, a, ops, where[i].second, c->stream); });
+            continue;
+        }
+        a.in = cur;
+        a.out = c->fused_xchg ? cur : c->state;
+        const bool pre_swap = i + 1 < gp.steps.size() && gp.steps[i + 1].kind == GSTEP_SWAP;
+        if (c->fused_xchg && pre_swap) {
+            const bool to_recv = (cur == c->state);
+            next = to_recv ? c->recv : c->state;
+            a.xchg_nl = gp.nl;
+            a.xchg_g = c->g;
+            a.xchg_rank = c->emulated ? -1 : c->rank;
+            for (int j = 0; j < (1 << c->g); ++j) {
+                if (c->emulated)
+                    a.xchg_dst[j] = (char *)next + (size_t)j * c->nl_amps * elem_bytes(c->dt);
+                else
+                    a.xchg_dst[j] = to_recv ? c->peer_recv[j] : c->peer_state[j];
+            }
+        }
+        run(c, SV_K_GATE_TILE, [&] { launch_gate_pass(c->dt, a, ops, where[i].second, c->stream); });
+        if (!c->fused_xchg) cur = c->state;
+    }
+    if (cur != c->state)
+        SV_CUDA(cudaMemcpyAsync(c->state, cur, c->nres * elem_bytes(c->dt), cudaMemcpyDeviceToDevice, c->stream));
+}
+
 MeanArgs mean_args(sv_ctx *c, bool with_oracle) {
     MeanArgs m;
     m.a = c->state;
@@ -537,6 +628,7 @@ void destroy(sv_ctx *c) {
     cudaFree(c->d_coefs);
     cudaFree(c->d_samp);
     cudaFree(c->d_deco);
+    cudaFree(c->d_gprog);
     cudaFree(c->d_shots);
     if (c->comm) ncclCommDestroy(c->comm);
     cudaFree(c->state);
@@ -905,6 +997,38 @@ sv_status sv_plan_wht(int n, int world, sv_dtype dtype, int k, int with_oracle, 
             o.tile_mask = (s.group >= 0) ? p.groups[s.group].tile : 0;
             o.proc_mask = (s.group >= 0) ? p.groups[s.group].proc : 0;
         }
+    });
+}
+
+sv_status sv_apply_gates(sv_ctx *c, const sv_gate *gates, uint64_t count) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CUDA(cudaSetDevice(c->device));
+        run_gates(c, gates, count);
+    });
+}
+
+sv_status sv_plan_gates(int n, int world, sv_dtype dtype, const sv_gate *gates, uint64_t count,
+                        sv_gate_plan_step *out, int cap, int *nsteps, uint64_t *order) {
+    return guarded([&] {
+        SV_CHECK(world >= 1 && (world & (world - 1)) == 0, SV_EINVAL, "world must be a power of two");
+        int g = 0;
+        while ((1 << g) < world) ++g;
+        SV_CHECK(g <= n, SV_EINVAL, "world larger than 2^n");
+        const GatePlan gp = plan_gates(n, g, dtype, gates, count);
+        if (nsteps) *nsteps = (int)gp.steps.size();
+        for (int i = 0; i < (int)gp.steps.size() && i < cap && out; ++i) {
+            const GateStep &s = gp.steps[i];
+            sv_gate_plan_step &o = out[i];
+            o.kind = s.kind;
+            o.tile_bits = s.kind == GSTEP_WHOLE ? n : gp.T;
+            o.tile_mask = s.tile;
+            o.proc_mask = s.proc;
+            o.first = s.first;
+            o.count = s.count;
+        }
+        if (order)
+            for (size_t j = 0; j < gp.order.size(); ++j) order[j] = gp.order[j];
     });
 }
 

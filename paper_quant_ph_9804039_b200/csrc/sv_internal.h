@@ -101,6 +101,62 @@ Plan make_plan(int n, int g, sv_dtype dtype);
 std::vector<Step> schedule_wht(const Plan &plan, int k, bool with_oracle);
 
 // ------------------------------------------------------------------------- //
+// Gate circuits (gate_plan.cpp)                          //
+// ------------------------------------------------------------------------- //
+enum GateStepKind { GSTEP_PASS = 0, GSTEP_SWAP = 1, GSTEP_WHOLE = 2 };
+
+struct GateStep {
+    int kind = GSTEP_PASS;
+    uint64_t proc = 0;   // physical slots targeted by the pass's gates
+    uint64_t tile = 0;   // physical slots of one tile (popcount == T)
+    int swapped = 0;     // layout during the pass: 0 natural, 1 top-g local <-> rank bits
+    uint64_t first = 0;  // gates order[first .. first + count)
+    uint64_t count = 0;
+};
+
+struct GatePlan {
+    int n = 0, nl = 0, g = 0, T = 0;
+    std::vector<GateStep> steps;
+    std::vector<uint64_t> order;   // gate indices in execution order
+};
+
+// Validates every gate (throws Error{SV_EINVAL}) and builds the schedule.
+GatePlan plan_gates(int n, int g, sv_dtype dtype, const sv_gate *gates, uint64_t count);
+// Physical slot of logical qubit q in layout `swapped` (section 3.1 swap of
+// the top-g local slots [nl-g, nl) with the rank bits [nl, n)).
+inline int gate_phys(int q, int nl, int g, int swapped) {
+    if (!swapped) return q;
+    if (q >= nl) return q - g;
+    if (q >= nl - g) return q + g;
+    return q;
+}
+
+// One gate-circuit tile pass / the whole-state gate kernel (gates.cu).
+struct GatePassArgs {
+    void *in = nullptr;
+    void *out = nullptr;
+    uint64_t tile_mask = 0;       // physical slots of a tile
+    int total_bits = 0;           // index bits of the launched buffer
+    int g = 0;                    // rank bits
+    int rank = 0;                 // own rank (real) -- controls on rank bits are decided on the host
+    int emulated = 0;
+    int swapped = 0;
+    int n = 0, nl = 0;
+    const sv_gate *gates = nullptr;  // host
+    const uint64_t *order = nullptr; // host: this pass's gate indices (execution order)
+    uint64_t count = 0;
+    // fused qubit-swap exchange as in PassArgs
+    int xchg_nl = 0, xchg_g = 0, xchg_rank = -1;
+    void *xchg_dst[8] = {};
+};
+// Append the op program of one pass (whole: the one-CTA kernel) to `prog`
+// (16-byte aligned records); returns the op count.  Ops whose rank-bit
+// controls fail on this rank are dropped.
+uint64_t build_gate_ops(sv_dtype dt, const GatePassArgs &a, bool whole, std::vector<unsigned char> &prog);
+void launch_gate_pass(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, uint64_t nops, cudaStream_t s);
+void launch_gate_whole(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, uint64_t nops, cudaStream_t s);
+
+// ------------------------------------------------------------------------- //
 // Kernel launchers (wht.cu, mean.cu, misc.cu)                                //
 // ------------------------------------------------------------------------- //
 struct PassArgs {
