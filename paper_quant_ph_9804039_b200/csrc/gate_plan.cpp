@@ -10,9 +10,8 @@
 //
 // Order: gates are taken greedily left to right.  A later gate may join the
 // current pass ahead of gates it skips only if it commutes with every skipped
-// gate (sufficient condition: different targets and neither gate's target is
-// a control of the other), so the result is the circuit's product exactly
-// (up to rounding order).
+// gate (CommuteSet: sufficient conditions), so the result is the circuit's
+// product exactly (up to rounding order).
 //
 // Sharding (section 3.1): "All of the processors can run in
 // parallel operating only on local data as long as they do not use any of
@@ -77,7 +76,8 @@ GatePlan plan_gates(int n, int g, sv_dtype dtype, const sv_gate *gates, uint64_t
         s.kind = GSTEP_PASS;
         s.swapped = swapped;
         s.first = p.order.size();
-        uint64_t proc = 0, st = 0, sc = 0;  // skipped gates: targets, controls (logical)
+        uint64_t proc = 0;
+        CommuteSet skipped;  // gates left for a later pass (logical qubits)
         next.clear();
         for (size_t k = 0; k < pending.size(); ++k) {
             const uint64_t j = pending[k];
@@ -86,9 +86,8 @@ GatePlan plan_gates(int n, int g, sv_dtype dtype, const sv_gate *gates, uint64_t
                 continue;
             }
             const sv_gate &gt = gates[j];
-            const uint64_t tb = 1ull << gt.target;
             const int pt = gate_phys(gt.target, nl, g, swapped);
-            bool ok = pt < nl && !(tb & (st | sc)) && !(gt.controls & st);
+            bool ok = pt < nl && skipped.commutes(gt);
             if (ok) {
                 const uint64_t np = proc | (1ull << pt);
                 ok = __builtin_popcountll(np | carry) <= T;
@@ -99,8 +98,7 @@ GatePlan plan_gates(int n, int g, sv_dtype dtype, const sv_gate *gates, uint64_t
             }
             if (!ok) {
                 next.push_back(j);
-                st |= tb;
-                sc |= gt.controls;
+                skipped.add(gt);
             }
         }
         s.count = p.order.size() - s.first;

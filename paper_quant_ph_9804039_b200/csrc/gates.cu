@@ -33,11 +33,23 @@ namespace sv {
 template <typename R>
 struct alignas(16) GOp {
     R m[8];                  // w, x, y, z as (re, im)
-    unsigned int ph;         // register layout (0 = A, 1 = B, 2 = C)
+    unsigned int ph;         // register layout (0 = A, 1 = B, 2 = C) | kind << 8
     unsigned int ri;         // register index of the target tile bit (whole kernel: target slot)
     unsigned int jm;         // controls that are register bits of ph (register-index space)
     unsigned int tm;         // controls that are thread bits of ph (tile-element space)
     unsigned long long fm;   // controls outside the tile (local index space; whole kernel: all controls)
+};
+
+// Matrix shape, decided on the host from the exact coefficients: the same
+// [w x; y z] product with the zero terms (and unit factors) skipped, so the
+// result is identical to the general formula up to the rounding of the
+// skipped exact zeros / ones.
+enum GateKind : unsigned int {
+    GK_GENERAL = 0,   // [w x; y z]
+    GK_DIAG = 1,      // x = y = 0: (w u, z v)
+    GK_PHASE = 2,     // x = y = 0, w = 1: (u, z v)
+    GK_ANTI = 3,      // w = z = 0: (x v, y u)
+    GK_SWAP = 4,      // w = z = 0, x = y = 1 (NOT): (v, u)
 };
 
 // (u, v) <- (w u + x v, y u + z v), complex.
@@ -50,23 +62,65 @@ __device__ __forceinline__ void cmat(E &u, E &v, const R (&m)[8]) {
     v.y = m[4] * a.y + m[5] * a.x + m[6] * b.y + m[7] * b.x;
 }
 
-template <int I, int NR, typename E, typename R>
+// c <- (re, im) * c, complex
+template <typename E, typename R>
+__device__ __forceinline__ void cscale(E &c, R re, R im) {
+    const E a = c;
+    c.x = re * a.x - im * a.y;
+    c.y = re * a.y + im * a.x;
+}
+
+template <unsigned int K, typename E, typename R>
+__device__ __forceinline__ void cmat_k(E &u, E &v, const R (&m)[8]) {
+    if constexpr (K == GK_GENERAL) {
+        cmat(u, v, m);
+    } else if constexpr (K == GK_DIAG) {
+        cscale(u, m[0], m[1]);
+        cscale(v, m[6], m[7]);
+    } else if constexpr (K == GK_PHASE) {
+        cscale(v, m[6], m[7]);
+    } else if constexpr (K == GK_ANTI) {
+        const E a = u, b = v;
+        u.x = m[2] * b.x - m[3] * b.y;
+        u.y = m[2] * b.y + m[3] * b.x;
+        v.x = m[4] * a.x - m[5] * a.y;
+        v.y = m[4] * a.y + m[5] * a.x;
+    } else {
+        const E a = u;
+        u = v;
+        v = a;
+    }
+}
+
+template <int I, unsigned int K, int NR, typename E, typename R>
 __device__ __forceinline__ void gate_apply(E (&x)[NR], const R (&m)[8], unsigned int jm) {
 #pragma unroll
     for (int j = 0; j < NR; ++j)
         if (!(j & (1 << I)))
-            if (((unsigned int)j & jm) == jm) cmat(x[j], x[j | (1 << I)], m);
+            if (((unsigned int)j & jm) == jm) cmat_k<K>(x[j], x[j | (1 << I)], m);
+}
+
+template <int I, int NR, typename E, typename R>
+__device__ __forceinline__ void gate_apply_kind(E (&x)[NR], const R (&m)[8], unsigned int jm, unsigned int kind) {
+    switch (kind) {
+        case GK_DIAG: gate_apply<I, GK_DIAG>(x, m, jm); break;
+        case GK_PHASE: gate_apply<I, GK_PHASE>(x, m, jm); break;
+        case GK_ANTI: gate_apply<I, GK_ANTI>(x, m, jm); break;
+        case GK_SWAP: gate_apply<I, GK_SWAP>(x, m, jm); break;
+        default: gate_apply<I, GK_GENERAL>(x, m, jm); break;
+    }
 }
 
 template <class L, typename E, typename R>
-__device__ __forceinline__ void gate_dispatch(E (&x)[L::NR], const R (&m)[8], unsigned int ri, unsigned int jm) {
+__device__ __forceinline__ void gate_dispatch(E (&x)[L::NR], const R (&m)[8], unsigned int ri, unsigned int jm,
+                                              unsigned int kind) {
     switch (ri) {
-        case 0: gate_apply<0>(x, m, jm); break;
-        case 1: gate_apply<1>(x, m, jm); break;
-        case 2: gate_apply<2>(x, m, jm); break;
-        case 3: gate_apply<3>(x, m, jm); break;
+        case 0: gate_apply_kind<0>(x, m, jm, kind); break;
+        case 1: gate_apply_kind<1>(x, m, jm, kind); break;
+        case 2: gate_apply_kind<2>(x, m, jm, kind); break;
+        case 3: gate_apply_kind<3>(x, m, jm, kind); break;
         default:
-            if constexpr (L::kRB > 4) gate_apply<(L::kRB > 4 ? 4 : 0)>(x, m, jm);
+            if constexpr (L::kRB > 4) gate_apply_kind<(L::kRB > 4 ? 4 : 0)>(x, m, jm, kind);
             break;
     }
 }
@@ -116,12 +170,14 @@ __global__ void __launch_bounds__(1 << (TB - RB), 2)
         unsigned int ph, ri, jm, tm;
         unsigned long long fm;
         load_op(ops + k, m, ph, ri, jm, tm, fm);
+        const unsigned int kind = ph >> 8;
+        ph &= 0xffu;
         if (ph != cur) {
             relayout_dyn<L>(x, sm, tid, cur, ph);
             cur = ph;
         }
         const unsigned int et = cur == 0 ? eth[0] : (cur == 1 ? eth[1] : eth[2]);
-        if ((et & tm) == tm && (base & fm) == fm) gate_dispatch<L>(x, m, ri, jm);
+        if ((et & tm) == tm && (base & fm) == fm) gate_dispatch<L>(x, m, ri, jm, kind);
     }
     E *gout = reinterpret_cast<E *>(p.out) + base;
     if (cur == 0) pass_store<L, 0>(x, gout, base, p, tid, s_dst);
@@ -145,10 +201,19 @@ __global__ void __launch_bounds__(512) gate_whole_kernel(E *a, int n, const GOp<
         unsigned int ph, q, jm, tm;
         unsigned long long cm;
         load_op(ops + k, m, ph, q, jm, tm, cm);
+        const unsigned int kind = ph >> 8;
         const unsigned int bit = 1u << q;
         for (unsigned int pr = tid; pr < N / 2; pr += nt) {
             const unsigned int i = ((pr >> q) << (q + 1)) | (pr & (bit - 1));
-            if ((i & (unsigned int)cm) == (unsigned int)cm) cmat(s[i], s[i | bit], m);
+            if ((i & (unsigned int)cm) == (unsigned int)cm) {
+                switch (kind) {
+                    case GK_DIAG: cmat_k<GK_DIAG>(s[i], s[i | bit], m); break;
+                    case GK_PHASE: cmat_k<GK_PHASE>(s[i], s[i | bit], m); break;
+                    case GK_ANTI: cmat_k<GK_ANTI>(s[i], s[i | bit], m); break;
+                    case GK_SWAP: cmat_k<GK_SWAP>(s[i], s[i | bit], m); break;
+                    default: cmat_k<GK_GENERAL>(s[i], s[i | bit], m); break;
+                }
+            }
         }
         __syncthreads();
     }
@@ -160,10 +225,20 @@ __global__ void __launch_bounds__(512) gate_whole_kernel(E *a, int n, const GOp<
 // ------------------------------------------------------------------------- //
 namespace {
 
+unsigned int gate_kind(const sv_gate &g) {
+    const double *m = g.m;
+    const bool offzero = m[2] == 0.0 && m[3] == 0.0 && m[4] == 0.0 && m[5] == 0.0;
+    const bool diagzero = m[0] == 0.0 && m[1] == 0.0 && m[6] == 0.0 && m[7] == 0.0;
+    if (offzero) return (m[0] == 1.0 && m[1] == 0.0) ? GK_PHASE : GK_DIAG;
+    if (diagzero) return (m[2] == 1.0 && m[3] == 0.0 && m[4] == 1.0 && m[5] == 0.0) ? GK_SWAP : GK_ANTI;
+    return GK_GENERAL;
+}
+
 template <typename R>
 GOp<R> op_coefs(const sv_gate &g) {
     GOp<R> o{};
     for (int e = 0; e < 8; ++e) o.m[e] = (R)g.m[e];
+    o.ph = gate_kind(g) << 8;
     return o;
 }
 
@@ -177,18 +252,17 @@ void build_tile_ops(const GatePassArgs &a, std::vector<GOp<R>> &out) {
     for (int sl = 0; sl < 64; ++sl)
         if ((a.tile_mask >> sl) & 1) slot2bit[sl] = b++;
     struct Pend {
-        uint64_t j;          // gate index
+        sv_gate g;           // the gate (matrix possibly fused with later ones)
         int bt;              // target tile bit
         unsigned int tc;     // controls on tile bits (tile-element space)
         unsigned long long fm;
     };
     std::vector<Pend> pend;
     for (uint64_t k = 0; k < a.count; ++k) {
-        const uint64_t j = a.order[k];
-        const sv_gate &g = a.gates[j];
+        const sv_gate &g = a.gates[a.order[k]];
         const int pt = gate_phys(g.target, a.nl, a.g, a.swapped);
         SV_CHECK(slot2bit[pt] >= 0, SV_EINVAL, "internal: gate target outside its pass tile");
-        Pend pd{j, slot2bit[pt], 0u, 0ull};
+        Pend pd{g, slot2bit[pt], 0u, 0ull};
         bool live = true;
         for (int q = 0; q < a.n; ++q) {
             if (!((g.controls >> q) & 1ull)) continue;
@@ -201,24 +275,49 @@ void build_tile_ops(const GatePassArgs &a, std::vector<GOp<R>> &out) {
                 pd.fm |= 1ull << pq;
             }
         }
-        if (live) pend.push_back(pd);
+        if (!live) continue;
+        // Fusion: a gate with the same target and controls as an earlier op
+        // of this pass, with only commuting ops in between, is multiplied
+        // into it (host fp64 2x2 product M_later * M_earlier).
+        bool fused = false;
+        CommuteSet between;
+        for (size_t i = pend.size(); i-- > 0;) {
+            sv_gate &e = pend[i].g;
+            if (e.target == g.target && e.controls == g.controls && between.commutes(g)) {
+                double r[8];
+                for (int rr = 0; rr < 2; ++rr)
+                    for (int cc = 0; cc < 2; ++cc) {
+                        double re = 0.0, im = 0.0;
+                        for (int kk = 0; kk < 2; ++kk) {
+                            const double ar = g.m[2 * (2 * rr + kk)], ai = g.m[2 * (2 * rr + kk) + 1];
+                            const double br = e.m[2 * (2 * kk + cc)], bi = e.m[2 * (2 * kk + cc) + 1];
+                            re += ar * br - ai * bi;
+                            im += ar * bi + ai * br;
+                        }
+                        r[2 * (2 * rr + cc)] = re;
+                        r[2 * (2 * rr + cc) + 1] = im;
+                    }
+                for (int t = 0; t < 8; ++t) e.m[t] = r[t];
+                fused = true;
+                break;
+            }
+            between.add(e);
+            if (!between.commutes(g)) break;
+        }
+        if (!fused) pend.push_back(pd);
     }
     // Layout schedule: in the current layout run every ready op (commutes
     // with all earlier pending ops) whose target is a register bit; when none
     // is left, move to the layout that runs the most ready ops next.
     auto ready_in = [&](int ph, std::vector<size_t> *take) {
-        uint64_t st = 0, sc = 0;
+        CommuteSet skipped;
         int cnt = 0;
         for (size_t i = 0; i < pend.size(); ++i) {
-            const sv_gate &g = a.gates[pend[i].j];
-            const uint64_t tb = 1ull << g.target;
-            const bool ready = !(tb & (st | sc)) && !(g.controls & st);
-            if (ready && L::is_reg(ph, pend[i].bt)) {
+            if (skipped.commutes(pend[i].g) && L::is_reg(ph, pend[i].bt)) {
                 ++cnt;
                 if (take) take->push_back(i);
             } else {
-                st |= tb;
-                sc |= g.controls;
+                skipped.add(pend[i].g);
             }
         }
         return cnt;
@@ -242,8 +341,8 @@ void build_tile_ops(const GatePassArgs &a, std::vector<GOp<R>> &out) {
         std::vector<char> used(pend.size(), 0);
         for (size_t i : take) {
             const Pend &pd = pend[i];
-            GOp<R> o = op_coefs<R>(a.gates[pd.j]);
-            o.ph = (unsigned int)cur;
+            GOp<R> o = op_coefs<R>(pd.g);
+            o.ph |= (unsigned int)cur;
             o.ri = 0;
             for (int r = 0; r < L::kRB; ++r)
                 if (L::reg_bit(cur, r) == pd.bt) o.ri = (unsigned int)r;

@@ -131,6 +131,32 @@ inline int gate_phys(int q, int nl, int g, int swapped) {
     return q;
 }
 
+// x = y = 0 exactly: the gate is diagonal (a phase on each basis state).
+inline bool gate_diag(const sv_gate &g) { return g.m[2] == 0.0 && g.m[3] == 0.0 && g.m[4] == 0.0 && g.m[5] == 0.0; }
+
+// Gates a later gate must commute with to be moved ahead of them (sufficient
+// conditions).  A controlled 2x2 is P0 (x) I + P1 (x) U on its controls:
+//  * two non-diagonal gates commute if the targets differ and neither target
+//    is a control of the other;
+//  * a diagonal gate D commutes with any gate whose target is outside D's
+//    support (target + controls): D commutes with the control projectors;
+//  * two diagonal gates always commute.
+struct CommuteSet {
+    uint64_t tnd = 0;   // targets of non-diagonal gates
+    uint64_t cnd = 0;   // controls of non-diagonal gates
+    uint64_t sd = 0;    // supports of diagonal gates
+    void add(const sv_gate &g) {
+        const uint64_t t = 1ull << g.target;
+        if (gate_diag(g)) sd |= t | g.controls;
+        else { tnd |= t; cnd |= g.controls; }
+    }
+    bool commutes(const sv_gate &g) const {
+        const uint64_t t = 1ull << g.target;
+        if (gate_diag(g)) return !((t | g.controls) & tnd);
+        return !(t & (tnd | cnd | sd)) && !(g.controls & tnd);
+    }
+};
+
 // One gate-circuit tile pass / the whole-state gate kernel (gates.cu).
 struct GatePassArgs {
     void *in = nullptr;

@@ -115,3 +115,51 @@ def grover_circuit(n: int, marked: int, k: int, prepare: bool = True) -> np.ndar
         out += [record(q, X) for q in range(n)]
         out += [record(q, H) for q in range(n)]
     return circuit(out)
+
+
+def structured_circuit(n: int, count: int, seed: int, max_controls: int = 2) -> np.ndarray:
+    """Gates drawn from the special shapes the engine treats specially and
+    the general case: X (NOT), Y (anti-diagonal), Z / S / T / phase(theta)
+    (phase: w = 1), diag(e^{ia}, e^{ib}), H and random unitaries, each with
+    0..max_controls random controls."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        t = int(rng.integers(0, n))
+        kind = int(rng.integers(0, 8))
+        if kind == 0:
+            m = X
+        elif kind == 1:
+            m = Y
+        elif kind == 2:
+            m = Z
+        elif kind == 3:
+            m = phase(float(rng.uniform(-math.pi, math.pi)))
+        elif kind == 4:
+            a, b = rng.uniform(-math.pi, math.pi, 2)
+            m = np.diag([np.exp(1j * a), np.exp(1j * b)])
+        elif kind == 5:
+            a, b = rng.uniform(-math.pi, math.pi, 2)
+            m = np.array([[0, np.exp(1j * a)], [np.exp(1j * b), 0]])
+        elif kind == 6:
+            m = H
+        else:
+            m = random_unitary(rng)
+        ctr = []
+        if max_controls > 0 and n > 1:
+            k = int(rng.integers(0, min(max_controls, n - 1) + 1))
+            others = [q for q in range(n) if q != t]
+            ctr = [int(c) for c in rng.choice(others, size=k, replace=False)]
+        out.append(record(t, m, ctr))
+    return circuit(out)
+
+
+def layered_circuit(n: int, layers: int, seed: int) -> np.ndarray:
+    """Hardware-efficient-ansatz-like layers: a random unitary on every qubit,
+    then a CZ (controlled-Z) chain q -> q+1."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(layers):
+        out += [record(q, random_unitary(rng)) for q in range(n)]
+        out += [record(q + 1, Z, [q]) for q in range(n - 1)]
+    return circuit(out)

@@ -70,6 +70,43 @@ def test_random_circuit_matches_oracle(dtype, n, count, seed):
 
 
 @pytest.mark.parametrize("dtype", DT, ids=DT_IDS)
+@pytest.mark.parametrize("n,count,seed", [(6, 80, 11), (13, 200, 12), (16, 300, 13), (22, 200, 14)])
+def test_structured_gate_shapes_match_oracle(dtype, n, count, seed):
+    # X / Y / Z / phase / diagonal / anti-diagonal / H / general, with controls
+    gates = C.structured_circuit(n, count, seed, max_controls=3)
+    a = rand_state(n, dtype, 200 + seed)
+    ref = orc.apply_gates(a.copy(), gates)
+    assert_close(run_gpu(a, dtype, gates), ref, dtype, count, f"structured n={n} G={count}")
+
+
+@pytest.mark.parametrize("dtype", DT, ids=DT_IDS)
+def test_fusable_runs_match_oracle(dtype):
+    # same-target same-control gates separated by commuting gates are fused
+    # into one 2x2 on the host; separated by a non-commuting gate they are not
+    n = 18
+    rng = np.random.default_rng(3)
+    recs = []
+    for _ in range(6):
+        for q in (0, 5, 11, 17):
+            recs.append(C.record(q, C.random_unitary(rng), [3] if q != 3 else []))
+        recs.append(C.record(9, C.phase(0.3), [0]))       # diagonal: blocks fusion on 0 and 9 only
+        recs.append(C.record(5, C.X, [11]))               # non-diagonal on 5 controlled by 11
+    gates = C.circuit(recs + [C.record(q, C.H) for q in range(n)] * 3)
+    a = rand_state(n, dtype, 4)
+    ref = orc.apply_gates(a.copy(), gates)
+    assert_close(run_gpu(a, dtype, gates), ref, dtype, gates.size, "fusable runs")
+
+
+@pytest.mark.parametrize("dtype", DT, ids=DT_IDS)
+def test_layered_circuit_matches_oracle(dtype):
+    n = 20
+    gates = C.layered_circuit(n, 4, 21)
+    a = rand_state(n, dtype, 22)
+    ref = orc.apply_gates(a.copy(), gates)
+    assert_close(run_gpu(a, dtype, gates), ref, dtype, gates.size, "layered n=20")
+
+
+@pytest.mark.parametrize("dtype", DT, ids=DT_IDS)
 def test_many_gates_on_few_qubits_one_pass(dtype):
     # 400 gates on 10 qubits: one tile pass with a long op program and relayouts
     n = 20
