@@ -150,15 +150,15 @@ __device__ __forceinline__ void load_op(const GOp<R> *op, R (&m)[8], unsigned in
     fm = __ldg(&op->fm);
 }
 
-template <typename E, int TB, int RB>
+template <typename E, int TB, int RB, bool XCHG>
 __global__ void __launch_bounds__(1 << (TB - RB), 2)
     gate_tile_kernel(const KParams p, const GOp<typename RealOf<E>::T> *__restrict__ ops, int nops) {
     using L = Layout<E, TB, RB>;
     using R = typename RealOf<E>::T;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     E *sm = reinterpret_cast<E *>(smem_raw);
-    __shared__ E *s_dst[8];
-    load_xdst(p, threadIdx.x, s_dst);
+    __shared__ E *s_dst[XCHG ? 8 : 1];
+    if constexpr (XCHG) load_xdst(p, threadIdx.x, s_dst);
     const int tid = threadIdx.x;
     const unsigned long long base = tile_base(blockIdx.x, p.free_mask);
     E x[L::NR];
@@ -180,9 +180,9 @@ __global__ void __launch_bounds__(1 << (TB - RB), 2)
         if ((et & tm) == tm && (base & fm) == fm) gate_dispatch<L>(x, m, ri, jm, kind);
     }
     E *gout = reinterpret_cast<E *>(p.out) + base;
-    if (cur == 0) pass_store<L, 0>(x, gout, base, p, tid, s_dst);
-    else if (cur == 1) pass_store<L, 1>(x, gout, base, p, tid, s_dst);
-    else pass_store<L, 2>(x, gout, base, p, tid, s_dst);
+    if (cur == 0) pass_store<L, 0, XCHG>(x, gout, base, p, tid, s_dst);
+    else if (cur == 1) pass_store<L, 1, XCHG>(x, gout, base, p, tid, s_dst);
+    else pass_store<L, 2, XCHG>(x, gout, base, p, tid, s_dst);
 }
 
 // Whole state (n <= T) in one CTA: every gate as a V/2-pair loop over shared
@@ -405,11 +405,14 @@ void launch_tile_gates(const GatePassArgs &a, const void *dev_ops, uint64_t nops
     SV_CHECK(nops <= 0x7fffffffull, SV_EINVAL, "too many gates in one pass");
     const unsigned long long ntiles = 1ull << f;
     SV_CHECK(ntiles <= 0x7fffffffull, SV_EINVAL, "too many tiles for one launch");
-    auto fn = gate_tile_kernel<E, TB, RB>;
+    auto fn = kp.xchg ? gate_tile_kernel<E, TB, RB, true> : gate_tile_kernel<E, TB, RB, false>;
     const int smem = (1 << TB) * (int)sizeof(E);
     static bool attr = false;
     if (!attr) {
-        SV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        SV_CUDA(cudaFuncSetAttribute(gate_tile_kernel<E, TB, RB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     smem));
+        SV_CUDA(cudaFuncSetAttribute(gate_tile_kernel<E, TB, RB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     smem));
         attr = true;
     }
     fn<<<(unsigned int)ntiles, L::NT, smem, s>>>(kp, reinterpret_cast<const GOp<R> *>(dev_ops), (int)nops);

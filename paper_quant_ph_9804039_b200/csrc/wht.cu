@@ -8,12 +8,13 @@
 
 namespace sv {
 
-template void launch_tile_dispatch<false>(sv_dtype, const KParams &, int, int, int, unsigned long long,
+template void launch_tile_dispatch<false>(sv_dtype, const KParamsT<false> &, int, int, int, unsigned long long,
                                           cudaStream_t);
 
 void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
     const int TB = tile_bits(dt);
     KParams kp{};
+    KParamsT<true> kc{};  // coefficients of the general-2x2 flavour
     kp.in = a.in;
     kp.out = a.out;
     kp.marked = reinterpret_cast<const unsigned long long *>(a.marked);
@@ -22,6 +23,7 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
     kp.f0_scale = a.f0_scale;
     kp.mid = a.mid;
     kp.has_origin = a.has_origin;
+    SV_CHECK(a.scale_in == nullptr || a.noisy, SV_EINVAL, "internal: scale_in needs the general-2x2 kernels");
     kp.scale_in = a.scale_in;
     kp.xchg = a.xchg_nl > 0 ? 1 : 0;
     if (kp.xchg) {
@@ -41,7 +43,7 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
             if ((a.proc_mask >> sl) & 1) proc |= 1u << b;
             if (a.noisy)
                 for (int h = 0; h < 2; ++h)
-                    for (int e = 0; e < 4; ++e) kp.coef[h][b][e] = a.coef[h][sl][e];
+                    for (int e = 0; e < 4; ++e) kc.coef[h][b][e] = a.coef[h][sl][e];
             kp.slot[b++] = (signed char)sl;
         } else {
             kp.free_mask |= 1ull << sl;
@@ -59,9 +61,18 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
     while (u < TB && !((proc >> u) & 1u)) ++u;
     SV_CHECK(u < TB && proc == (((1u << TB) - 1u) & ~((1u << u) - 1u)), SV_EINVAL,
              "internal: processed tile bits are not the top ones");
+    // u == 0 kernels assume the contiguous tile (slots [0, T), tile t at t * 2^T)
+    SV_CHECK(u != 0 || (a.tile_mask == (1ull << TB) - 1ull && kp.free_mask == ((~0ull >> (64 - a.total_bits)) & ~((1ull << TB) - 1ull))),
+             SV_EINVAL, "internal: a fully processed tile must be the contiguous one");
     const unsigned long long ntiles = 1ull << f;
-    if (a.noisy) launch_tile_dispatch<true>(dt, kp, a.pre, a.post, u, ntiles, s);
-    else launch_tile_dispatch<false>(dt, kp, a.pre, a.post, u, ntiles, s);
+    if (a.noisy) {
+        static_cast<KParams &>(kc) = kp;
+        launch_tile_dispatch<true>(dt, kc, a.pre, a.post, u, ntiles, s);
+    } else {
+        KParamsT<false> ki{};
+        static_cast<KParams &>(ki) = kp;
+        launch_tile_dispatch<false>(dt, ki, a.pre, a.post, u, ntiles, s);
+    }
 }
 
 // ------------------------------------------------------------------------- //

@@ -165,11 +165,20 @@ struct KParams {
     // fused qubit-swap exchange (global_store_xchg): 0 = plain store
     int xchg, xnl, xg, xrank;      // local index bits, rank bits, own rank (-1: emulated)
     void *xdst[8];                 // destination buffer of each rank
-    // general 2x2 stages (NEXT-1/2): per half (0 = before the op, 1 = after)
-    // and tile bit, [w x; y z] row-major
-    double coef[2][16][4];
     const double *scale_in;        // != nullptr: multiply the loaded tile by *scale_in (renormalisation)
 };
+
+// The general-2x2 flavour (NEXT-1/2) carries its per-pass coefficients as
+// kernel parameters: per half (0 = before the op, 1 = after) and tile bit,
+// [w x; y z] row-major.  The ideal flavour's parameter block stays small
+// (measured on B200: the 1 KiB coefficient block in every launch's
+// parameters cost the contiguous c4 pass ~10%).
+template <bool NOISY>
+struct KParamsT : KParams {
+    double coef[2][16][4];
+};
+template <>
+struct KParamsT<false> : KParams {};
 
 // Publish the exchange destinations in shared memory (constant indices only:
 // a runtime-indexed kernel-parameter array would be copied to local memory).
@@ -257,7 +266,7 @@ __device__ __forceinline__ void scale<float2, float>(float2 &x, float s) {
 // unprocessed slots of a tile are its lowest ones (plan.cpp make_group), so
 // U is a template parameter and the unrolled stage code has no branches.
 template <class L, int PH, int U, bool NOISY, int HALF, typename E>
-__device__ __forceinline__ void run_stages(E (&x)[L::NR], const KParams &p) {
+__device__ __forceinline__ void run_stages(E (&x)[L::NR], const KParamsT<NOISY> &p) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
         if (i < L::kRB) {
@@ -334,23 +343,32 @@ __device__ __forceinline__ float4 ld_stream(const float4 *p) {
 }
 
 // Global offset (elements) of tile element e under the pass's slot map.
-template <class L, int PH>
+// CONTIG: the tile is slots [0, T) (the contiguous group): offsets are
+// compile-time functions of the thread and register bits, no slot map.
+template <class L, int PH, bool CONTIG = false>
 __device__ __forceinline__ unsigned long long goff_thr(const KParams &p, int tid) {
+    if constexpr (CONTIG) return (unsigned long long)L::ethr(PH, (uint32_t)tid);
+    // The slot loads are unconditional (uniform LDCU); a thread-dependent
+    // branch around them made ptxas emit per-thread predicated LDCs through
+    // the indexed constant cache at every CTA start (measured on B200: +11%
+    // on the contiguous c4 pass, whose CTAs are short-lived).
     unsigned long long o = 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i)
-        if (i < (L::kTB - L::kRB))
-            if ((tid >> i) & 1) o += 1ull << p.slot[L::thr_bit(PH, i)];
+        if (i < (L::kTB - L::kRB)) {
+            const unsigned long long stride = 1ull << p.slot[L::thr_bit(PH, i)];
+            o += (unsigned long long)((tid >> i) & 1) * stride;
+        }
     return o;
 }
 
-template <class L, int PH, typename E>
+template <class L, int PH, bool CONTIG = false, typename E>
 __device__ __forceinline__ void global_load(E (&x)[L::NR], const E *g, const KParams &p, int tid) {
-    const unsigned long long t = goff_thr<L, PH>(p, tid);
+    const unsigned long long t = goff_thr<L, PH, CONTIG>(p, tid);
     unsigned long long st[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i)
-        if (i < L::kRB) st[i] = 1ull << p.slot[L::reg_bit(PH, i)];
+        if (i < L::kRB) st[i] = CONTIG ? (1ull << L::reg_bit(PH, i)) : (1ull << p.slot[L::reg_bit(PH, i)]);
     if constexpr (L::VE == 2) {
 #pragma unroll
         for (int v = 0; v < L::NR / 2; ++v) {
@@ -373,13 +391,13 @@ __device__ __forceinline__ void global_load(E (&x)[L::NR], const E *g, const KPa
     }
 }
 
-template <class L, int PH, typename E>
+template <class L, int PH, bool CONTIG = false, typename E>
 __device__ __forceinline__ void global_store(const E (&x)[L::NR], E *g, const KParams &p, int tid) {
-    const unsigned long long t = goff_thr<L, PH>(p, tid);
+    const unsigned long long t = goff_thr<L, PH, CONTIG>(p, tid);
     unsigned long long st[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i)
-        if (i < L::kRB) st[i] = 1ull << p.slot[L::reg_bit(PH, i)];
+        if (i < L::kRB) st[i] = CONTIG ? (1ull << L::reg_bit(PH, i)) : (1ull << p.slot[L::reg_bit(PH, i)]);
     if constexpr (L::VE == 2) {
 #pragma unroll
         for (int v = 0; v < L::NR / 2; ++v) {
@@ -449,15 +467,17 @@ __device__ __forceinline__ void global_store_xchg(const E (&x)[L::NR], unsigned 
 }
 
 // Final store of a pass: plain (in place / to the next pass's buffer) or
-// through the exchange.
-template <class L, int PH, typename E>
+// through the exchange.  XCHG is a template parameter so the plain passes
+// carry no exchange code at all (measured on B200: a runtime branch here cost
+// 10% on every c4 pass).
+template <class L, int PH, bool XCHG, bool CONTIG = false, typename E>
 __device__ __forceinline__ void pass_store(const E (&x)[L::NR], E *gout, unsigned long long base, const KParams &p,
                                            int tid, E *const *sdst) {
-    if (p.xchg) {
-        __syncthreads();  // sdst published (uniform branch)
+    if constexpr (XCHG) {
+        __syncthreads();  // sdst published
         global_store_xchg<L, PH>(x, base, p, tid, sdst);
     } else {
-        global_store<L, PH>(x, gout, p, tid);
+        global_store<L, PH, CONTIG>(x, gout, p, tid);
     }
 }
 
@@ -542,8 +562,8 @@ __device__ __forceinline__ bool oracle_lookup(const KParams &p, unsigned long lo
 
 // Everything after the tile is in registers (layout A): stage sets, the
 // elementwise op, relayouts through `sm`, and the coalesced global store.
-template <class L, bool PRE, bool POST, int U, bool NOISY, typename E>
-__device__ __forceinline__ void tile_body(E (&x)[L::NR], E *sm, const KParams &p, unsigned long long base, E *gout,
+template <class L, bool PRE, bool POST, int U, bool NOISY, bool XCHG, typename E>
+__device__ __forceinline__ void tile_body(E (&x)[L::NR], E *sm, const KParamsT<NOISY> &p, unsigned long long base, E *gout,
                                           int tid, E *const *sdst, bool has_marked, const unsigned long long *s_mlo,
                                           const unsigned long long *s_mcnt) {
     if (PRE) {
@@ -559,9 +579,9 @@ __device__ __forceinline__ void tile_body(E (&x)[L::NR], E *sm, const KParams &p
             run_stages<L, 1, U, NOISY, 1>(x, p);
             relayout<L, 1, 0>(x, sm, tid);
             run_stages<L, 0, U, NOISY, 1>(x, p);
-            pass_store<L, 0>(x, gout, base, p, tid, sdst);
+            pass_store<L, 0, XCHG, (U == 0)>(x, gout, base, p, tid, sdst);
         } else {
-            pass_store<L, 2>(x, gout, base, p, tid, sdst);
+            pass_store<L, 2, XCHG, (U == 0)>(x, gout, base, p, tid, sdst);
         }
     } else {
         if (has_marked) __syncthreads();  // s_mlo / s_mcnt (uniform branch)
@@ -572,17 +592,17 @@ __device__ __forceinline__ void tile_body(E (&x)[L::NR], E *sm, const KParams &p
             run_stages<L, 1, U, NOISY, 1>(x, p);
             relayout<L, 1, 2>(x, sm, tid);
             run_stages<L, 2, U, NOISY, 1>(x, p);
-            pass_store<L, 2>(x, gout, base, p, tid, sdst);
+            pass_store<L, 2, XCHG, (U == 0)>(x, gout, base, p, tid, sdst);
         } else {
-            pass_store<L, 0>(x, gout, base, p, tid, sdst);
+            pass_store<L, 0, XCHG, (U == 0)>(x, gout, base, p, tid, sdst);
         }
     }
 }
 
 // tile_body for the two-layout strided family (Layout2): A -> B stages,
 // the op in B, B -> A stages; without processed bits in B it stays in A.
-template <class L, bool PRE, bool POST, int U, bool NOISY, typename E>
-__device__ __forceinline__ void tile_body2(E (&x)[L::NR], E *sm, const KParams &p, unsigned long long base, E *gout,
+template <class L, bool PRE, bool POST, int U, bool NOISY, bool XCHG, typename E>
+__device__ __forceinline__ void tile_body2(E (&x)[L::NR], E *sm, const KParamsT<NOISY> &p, unsigned long long base, E *gout,
                                            int tid, E *const *sdst, bool has_marked, const unsigned long long *s_mlo,
                                            const unsigned long long *s_mcnt) {
     constexpr bool kNeedB = U < L::kTB - L::kRB;
@@ -602,9 +622,9 @@ __device__ __forceinline__ void tile_body2(E (&x)[L::NR], E *sm, const KParams &
                 relayout<L, 1, 0>(x, sm, tid);
                 run_stages<L, 0, U, NOISY, 1>(x, p);
             }
-            pass_store<L, 0>(x, gout, base, p, tid, sdst);
+            pass_store<L, 0, XCHG>(x, gout, base, p, tid, sdst);
         } else {
-            pass_store<L, kLast>(x, gout, base, p, tid, sdst);
+            pass_store<L, kLast, XCHG>(x, gout, base, p, tid, sdst);
         }
     } else {
         if (has_marked) __syncthreads();
@@ -616,55 +636,62 @@ __device__ __forceinline__ void tile_body2(E (&x)[L::NR], E *sm, const KParams &
                 run_stages<L, 1, U, NOISY, 1>(x, p);
             }
         }
-        pass_store<L, POST ? kLast : 0>(x, gout, base, p, tid, sdst);
+        pass_store<L, POST ? kLast : 0, XCHG>(x, gout, base, p, tid, sdst);
     }
 }
 
 // Strided complex64 tiles (U >= 3) with the two-layout family.
-template <int TB, int RB, bool PRE, bool POST, int U, bool NOISY>
-__global__ void __launch_bounds__(1 << (TB - RB), SV_TILE_MIN_BLOCKS) wht_tile2_kernel(const KParams p) {
+template <int TB, int RB, bool PRE, bool POST, int U, bool NOISY, bool XCHG>
+__global__ void __launch_bounds__(1 << (TB - RB), SV_TILE_MIN_BLOCKS) wht_tile2_kernel(const KParamsT<NOISY> p) {
     using L = Layout2<TB, RB>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float2 *sm = reinterpret_cast<float2 *>(smem_raw);
     __shared__ unsigned long long s_mlo, s_mcnt;
-    __shared__ float2 *s_dst[8];
-    load_xdst(p, threadIdx.x, s_dst);
+    __shared__ float2 *s_dst[XCHG ? 8 : 1];
+    if constexpr (XCHG) load_xdst(p, threadIdx.x, s_dst);
     const int tid = threadIdx.x;
     const unsigned long long base = tile_base(blockIdx.x, p.free_mask);
     float2 x[L::NR];
     global_load<L, 0>(x, reinterpret_cast<const float2 *>(p.in) + base, p, tid);
-    if (p.scale_in) apply_scale(x, *p.scale_in);
+    if constexpr (NOISY) {  // renormalisation (decoherence) rides only on the general-2x2 flavour
+        if (p.scale_in) apply_scale(x, *p.scale_in);
+    }
     const bool has_marked = (p.mid == MID_ORACLE) && oracle_lookup(p, blockIdx.x, tid, &s_mlo, &s_mcnt);
-    tile_body2<L, PRE, POST, U, NOISY>(x, sm, p, base, reinterpret_cast<float2 *>(p.out) + base, tid, s_dst, has_marked, &s_mlo,
+    tile_body2<L, PRE, POST, U, NOISY, XCHG>(x, sm, p, base, reinterpret_cast<float2 *>(p.out) + base, tid, s_dst, has_marked, &s_mlo,
                                 &s_mcnt);
 }
 
 // One CTA per tile: 128-bit loads straight into registers (layout A).
-template <typename E, int TB, int RB, bool PRE, bool POST, int U, bool NOISY>
-__global__ void __launch_bounds__(1 << (TB - RB), (TB - RB >= 9) ? 1 : SV_TILE_MIN_BLOCKS) wht_tile_kernel(const KParams p) {
+template <typename E, int TB, int RB, bool PRE, bool POST, int U, bool NOISY, bool XCHG>
+__global__ void __launch_bounds__(1 << (TB - RB), (TB - RB >= 9) ? 1 : SV_TILE_MIN_BLOCKS) wht_tile_kernel(const KParamsT<NOISY> p) {
     using L = Layout<E, TB, RB>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     E *sm = reinterpret_cast<E *>(smem_raw);
     __shared__ unsigned long long s_mlo, s_mcnt;
-    __shared__ E *s_dst[8];
-    load_xdst(p, threadIdx.x, s_dst);
+    __shared__ E *s_dst[XCHG ? 8 : 1];
+    if constexpr (XCHG) load_xdst(p, threadIdx.x, s_dst);
     const int tid = threadIdx.x;
-    const unsigned long long base = tile_base(blockIdx.x, p.free_mask);
+    // U == 0: the contiguous group, tile t = slots [0, T) at t * 2^T
+    const unsigned long long base =
+        (U == 0) ? ((unsigned long long)blockIdx.x << TB) : tile_base(blockIdx.x, p.free_mask);
     E x[L::NR];
-    global_load<L, 0>(x, reinterpret_cast<const E *>(p.in) + base, p, tid);
-    if (p.scale_in) apply_scale(x, *p.scale_in);
+    global_load<L, 0, (U == 0)>(x, reinterpret_cast<const E *>(p.in) + base, p, tid);
+    if constexpr (NOISY) {  // renormalisation (decoherence) rides only on the general-2x2 flavour
+        if (p.scale_in) apply_scale(x, *p.scale_in);
+    }
     const bool has_marked = (p.mid == MID_ORACLE) && oracle_lookup(p, blockIdx.x, tid, &s_mlo, &s_mcnt);
-    tile_body<L, PRE, POST, U, NOISY>(x, sm, p, base, reinterpret_cast<E *>(p.out) + base, tid, s_dst, has_marked, &s_mlo, &s_mcnt);
+    tile_body<L, PRE, POST, U, NOISY, XCHG>(x, sm, p, base, reinterpret_cast<E *>(p.out) + base, tid, s_dst, has_marked, &s_mlo, &s_mcnt);
 }
 
-template <typename E, int TB, int RB, bool PRE, bool POST, int U, bool NOISY>
-static void launch_tile_t(const KParams &kp, unsigned long long ntiles, cudaStream_t s) {
+template <typename E, int TB, int RB, bool PRE, bool POST, int U, bool NOISY, bool XCHG>
+static void launch_tile_x(const KParamsT<NOISY> &kp, unsigned long long ntiles, cudaStream_t s) {
     using L = Layout<E, TB, RB>;
-    auto fn = wht_tile_kernel<E, TB, RB, PRE, POST, U, NOISY>;
+    auto fn = wht_tile_kernel<E, TB, RB, PRE, POST, U, NOISY, XCHG>;
     // short-run strided c64 tiles (64-128 B runs): halve the relayouts with the
     // two-layout family; longer runs keep 16-byte accesses (measured on B200:
     // U = 3/4 passes 14-17% faster, U = 6 passes 9% slower with Layout2)
-    if constexpr (sizeof(E) == 8 && U >= 3 && U <= SV_2LAYOUT_MAX_U) fn = wht_tile2_kernel<TB, RB, PRE, POST, U, NOISY>;
+    if constexpr (sizeof(E) == 8 && U >= 3 && U <= SV_2LAYOUT_MAX_U)
+        fn = wht_tile2_kernel<TB, RB, PRE, POST, U, NOISY, XCHG>;
     const int smem = (1 << TB) * (int)sizeof(E);
     static bool attr = false;
     if (!attr) {
@@ -676,8 +703,14 @@ static void launch_tile_t(const KParams &kp, unsigned long long ntiles, cudaStre
     SV_CUDA(cudaGetLastError());
 }
 
+template <typename E, int TB, int RB, bool PRE, bool POST, int U, bool NOISY>
+static void launch_tile_t(const KParamsT<NOISY> &kp, unsigned long long ntiles, cudaStream_t s) {
+    if (kp.xchg) launch_tile_x<E, TB, RB, PRE, POST, U, NOISY, true>(kp, ntiles, s);
+    else launch_tile_x<E, TB, RB, PRE, POST, U, NOISY, false>(kp, ntiles, s);
+}
+
 template <typename E, int TB, int RB, int U, bool NOISY>
-static void launch_tile_u(const KParams &kp, int pre, int post, int u, unsigned long long ntiles, cudaStream_t s) {
+static void launch_tile_u(const KParamsT<NOISY> &kp, int pre, int post, int u, unsigned long long ntiles, cudaStream_t s) {
     if constexpr (U < TB) {
         if (u != U) return launch_tile_u<E, TB, RB, U + 1, NOISY>(kp, pre, post, u, ntiles, s);
         if (pre && post) launch_tile_t<E, TB, RB, true, true, U, NOISY>(kp, ntiles, s);
@@ -694,13 +727,13 @@ static void launch_tile_u(const KParams &kp, int pre, int post, int u, unsigned 
 namespace sv {
 // Both dtypes, one stage flavour (instantiated in wht.cu / wht_noisy.cu).
 template <bool NOISY>
-void launch_tile_dispatch(sv_dtype dt, const KParams &kp, int pre, int post, int u, unsigned long long ntiles,
+void launch_tile_dispatch(sv_dtype dt, const KParamsT<NOISY> &kp, int pre, int post, int u, unsigned long long ntiles,
                           cudaStream_t s) {
     if (dt == SV_C64) launch_tile_u<float2, kTileBitsC64, kRegBitsC64, 0, NOISY>(kp, pre, post, u, ntiles, s);
     else launch_tile_u<double2, kTileBitsC128, kRegBitsC128, 0, NOISY>(kp, pre, post, u, ntiles, s);
 }
-extern template void launch_tile_dispatch<false>(sv_dtype, const KParams &, int, int, int, unsigned long long,
+extern template void launch_tile_dispatch<false>(sv_dtype, const KParamsT<false> &, int, int, int, unsigned long long,
                                                  cudaStream_t);
-extern template void launch_tile_dispatch<true>(sv_dtype, const KParams &, int, int, int, unsigned long long,
+extern template void launch_tile_dispatch<true>(sv_dtype, const KParamsT<true> &, int, int, int, unsigned long long,
                                                 cudaStream_t);
 }  // namespace sv
