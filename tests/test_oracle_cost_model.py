@@ -1,0 +1,89 @@
+"""Pins of the oracle's analytical model (oracle/cost_model.py, Eqs. 2-9)
+against numbers the paper prints -- Table 6 (T3E) and Table 5 (SP2)
+"Calculated Time" columns, with Table 2 (sizes), Table 3 (reorganisation
+counts) and Fig. 9 (constants) -- and against the identities the equations
+fix (Eq. 9 = 3 x Eq. 6, Eq. 7 -> Eq. 6 at n_p = 0, Eq. 5 = Eq. 4 at n_l = 0,
+T_reorg = 0 at n_c = 0, Eq. 8 - 3 Eq. 7 = 2 l t_lat).
+
+The papers' step profiles (l_step, n_b_step per step) are not printed, so the
+Table 5/6 pins calibrate ONE quantity from the printed 1-processor time (the
+dynamic-structure state count sum l_i 2^(n_b_i - 1)) and then predict the
+multi-processor "Calculated" entries, which exercise Eq. 7's s^(n_b - n_p)
+scaling, Eq. 4's non-scaling link traversal and Eq. 2's reorganisation
+term; n_c (changed parallel bits per reorganisation) is bracketed by
+[1, n_p]."""
+import pytest
+
+from oracle import cost_model as M
+
+
+def profile_for(l_total, n_b, n_l, target_seq, mp, s=2):
+    """Two-step dynamic profile (l_a ops at n_b, the rest at n_b - 1: the
+    paper's dynamic structure grows as bits are used) whose Eq. 6 time is
+    target_seq."""
+    trav = l_total * s ** n_l * mp["t_t"]
+    K = (target_seq - trav) / M.t_op(mp, s)  # sum l_i s^(n_b_i - 1)
+    hi, lo = s ** (n_b - 1), s ** (n_b - 2)
+    l_a = (K - l_total * lo) / (hi - lo)
+    assert 0 < l_a < l_total
+    l_a = round(l_a)
+    return [(l_a, n_b, n_l, 0), (l_total - l_a, n_b - 1, n_l, 0)]
+
+
+def with_reorgs(steps, R, n_c):
+    """Split the work into R + 1 steps with R reorganisations of n_c bits."""
+    out = []
+    for (l, n_b, n_l, _) in steps:
+        out.append((l, n_b, n_l, 0))
+    # the reorganisation cost does not depend on how l is split: attach them
+    # to zero-work steps of the largest size
+    n_b_max = max(n_b for (_, n_b, _, _) in steps)
+    n_l = steps[0][2]
+    out += [(0, n_b_max, n_l, n_c)] * R
+    return out
+
+
+def test_table6_mult2_t3e():
+    # Table 2: Mult2 -- 2 states, 16 QU-bits, 7,137 laser ops, 10 link bits
+    # Table 6 "Calculated Time": 1 proc 282 s, 2: 143, 4: 73, 8: 38
+    # Table 3: Mult2 reorganisations with 1 / 2 / 3 parallel bits: 6 / 7 / 22
+    mp = M.T3E
+    base = profile_for(7137, 16, 10, 282.0, mp)
+    assert M.t_seqdyn(base, 2, mp) == pytest.approx(282.0, rel=1e-4)
+    p1 = M.t_par(with_reorgs(base, 6, 1), 1, 2, mp)
+    assert p1 == pytest.approx(143.0, rel=0.01)
+    for n_p, R, printed in ((2, 7, 73.0), (3, 22, 38.0)):
+        lo = M.t_par(with_reorgs(base, R, 1), n_p, 2, mp)
+        hi = M.t_par(with_reorgs(base, R, n_p), n_p, 2, mp)
+        assert abs(lo - printed) / printed < 0.05 and abs(hi - printed) / printed < 0.05, (n_p, lo, hi, printed)
+
+
+def test_table5_f15_3bits_sp2():
+    # Table 2: f15_3bits -- 2 states, 18 QU-bits, 70,793 laser ops, 12 link bits
+    # Table 5 "Calculated Time": 1 proc 16111 s, 4: 4196, 8: 2234
+    # Table 3: f15_3bits reorganisations with 2 / 3 parallel bits: 8 / 28
+    mp = M.SP2
+    base = profile_for(70793, 18, 12, 16111.0, mp)
+    for n_p, R, printed in ((2, 8, 4196.0), (3, 28, 2234.0)):
+        lo = M.t_par(with_reorgs(base, R, 1), n_p, 2, mp)
+        hi = M.t_par(with_reorgs(base, R, n_p), n_p, 2, mp)
+        assert abs(lo - printed) / printed < 0.05 and abs(hi - printed) / printed < 0.05, (n_p, lo, hi, printed)
+
+
+def test_identities():
+    mp = M.T3E
+    steps = [(100, 12, 4, 2), (250, 14, 5, 1), (80, 16, 6, 3)]
+    assert M.t_seqdec(steps, 2, mp) == 3 * M.t_seqdyn(steps, 2, mp)  # Eq. 9
+    zero_c = [(l, n_b, n_l, 0) for (l, n_b, n_l, _) in steps]
+    assert M.t_par(zero_c, 0, 2, mp) == M.t_seqdyn(zero_c, 2, mp)  # Eq. 7 -> Eq. 6
+    assert M.t_seqflat(350, 14, 2, mp) == M.t_comp(350, 14, 0, 2, mp)  # Eq. 5
+    assert M.t_reorg(10, 16, 0, 2, mp) == 0.0  # nothing moves
+    l_total = sum(l for (l, _, _, _) in steps)
+    assert M.t_pardec(steps, 2, 2, mp) - 3 * M.t_par(steps, 2, 2, mp) == pytest.approx(2 * l_total * mp["t_lat"])
+    # Eq. 2: moving all n_l link bits moves every block but one of s^n_l
+    assert M.t_reorg(3, 8, 3, 2, mp) == pytest.approx(7 * (mp["t_lat"] + mp["t_b"] * 16 * 32 + mp["t_lr"]))
+    # three-state simulations use t_op3 (Fig. 9)
+    assert M.t_comp(1, 3, 0, 3, mp) == pytest.approx(mp["t_t"] + 9 * mp["t_op3"])
+    # scaling every machine constant by c scales every time by c
+    mp2 = {k: (v * 3.0 if k != "q" else v) for k, v in mp.items()}
+    assert M.t_pardec(steps, 1, 2, mp2) == pytest.approx(3.0 * M.t_pardec(steps, 1, 2, mp))
