@@ -38,6 +38,28 @@ static void validate_gate(int n, const sv_gate &g, uint64_t j) {
              "gate " + std::to_string(j) + ": a gate cannot control its own target");
 }
 
+// Ops a pass runs after the host fusion of gates.cu (build_tile_ops): a gate
+// with the same target and controls as an earlier op of the pass, with only
+// commuting ops in between, is multiplied into it.
+uint64_t fused_op_count(const sv_gate *gates, const uint64_t *order, uint64_t count) {
+    std::vector<const sv_gate *> ops;
+    for (uint64_t k = 0; k < count; ++k) {
+        const sv_gate &g = gates[order[k]];
+        bool fused = false;
+        CommuteSet between;
+        for (size_t i = ops.size(); i-- > 0;) {
+            if (ops[i]->target == g.target && ops[i]->controls == g.controls && between.commutes(g)) {
+                fused = true;
+                break;
+            }
+            between.add(*ops[i]);
+            if (!between.commutes(g)) break;
+        }
+        if (!fused) ops.push_back(&g);
+    }
+    return ops.size();
+}
+
 GatePlan plan_gates(int n, int g, sv_dtype dtype, const sv_gate *gates, uint64_t count) {
     SV_CHECK(n >= 1 && n <= 40, SV_EINVAL, "n must be in [1, 40]");
     SV_CHECK(dtype == SV_C64 || dtype == SV_C128, SV_EINVAL, "dtype must be SV_C64 or SV_C128");
@@ -59,6 +81,7 @@ GatePlan plan_gates(int n, int g, sv_dtype dtype, const sv_gate *gates, uint64_t
             p.order.push_back(j);
             s.proc |= 1ull << gates[j].target;
         }
+        s.ops = count;  // the one-CTA kernel runs every gate as given
         s.tile = (n >= 64) ? ~0ull : ((1ull << n) - 1ull);
         p.steps.push_back(s);
         return p;
@@ -112,6 +135,7 @@ GatePlan plan_gates(int n, int g, sv_dtype dtype, const sv_gate *gates, uint64_t
             swapped ^= 1;
             continue;
         }
+        s.ops = fused_op_count(gates, p.order.data() + s.first, s.count);
         // tile = processed slots + the lowest other slots (carry first) up to T
         s.proc = proc;
         s.tile = proc;

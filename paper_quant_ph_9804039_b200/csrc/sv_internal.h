@@ -112,6 +112,7 @@ struct GateStep {
     int swapped = 0;     // layout during the pass: 0 natural, 1 top-g local <-> rank bits
     uint64_t first = 0;  // gates order[first .. first + count)
     uint64_t count = 0;
+    uint64_t ops = 0;    // ops after the host fusion of same-target gates (gates.cu)
 };
 
 struct GatePlan {

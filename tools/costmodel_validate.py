@@ -1,0 +1,149 @@
+"""Calibrate the B200 refit of the paper's model on one GPU, then validate it
+on held-out workloads -- the analog of the paper's Tables 5/6 ("Observed and
+Calculated run times", section 3.5.2).
+
+python tools/costmodel_validate.py [--out gpurun_out/costmodel_validation.json] [--quick]
+
+Calibration (n = 30, complex64): per-class WHT pass bandwidths, the mean /
+reduce pass bandwidths, the per-pair gate cost t_gate from a compute-bound
+gate pass, the emulated exchange copy bandwidth.  Validation: other sizes
+(n = 28, 32, 34), the mean diffusion, gate circuits, emulated sharding.
+Observed = device time from the library's CUDA events (sv_profile), summed
+over the call's launches.
+"""
+from __future__ import annotations
+
+import argparse
+import collections
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import paper_quant_ph_9804039_b200 as sv  # noqa: E402
+from paper_quant_ph_9804039_b200 import costmodel as CM  # noqa: E402
+from tests import circuits as C  # noqa: E402
+
+
+def profiled(ctx, fn):
+    """Run fn() once for warm-up, then once profiled; return (total device ms, timeline)."""
+    fn()
+    sv.sv_synchronize(ctx)
+    sv.sv_profile(ctx, True)
+    fn()
+    tl = sv.sv_profile_timeline(ctx)
+    sv.sv_profile(ctx, False)
+    return sum(ms for _, ms in tl), tl
+
+
+def calibrate(n=30):
+    prm = CM.B200Params()
+    S = (1 << n) * 8
+    with sv.sv_init(n, 1, sv.SV_C64, sv.SV_INIT_UNIFORM) as c:
+        sv.sv_set_marked(c, sv.sv_marked_from_seed(n, 16, 1))
+        k = 4
+        _, tl = profiled(c, lambda: sv.sv_iterate(c, k, sv.SV_DIFFUSE_WHT))
+        plan = [s for s in sv.sv_plan_wht(n, 1, sv.SV_C64, k, True) if s["kind"] == 0]
+        passes = [ms for kind, ms in tl if kind == sv.SV_K_WHT_TILE]
+        assert len(plan) == len(passes)
+        by = collections.defaultdict(list)
+        for st, ms in zip(plan, passes):
+            by[CM.pass_class(st["tile_mask"], bool(st["pre"] and st["post"]))].append(ms)
+        prm.bw_pass = {cls: 2 * S / (np.mean(v) / 1e3) for cls, v in by.items()}
+        prm.bw_pass["default"] = 2 * S * len(passes) / (sum(passes) / 1e3)
+        _, tl = profiled(c, lambda: sv.sv_iterate(c, 8, sv.SV_DIFFUSE_MEAN))
+        red = [ms for kind, ms in tl if kind == sv.SV_K_REDUCE]
+        mean = [ms for kind, ms in tl if kind == sv.SV_K_MEAN]
+        prm.bw_reduce = S / (np.mean(red) / 1e3)
+        prm.bw_mean = 2 * S / (np.mean(mean) / 1e3)
+    # gate compute: 400 controlled general gates on 10 target qubits at n = 26
+    # -> one compute-bound pass (few fuse: controls differ)
+    ng = 26
+    gates = C.random_circuit(ng, 400, 5, max_controls=2, qubits=range(3, 13), p_control=1.0)
+    with sv.sv_init(ng, 1, sv.SV_C64, sv.SV_INIT_GAUSSIAN) as c:
+        tot, tl = profiled(c, lambda: sv.sv_apply_gates(c, gates))
+    steps, _ = sv.sv_plan_gates(ng, 1, sv.SV_C64, gates)
+    assert len(steps) == 1
+    prm.t_gate = (tot / 1e3) / (steps[0]["ops"] * (1 << (ng - 1)))
+    # emulated exchange copy bandwidth (unfused mode: device-local chunk copies)
+    ne = 28
+    with sv.sv_init(ne, 1, sv.SV_C64, sv.SV_INIT_UNIFORM, world=2) as c:
+        sv.sv_set_exchange(c, False)
+        sv.sv_set_marked(c, sv.sv_marked_from_seed(ne, 4, 1))
+        _, tl = profiled(c, lambda: sv.sv_iterate(c, 1, sv.SV_DIFFUSE_WHT))
+        ex = [ms for kind, ms in tl if kind == sv.SV_K_EXCHANGE]
+        prm.bw_copy = 2 * (1 << ne) * 8 / (np.mean(ex) / 1e3)  # read + write of the whole emulated buffer
+    return prm
+
+
+def observe_wht(n, k, world=1, init=sv.SV_INIT_UNIFORM, fused=None):
+    with sv.sv_init(n, 1, sv.SV_C64, init, world=world) as c:
+        if fused is not None:
+            sv.sv_set_exchange(c, fused)
+        sv.sv_set_marked(c, sv.sv_marked_from_seed(n, 16, 1))
+        tot, _ = profiled(c, lambda: sv.sv_iterate(c, k, sv.SV_DIFFUSE_WHT))
+    return tot / 1e3
+
+
+def observe_mean(n, k):
+    with sv.sv_init(n, 1, sv.SV_C64, sv.SV_INIT_UNIFORM) as c:
+        sv.sv_set_marked(c, sv.sv_marked_from_seed(n, 16, 1))
+        tot, _ = profiled(c, lambda: sv.sv_iterate(c, k, sv.SV_DIFFUSE_MEAN))
+    return tot / 1e3
+
+
+def observe_gates(n, gates, world=1):
+    with sv.sv_init(n, 1, sv.SV_C64, sv.SV_INIT_GAUSSIAN, world=world) as c:
+        if world > 1:
+            sv.sv_set_exchange(c, False)
+        tot, _ = profiled(c, lambda: sv.sv_apply_gates(c, gates))
+    return tot / 1e3
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "costmodel_validation.json"))
+    ap.add_argument("--quick", action="store_true", help="skip the n = 34 (128 GiB) rows")
+    args = ap.parse_args()
+    t0 = time.time()
+    prm = calibrate()
+    rows = []
+
+    def row(name, P, obs, pred):
+        rows.append({"workload": name, "P": P, "observed_s": obs, "calculated_s": pred,
+                     "relative_difference": (pred - obs) / obs})
+        print(json.dumps(rows[-1]), flush=True)
+
+    for n, k in ((28, 64), (32, 16)) + (() if args.quick else ((34, 8),)):
+        row(f"WHT n={n} k={k} (c64)", 1, observe_wht(n, k), CM.predict_wht(n, 1, 0, k, prm)["t"])
+    for n, k in ((28, 64),) + (() if args.quick else ((34, 8),)):
+        row(f"mean n={n} k={k} (c64)", 1, observe_mean(n, k), CM.predict_mean(n, 1, 0, k, prm)["t"])
+    n = 30
+    work = {"QFT": C.qft_circuit(n), "layered_x4": C.layered_circuit(n, 4, 1),
+            "random_300": C.random_circuit(n, 300, 2, max_controls=2),
+            "h_layers_x4": C.circuit([C.record(q, C.H) for q in range(n)] * 4)}
+    for name, g in work.items():
+        row(f"gates {name} n={n} (c64)", 1, observe_gates(n, g), CM.predict_gates(n, 1, 0, g, prm)["t"])
+    for P in (2, 4):
+        row(f"WHT n=30 k=4 emulated P={P} (a2a copies)", P, observe_wht(30, 4, world=P, fused=False),
+            CM.predict_wht(30, P, 0, 4, prm, emulated=True, fused_exchange=False)["t"])
+    rel = [abs(r["relative_difference"]) for r in rows]
+    out = {"calibration": {"n": 30, "dtype": "c64", "bw_pass": prm.bw_pass, "bw_mean": prm.bw_mean,
+                           "bw_reduce": prm.bw_reduce, "t_gate": prm.t_gate, "bw_copy": prm.bw_copy,
+                           "t_launch": prm.t_launch, "bw_nvlink_nominal": prm.bw_nvlink, "t_lat_assumed": prm.t_lat},
+           "paper_terms": {"t_op_per_pair_per_pass_s": prm.as_machine_params(0).t_op2, "t_t": 0.0,
+                           "t_b_s_per_byte": 1.0 / prm.bw_nvlink, "t_lr": 0.0},
+           "validation": rows, "max_abs_relative_difference": max(rel), "mean_abs_relative_difference": float(np.mean(rel)),
+           "wall_s": time.time() - t0}
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    json.dump(out, open(args.out, "w"), indent=1)
+    print(json.dumps({k: v for k, v in out.items() if k != "validation"}, indent=1))
+
+
+if __name__ == "__main__":
+    main()
