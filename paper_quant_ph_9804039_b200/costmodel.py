@@ -129,14 +129,28 @@ class B200Params:
     bw_pass: dict = dataclasses.field(default_factory=lambda: {"default": 5.6e12})
     bw_mean: float = 6.0e12        # fused flip + invert-about-mean pass (2 S_l)
     bw_reduce: float = 6.0e12      # read-only sum pass (S_l)
-    t_gate: float = 2.0e-12        # seconds per amplitude pair per gate op (compute term)
+    t_gate: float = 7e-13          # seconds per amplitude pair per general 2x2 op (compute term)
+    t_diag: float = 3e-13          # ... per diagonal op (phase / controlled phase)
     bw_nvlink: float = 900e9       # per direction, NVLink 5 (nominal)
     bw_copy: float = 3.0e12        # device-local copy (emulated exchange), bytes moved / s
     t_lat: float = 15e-6           # one NCCL collective
     t_launch: float = 2e-6         # per kernel launch gap
 
     def bw(self, cls: str) -> float:
-        return self.bw_pass.get(cls, self.bw_pass.get("default", 5.6e12))
+        """Calibrated bandwidth of a class, else of the calibrated class with
+        the same fusion flag and the nearest run length, else the default."""
+        if cls in self.bw_pass:
+            return self.bw_pass[cls]
+        fused = cls.endswith("_fused")
+        run = int(cls[3:].split("_")[0])
+        best = None
+        for c, v in self.bw_pass.items():
+            if not c.startswith("run") or c.endswith("_fused") != fused:
+                continue
+            d = abs(int(c[3:].split("_")[0]) - run)
+            if best is None or d < best[0]:
+                best = (d, v)
+        return best[1] if best else self.bw_pass.get("default", 5.6e12)
 
     def as_machine_params(self, dtype: int = 0, cls: str = "default") -> MachineParams:
         """The refit in the paper's terms (per pair per pass t_op = 4q/BW)."""
@@ -192,29 +206,39 @@ def predict_mean(n: int, world: int, dtype: int, k: int, prm: B200Params, emulat
     return {"t": t, "passes": k + 1}
 
 
+def _is_diag(g) -> bool:
+    m = g["m"]
+    return m[2] == 0.0 and m[3] == 0.0 and m[4] == 0.0 and m[5] == 0.0
+
+
 def predict_gates(n: int, world: int, dtype: int, gates, prm: B200Params, emulated: bool = False) -> dict:
-    """sv_apply_gates: each pass costs max(HBM round trip, ops x pairs x
-    t_gate) -- Eq. 4's l s^(n_b - 1) t_op with the memory roofline; swaps as
-    in predict_wht (unfused all-to-all)."""
+    """sv_apply_gates: each pass costs its HBM round trip plus its on-chip
+    work, ops x pairs x t_op(kind) -- Eq. 4's l s^(n_b - 1) t_op next to the
+    memory term (a CTA's load, compute and store phases barely overlap at 2
+    CTAs / SM); swaps as in predict_wht (unfused all-to-all)."""
     from . import _sv as sv
 
-    steps, _ = sv.sv_plan_gates(n, world, dtype, gates)
+    steps, order = sv.sv_plan_gates(n, world, dtype, gates)
     eb = ELEM_BYTES[dtype]
     N_l = (1 << n) / (1 if emulated else world)
     S_l = N_l * eb
     t_pass = t_swap = 0.0
     npass = nswap = 0
     for st in steps:
-        if st["kind"] == 0:
-            t_mem = 2.0 * S_l / prm.bw(pass_class(st["tile_mask"], False))
-            t_ops = st["ops"] * (N_l / 2.0) * prm.t_gate
-            t_pass += max(t_mem, t_ops) + prm.t_launch
-            npass += 1
-        elif st["kind"] == 1:
+        if st["kind"] == 1:
             t_swap += _swap_time(S_l, world, prm, emulated)
             nswap += 1
+            continue
+        idx = order[st["first"]:st["first"] + st["count"]]
+        nd = sum(1 for j in idx if _is_diag(gates[int(j)]))
+        # host fusion shrinks the op count; spread it over the two kinds
+        scale = st["ops"] / max(st["count"], 1)
+        t_ops = scale * (nd * prm.t_diag + (st["count"] - nd) * prm.t_gate) * (N_l / 2.0)
+        if st["kind"] == 0:
+            t_pass += 2.0 * S_l / prm.bw(pass_class(st["tile_mask"], False)) + t_ops + prm.t_launch
+            npass += 1
         else:
-            t_pass += st["ops"] * (N_l / 2.0) * prm.t_gate + prm.t_launch
+            t_pass += t_ops + prm.t_launch
     return {"t": t_pass + t_swap, "t_pass": t_pass, "t_swap": t_swap, "passes": npass, "swaps": nswap}
 
 

@@ -61,15 +61,19 @@ def calibrate(n=30):
         mean = [ms for kind, ms in tl if kind == sv.SV_K_MEAN]
         prm.bw_reduce = S / (np.mean(red) / 1e3)
         prm.bw_mean = 2 * S / (np.mean(mean) / 1e3)
-    # gate compute: 400 controlled general gates on 10 target qubits at n = 26
-    # -> one compute-bound pass (few fuse: controls differ)
+    # gate compute: one compute-heavy pass at n = 26 on 10 target qubits
+    # (controls differ, so little fuses), general unitaries and controlled
+    # phases; t_op(kind) = (pass time - HBM round trip) / (ops x pairs)
     ng = 26
-    gates = C.random_circuit(ng, 400, 5, max_controls=2, qubits=range(3, 13), p_control=1.0)
-    with sv.sv_init(ng, 1, sv.SV_C64, sv.SV_INIT_GAUSSIAN) as c:
-        tot, tl = profiled(c, lambda: sv.sv_apply_gates(c, gates))
-    steps, _ = sv.sv_plan_gates(ng, 1, sv.SV_C64, gates)
-    assert len(steps) == 1
-    prm.t_gate = (tot / 1e3) / (steps[0]["ops"] * (1 << (ng - 1)))
+    t_mem = 2 * (1 << ng) * 8 / prm.bw("run13")
+    for attr, gates in (("t_gate", C.random_circuit(ng, 400, 5, max_controls=2, qubits=range(3, 13), p_control=1.0)),
+                        ("t_diag", C.circuit([C.record(3 + (i % 10), C.phase(0.1 * i + 0.05), [i % 3])
+                                              for i in range(400)]))):
+        with sv.sv_init(ng, 1, sv.SV_C64, sv.SV_INIT_GAUSSIAN) as c:
+            tot, _ = profiled(c, lambda: sv.sv_apply_gates(c, gates))
+        steps, _ = sv.sv_plan_gates(ng, 1, sv.SV_C64, gates)
+        assert len(steps) == 1
+        setattr(prm, attr, max(tot / 1e3 - t_mem, 0.0) / (steps[0]["ops"] * (1 << (ng - 1))))
     # emulated exchange copy bandwidth (unfused mode: device-local chunk copies)
     ne = 28
     with sv.sv_init(ne, 1, sv.SV_C64, sv.SV_INIT_UNIFORM, world=2) as c:
@@ -134,7 +138,7 @@ def main():
             CM.predict_wht(30, P, 0, 4, prm, emulated=True, fused_exchange=False)["t"])
     rel = [abs(r["relative_difference"]) for r in rows]
     out = {"calibration": {"n": 30, "dtype": "c64", "bw_pass": prm.bw_pass, "bw_mean": prm.bw_mean,
-                           "bw_reduce": prm.bw_reduce, "t_gate": prm.t_gate, "bw_copy": prm.bw_copy,
+                           "bw_reduce": prm.bw_reduce, "t_gate": prm.t_gate, "t_diag": prm.t_diag, "bw_copy": prm.bw_copy,
                            "t_launch": prm.t_launch, "bw_nvlink_nominal": prm.bw_nvlink, "t_lat_assumed": prm.t_lat},
            "paper_terms": {"t_op_per_pair_per_pass_s": prm.as_machine_params(0).t_op2, "t_t": 0.0,
                            "t_b_s_per_byte": 1.0 / prm.bw_nvlink, "t_lr": 0.0},
