@@ -574,41 +574,51 @@ void setup_peers(sv_ctx *c) {
     if (c->comm == nullptr || c->world > 8) return;
     dmalloc((void **)&c->d_barrier, sizeof(int), "barrier");
     SV_CUDA(cudaMemsetAsync(c->d_barrier, 0, sizeof(int), c->stream));
-    cudaIpcMemHandle_t h[2];
-    if (cudaIpcGetMemHandle(&h[0], c->state) != cudaSuccess || cudaIpcGetMemHandle(&h[1], c->recv) != cudaSuccess) {
-        cudaGetLastError();
-        return;
-    }
-    const size_t hb = sizeof(h);
+    // Every rank takes part in every collective below whatever its local
+    // outcome, and the mode is decided by an allreduce(min): ranks can never
+    // disagree on fused vs all-to-all (which would deadlock the schedule).
+    struct Entry {
+        cudaIpcMemHandle_t h[2];
+        int ok;
+        int pad;
+    };
+    Entry mine{};
+    mine.ok = (cudaIpcGetMemHandle(&mine.h[0], c->state) == cudaSuccess &&
+               cudaIpcGetMemHandle(&mine.h[1], c->recv) == cudaSuccess) ? 1 : 0;
+    if (!mine.ok) cudaGetLastError();
+    const size_t hb = sizeof(Entry);
     char *d_all = nullptr;
-    dmalloc((void **)&d_all, hb * c->world, "ipc handles");
-    std::vector<char> all(hb * c->world);
+    dmalloc((void **)&d_all, hb * c->world + sizeof(int), "ipc handles");
+    std::vector<Entry> all(c->world);
+    int *d_ok = reinterpret_cast<int *>(d_all + hb * c->world);
+    int ok = 0;
     try {
-        SV_CUDA(cudaMemcpyAsync(d_all + hb * c->rank, h, hb, cudaMemcpyHostToDevice, c->stream));
+        SV_CUDA(cudaMemcpyAsync(d_all + hb * c->rank, &mine, hb, cudaMemcpyHostToDevice, c->stream));
         SV_NCCL(ncclAllGather(d_all + hb * c->rank, d_all, hb, ncclChar, c->comm, c->stream));
         SV_CUDA(cudaMemcpyAsync(all.data(), d_all, hb * c->world, cudaMemcpyDeviceToHost, c->stream));
+        SV_CUDA(cudaStreamSynchronize(c->stream));
+        ok = 1;
+        for (int j = 0; j < c->world; ++j) ok &= all[j].ok;
+        for (int j = 0; j < c->world && ok; ++j) {
+            if (j == c->rank) continue;
+            if (cudaIpcOpenMemHandle(&c->peer_state[j], all[j].h[0], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+                cudaIpcOpenMemHandle(&c->peer_recv[j], all[j].h[1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                cudaGetLastError();
+                ok = 0;
+            }
+        }
+        SV_CUDA(cudaMemcpyAsync(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        SV_NCCL(ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, c->comm, c->stream));
+        SV_CUDA(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         SV_CUDA(cudaStreamSynchronize(c->stream));
     } catch (...) {
         cudaFree(d_all);
         throw;
     }
     SV_CUDA(cudaFree(d_all));
-    bool ok = true;
-    for (int j = 0; j < c->world; ++j) {
-        if (j == c->rank) {
-            c->peer_state[j] = c->state;
-            c->peer_recv[j] = c->recv;
-            continue;
-        }
-        cudaIpcMemHandle_t pj[2];
-        memcpy(pj, all.data() + hb * j, hb);
-        if (cudaIpcOpenMemHandle(&c->peer_state[j], pj[0], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
-            cudaIpcOpenMemHandle(&c->peer_recv[j], pj[1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-            cudaGetLastError();
-            ok = false;
-        }
-    }
-    c->xchg_capable = ok;
+    c->peer_state[c->rank] = c->state;
+    c->peer_recv[c->rank] = c->recv;
+    c->xchg_capable = ok != 0;
     c->fused_xchg = want && ok;
 }
 
