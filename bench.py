@@ -251,13 +251,16 @@ def run_ours(args):
     if prof[kname][0] == 0 and prof["wht_whole"][0] > 0:
         kname = "wht_whole"  # n <= T: the whole run is one CTA (latency-bound, c1)
     launches, kms = prof[kname]
+    resident = diff == "mean" and launches == args.steps  # all k iterations in one launch (mean_resident.cu)
     local_bytes = (N_amp // world) * (8 if dtype == sv.SV_C64 else 16)
-    algo_bytes = 2 * local_bytes  # one read + one write of the local state per pass
+    algo_bytes = 2 * local_bytes * (k if resident else 1)  # one read + one write of the local state per pass
     avg_s = (kms / 1e3) / max(launches, 1)
     peak, peak_src = measured_peaks()
     achieved = algo_bytes / avg_s / 1e9
     total_kernel_ms = sum(v[1] for name, v in prof.items() if name not in ("exchange", "allreduce"))
-    kdesc = {"wht_tile": "wht_tile_kernel / wht_tile2_kernel", "mean": "mean_kernel",
+    kdesc = {"wht_tile": "wht_tile_kernel / wht_tile2_kernel",
+             "mean": ("mean_resident_kernel (state held in shared memory for all k iterations; "
+                      "bytes = 2 S per iteration, served on-chip)") if resident else "mean_kernel",
              "wht_whole": "whole_state_kernel (one CTA; bytes = one load + store of the state)"}[kname]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": ncu_traffic(args.config, world), "kernel": f"{kname} ({kdesc})",

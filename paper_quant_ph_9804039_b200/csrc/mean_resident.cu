@@ -1,0 +1,200 @@
+// mean_resident.cu -- all k Grover iterations with the mean diffusion in ONE
+// persistent launch, for states that fit the GPU's aggregate shared memory
+// (148 SMs x ~220 KiB: n <= 20 complex128 / 21 complex64, e.g. c2).
+//
+// Same arithmetic as mean.cu (north star; Eq. 3's accumulate-and-redistribute
+// of a global sum):  b = O a,  a' = 2 mu - b,  mu = sum(b) / N.
+// At c2's size a launched iteration is launch- and reduction-latency bound
+// (~16 us for 33 MB of L2 traffic); here every block keeps its slice of the
+// state in shared memory for the whole call, so an iteration is one pass
+// over shared memory plus one grid barrier:
+//   * block b owns elements [b C, min((b+1) C, N)), loaded once, stored once;
+//   * per iteration: negate the block's marked elements (O), a_i <- 2 mu - a_i,
+//     fp64 partial sums of the new (O a')_i -> one partial per block in global
+//     memory -> grid barrier -> every block sums all partials in block order
+//     (identical, deterministic totals everywhere; G14) -> next mu;
+//   * the grid barrier is a generation counter (co-residency is guaranteed by
+//     the cooperative launch).
+// Single GPU only (sharded runs need the cross-rank allreduce between
+// iterations, so they keep the launched path).
+#include <cuda_runtime.h>
+
+#include "sv_internal.h"
+
+namespace sv {
+
+constexpr int kResThreads = 1024;
+
+__device__ __forceinline__ void grid_barrier(unsigned int *count, unsigned int *gen, unsigned int nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned int *vgen = gen;
+        const unsigned int g = *vgen;
+        __threadfence();
+        if (atomicAdd(count, 1u) == nblocks - 1) {
+            *count = 0u;
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (*vgen == g) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// Block-wide fp64 (re, im) sum, result broadcast to every thread.
+__device__ __forceinline__ void block_sum_bcast(double &re, double &im, double *red) {
+    for (int o = 16; o > 0; o >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, o);
+        im += __shfl_xor_sync(0xffffffffu, im, o);
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) { red[2 * w] = re; red[2 * w + 1] = im; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double r = 0.0, m = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { r += red[2 * i]; m += red[2 * i + 1]; }
+        red[64] = r;
+        red[65] = m;
+    }
+    __syncthreads();
+    re = red[64];
+    im = red[65];
+}
+
+template <typename E>
+__global__ void __launch_bounds__(kResThreads, 1)
+    mean_resident_kernel(E *a, unsigned long long N, unsigned long long C, double inv_N,
+                         const unsigned long long *marked, unsigned long long n_marked, int k, double *partials,
+                         unsigned int *bar) {
+    using R = decltype(E{}.x);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    E *s = reinterpret_cast<E *>(smem_raw);
+    __shared__ double red[66];
+    __shared__ unsigned long long s_mlo, s_mcnt;
+    const unsigned long long lo = (unsigned long long)blockIdx.x * C;
+    const unsigned long long hi = lo + C < N ? lo + C : N;
+    const unsigned int len = (unsigned int)(hi > lo ? hi - lo : 0);
+    const unsigned int nb = gridDim.x;
+    if (threadIdx.x == 0) {  // this block's marked entries: marked[s_mlo .. s_mlo + s_mcnt)
+        unsigned long long l = 0, h = n_marked;
+        while (l < h) { const unsigned long long md = (l + h) >> 1; if (marked[md] < lo) l = md + 1; else h = md; }
+        const unsigned long long first = l;
+        h = n_marked;
+        while (l < h) { const unsigned long long md = (l + h) >> 1; if (marked[md] < hi) l = md + 1; else h = md; }
+        s_mlo = first;
+        s_mcnt = l - first;
+    }
+    for (unsigned int i = threadIdx.x; i < len; i += blockDim.x) s[i] = __ldcg(a + lo + i);
+    __syncthreads();
+    const unsigned long long mlo = s_mlo, mcnt = s_mcnt;
+    // Negate this block's marked entries (O); returns the thread's share of
+    // sum over them of the values BEFORE negation.
+    auto negate_marked = [&](double &cr, double &ci) {
+        cr = 0.0;
+        ci = 0.0;
+        for (unsigned long long j = threadIdx.x; j < mcnt; j += blockDim.x) {
+            E &v = s[marked[mlo + j] - lo];
+            cr += (double)v.x;
+            ci += (double)v.y;
+            v.x = -v.x;
+            v.y = -v.y;
+        }
+    };
+    // Grid total of the per-block values (r, m): one partial per block, grid
+    // barrier, then warp 0 sums the partials in a fixed order (lane-strided,
+    // then a fixed shuffle tree) -- the same total in every block.
+    auto grid_total = [&](double r, double m, int parity, double &tr, double &ti) {
+        block_sum_bcast(r, m, red);
+        double *part = partials + (size_t)parity * 2 * nb;
+        if (threadIdx.x == 0) { part[2 * blockIdx.x] = r; part[2 * blockIdx.x + 1] = m; }
+        grid_barrier(bar, bar + 1, nb);
+        if (threadIdx.x < 32) {
+            double R0 = 0.0, M0 = 0.0;
+            for (unsigned int b = threadIdx.x; b < nb; b += 32) { R0 += __ldcg(&part[2 * b]); M0 += __ldcg(&part[2 * b + 1]); }
+            for (int o = 16; o > 0; o >>= 1) {
+                R0 += __shfl_xor_sync(0xffffffffu, R0, o);
+                M0 += __shfl_xor_sync(0xffffffffu, M0, o);
+            }
+            if (threadIdx.x == 0) { red[64] = R0; red[65] = M0; }
+        }
+        __syncthreads();
+        tr = red[64];
+        ti = red[65];
+    };
+    // first sum: of O a
+    double cr, ci, r = 0.0, m = 0.0;
+    for (unsigned int i = threadIdx.x; i < len; i += blockDim.x) { r += (double)s[i].x; m += (double)s[i].y; }
+    negate_marked(cr, ci);
+    __syncthreads();
+    double tr, ti;
+    grid_total(r - 2.0 * cr, m - 2.0 * ci, 0, tr, ti);
+    // invariant at the top of an iteration: s holds O a and (tr, ti) = sum(O a)
+    for (int it = 0; it < k; ++it) {
+        const R two_mr = (R)(2.0 * tr * inv_N), two_mi = (R)(2.0 * ti * inv_N);
+        r = 0.0;
+        m = 0.0;
+        for (unsigned int i = threadIdx.x; i < len; i += blockDim.x) {
+            E v = s[i];
+            v.x = two_mr - v.x;  // 2 mu - (O a)_i
+            v.y = two_mi - v.y;
+            s[i] = v;
+            r += (double)v.x;
+            m += (double)v.y;
+        }
+        if (it + 1 == k) break;
+        __syncthreads();
+        negate_marked(cr, ci);  // O of the next iteration: sum(O a') = sum(a') - 2 sum_marked(a')
+        __syncthreads();
+        grid_total(r - 2.0 * cr, m - 2.0 * ci, (it + 1) & 1, tr, ti);
+    }
+    __syncthreads();
+    for (unsigned int i = threadIdx.x; i < len; i += blockDim.x) a[lo + i] = s[i];
+}
+
+// Launch geometry: one wave of co-resident blocks, each holding C elements
+// in shared memory; grid = 0 if the state does not fit.
+static void resident_geometry(sv_dtype dt, uint64_t N, int &grid, uint64_t &C, int &smem, void *&fn) {
+    int dev = 0, sms = 0, smem_max = 0;
+    SV_CUDA(cudaGetDevice(&dev));
+    SV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    SV_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    const size_t eb = elem_bytes(dt);
+    const size_t budget = (size_t)smem_max - 1024;  // static shared + slack
+    fn = dt == SV_C64 ? (void *)mean_resident_kernel<float2> : (void *)mean_resident_kernel<double2>;
+    C = (N + sms - 1) / sms;
+    grid = 0;
+    smem = 0;
+    if (C * eb > budget) return;
+    smem = (int)(C * eb);
+    SV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int per = 0;
+    SV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kResThreads, smem));
+    const int g = (int)((N + C - 1) / C);
+    if (per >= 1 && g <= per * sms) grid = g;
+}
+
+bool mean_resident_fits(sv_dtype dt, uint64_t N, size_t partials_cap) {
+    int grid, smem;
+    uint64_t C;
+    void *fn;
+    resident_geometry(dt, N, grid, C, smem, fn);
+    return grid > 0 && (size_t)4 * grid <= partials_cap;
+}
+
+void launch_mean_resident(sv_dtype dt, void *a, uint64_t N, double inv_N, const uint64_t *marked, uint64_t m, int k,
+                          double *partials, unsigned int *bar, cudaStream_t s) {
+    int grid, smem;
+    uint64_t C;
+    void *fn;
+    resident_geometry(dt, N, grid, C, smem, fn);
+    SV_CHECK(grid > 0 && k >= 1, SV_EINVAL, "internal: resident mean launch without a fitting geometry");
+    unsigned long long Nl = N, Cl = C, ml = m;
+    const unsigned long long *mk = reinterpret_cast<const unsigned long long *>(marked);
+    void *args[] = {&a, &Nl, &Cl, &inv_N, &mk, &ml, &k, &partials, &bar};
+    SV_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kResThreads), args, (size_t)smem, s));
+}
+
+}  // namespace sv

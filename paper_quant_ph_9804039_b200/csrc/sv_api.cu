@@ -67,6 +67,8 @@ struct sv_ctx {
     double *d_partials = nullptr;  // 2 * kMaxGrid
     double *d_sums = nullptr;      // [0..1], [2..3] ping-pong; [4] norm; [6] scalar out
     unsigned int *d_counter = nullptr;
+    unsigned int *d_gbar = nullptr;  // grid barrier of the persistent mean kernel {count, generation}
+    bool mean_resident = true;       // SV_MEAN_RESIDENT=0 disables the one-launch path
     int mgrid = 1;
     Plan plan;
     // profiling
@@ -468,6 +470,15 @@ void run_mean(sv_ctx *c, int k, bool with_oracle) {
     }
     const int reps = with_oracle ? k : 1;
     if (reps == 0) return;
+    // single GPU, state within the aggregate shared memory: all iterations in
+    // one persistent launch (mean_resident.cu)
+    if (c->comm == nullptr && c->mean_resident && mean_resident_fits(c->dt, c->nres, 2 * kMaxGrid)) {
+        run(c, SV_K_MEAN, [&] {
+            launch_mean_resident(c->dt, c->state, c->nres, ldexp(1.0, -c->n), with_oracle ? c->d_marked : nullptr,
+                                 with_oracle ? c->n_marked : 0, reps, c->d_partials, c->d_gbar, c->stream);
+        });
+        return;
+    }
     MeanArgs m = mean_args(c, with_oracle);
     // first mu: sum of (O a) over the whole register (Eq. 3's accumulate)
     m.sum_out = c->d_sums;
@@ -650,6 +661,7 @@ void destroy(sv_ctx *c) {
     cudaFree(c->d_partials);
     cudaFree(c->d_sums);
     cudaFree(c->d_counter);
+    cudaFree(c->d_gbar);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -696,6 +708,9 @@ sv_status sv_init(sv_ctx **out, int n, uint64_t seed, sv_dtype dtype, sv_init_ki
         dmalloc((void **)&c->d_partials, 2 * kMaxGrid * sizeof(double), "partials");
         dmalloc((void **)&c->d_sums, 8 * sizeof(double), "sums");
         dmalloc((void **)&c->d_counter, sizeof(unsigned int), "counter");
+        dmalloc((void **)&c->d_gbar, 2 * sizeof(unsigned int), "grid barrier");
+        SV_CUDA(cudaMemsetAsync(c->d_gbar, 0, 2 * sizeof(unsigned int), c->stream));
+        if (const char *e = getenv("SV_MEAN_RESIDENT")) c->mean_resident = strcmp(e, "0") != 0;
         SV_CUDA(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned int), c->stream));
         SV_CUDA(cudaMemsetAsync(c->d_sums, 0, 8 * sizeof(double), c->stream));
         c->mgrid = std::min(mean_grid(c->nres, dtype), kMaxGrid);

@@ -237,6 +237,12 @@ uint64_t mean_chunk_elems(sv_dtype dt);  // amplitudes per chunk of the mean ker
 // sum of (O a) (the first mu of an sv_iterate call).
 void launch_mean_grid(sv_dtype dt, const MeanArgs &a, int grid, bool write, cudaStream_t s);
 
+// All k mean-diffusion iterations in one cooperative launch when the state
+// fits the aggregate shared memory of one wave (mean_resident.cu).
+bool mean_resident_fits(sv_dtype dt, uint64_t N, size_t partials_cap);
+void launch_mean_resident(sv_dtype dt, void *a, uint64_t N, double inv_N, const uint64_t *marked, uint64_t m, int k,
+                          double *partials, unsigned int *bar, cudaStream_t s);
+
 void launch_init_uniform(sv_dtype dt, void *a, uint64_t N, int n, cudaStream_t s);
 void launch_init_zero(sv_dtype dt, void *a, uint64_t N, int has_origin, cudaStream_t s);
 // Gaussian (G8): pass 1 writes the local sum |z|^2 into *norm_out (fp64),

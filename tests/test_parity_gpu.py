@@ -383,3 +383,25 @@ def test_profile_counts_launches():
         launches, ms = sv.sv_profile_read(c, sv.SV_K_WHT_TILE)
         plan = sv.sv_plan_wht(n, 1, sv.SV_C64, 3, True)
         assert launches == len(plan) and ms > 0.0
+
+
+@pytest.mark.parametrize("dtype", DT, ids=DT_IDS)
+@pytest.mark.parametrize("n,m,k", [(14, 0, 3), (17, 5, 9), (20, 64, 6), (21, 300, 4)])
+def test_mean_resident_and_launched_paths(dtype, n, m, k, monkeypatch):
+    """The one-launch shared-memory-resident mean path (mean_resident.cu,
+    states within the aggregate shared memory) and the launched per-iteration
+    path (SV_MEAN_RESIDENT=0) both equal the oracle; M = 0 (O = I) included."""
+    a0 = rand_state(n, dtype)
+    marked = orc.marked_from_seed(n, m, 7) if m else np.zeros(0, np.uint64)
+    ref = orc.iterate(a0.copy(), marked, k, orc.MEAN)
+    for env in ("1", "0"):
+        monkeypatch.setenv("SV_MEAN_RESIDENT", env)
+        with ctx_with(a0, dtype) as c:
+            sv.sv_set_marked(c, marked)
+            sv.sv_profile(c, True)
+            sv.sv_iterate(c, k, sv.SV_DIFFUSE_MEAN)
+            launches, _ = sv.sv_profile_read(c, sv.SV_K_MEAN)
+            got = sv.sv_get_amplitudes(c)
+        fits = (1 << n) * (8 if dtype == sv.SV_C64 else 16) <= 148 * 200 * 1024
+        assert launches == (1 if (env == "1" and fits) else k), (env, launches)
+        assert_close(got, ref, dtype, f"mean resident={env} n={n}", n=n, k=k)
