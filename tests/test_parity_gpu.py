@@ -269,6 +269,58 @@ def test_c5_semantics_small_gaussian(dtype):
     assert_close(res["16"], cf.general_state(a0, marked, 16), dtype, "closed form k=16", n=n, k=16)
 
 
+def test_c5_n34_full_size_properties():
+    """c5 at its full size on one B200 (n=34 complex64, 128 GiB; Gaussian
+    start, M=1024 from seed, 8 iterations of each diffusion).  The oracle
+    cannot hold this state, so the check uses what the closed form fixes at
+    any size, with the start taken from the oracle's own generator
+    (a_i^(0) = z_i / ||z||, z = or_gauss_draw): the marked residual is
+    invariant, a_i^(k) - a_j^(k) = a_i^(0) - a_j^(0) for marked i, j, and the
+    unmarked residual alternates, a_i^(k) - a_j^(k) = (-1)^k (a_i^(0) - a_j^(0))
+    (DESIGN.md "General-start closed form").  So every sampled pair gives the
+    same 1/||z||, which the law of large numbers puts at 1/sqrt(2N) (sd ~ 1e-5
+    relative).  The two diffusions (independent code paths) must also agree
+    amplitude by amplitude (G11)."""
+    n, m, seed, k = 34, 1024, 5, 8
+    N = 1 << n
+    marked = sv.sv_marked_from_seed(n, m, seed)
+    mset = set(int(x) for x in marked)
+    rs = np.random.default_rng(34)
+    unm = []
+    while len(unm) < 512:
+        i = int(rs.integers(0, N))
+        if i not in mset:
+            unm.append(i)
+    idx = [int(x) for x in marked] + unm
+    z = {i: orc.gauss_draw(seed, i) for i in idx}
+    got = {}
+    for diff in (sv.SV_DIFFUSE_WHT, sv.SV_DIFFUSE_MEAN):
+        with sv.sv_init(n, seed, sv.SV_C64, sv.SV_INIT_GAUSSIAN) as c:
+            sv.sv_set_marked(c, marked)
+            sv.sv_iterate(c, k, diff)
+            got[diff] = {i: complex(sv.sv_get_amplitudes(c, i, 1)[0]) for i in idx}
+            got[(diff, "p")] = sv.sv_measure_marked_mass(c)
+    for diff in (sv.SV_DIFFUSE_WHT, sv.SV_DIFFUSE_MEAN):
+        a = got[diff]
+        ratios = []
+        for group, sign in ((idx[:m], 1.0), (unm, (-1.0) ** k)):
+            for t in range(0, len(group) - 1, 2):
+                i, j = group[t], group[t + 1]
+                dz = z[i] - z[j]
+                if abs(dz) < 0.5:
+                    continue
+                ratios.append(sign * (a[i] - a[j]) / dz)
+        ratios = np.array(ratios)
+        c0 = np.median(ratios.real)
+        assert np.max(np.abs(ratios - c0)) <= 1e-4 * c0, (diff, float(np.max(np.abs(ratios - c0)) / c0))
+        assert abs(c0 * math.sqrt(2.0 * N) - 1.0) <= 1e-3, c0 * math.sqrt(2.0 * N)
+    wht, mean = got[sv.SV_DIFFUSE_WHT], got[sv.SV_DIFFUSE_MEAN]
+    diff_max = max(abs(wht[i] - mean[i]) for i in idx)
+    scale = max(abs(wht[i]) for i in idx)
+    assert diff_max <= 2 * rel64(n, k) * scale, (diff_max, scale)
+    assert abs(got[(sv.SV_DIFFUSE_WHT, "p")] - got[(sv.SV_DIFFUSE_MEAN, "p")]) <= 1e-6
+
+
 # --------------------------------------------------------------------------- #
 # sharded schedule, emulated on one GPU                                        #
 # --------------------------------------------------------------------------- #
