@@ -70,7 +70,7 @@ GatePlan plan_gates(int n, int g, sv_dtype dtype, const sv_gate *gates, uint64_t
     p.n = n;
     p.g = g;
     p.nl = n - g;
-    p.T = tile_bits(dtype);
+    p.T = gate_tile_bits(dtype);
     if (count == 0) return p;
     if (g == 0 && n <= p.T) {  // the whole state is one CTA's shared-memory tile
         GateStep s;

@@ -151,7 +151,7 @@ __device__ __forceinline__ void load_op(const GOp<R> *op, R (&m)[8], unsigned in
 }
 
 template <typename E, int TB, int RB, bool XCHG>
-__global__ void __launch_bounds__(1 << (TB - RB), 2)
+__global__ void __launch_bounds__(1 << (TB - RB), (TB - RB <= 7) ? 4 : 2)
     gate_tile_kernel(const KParams p, const GOp<typename RealOf<E>::T> *__restrict__ ops, int nops) {
     using L = Layout<E, TB, RB>;
     using R = typename RealOf<E>::T;
@@ -453,7 +453,7 @@ uint64_t build_gate_ops(sv_dtype dt, const GatePassArgs &a, bool whole, std::vec
     if (dt == SV_C64) {
         std::vector<GOp<float>> ops;
         if (whole) whole_ops<float2>(a, ops);
-        else build_tile_ops<Layout<float2, kTileBitsC64, kRegBitsC64>, float>(a, ops);
+        else build_tile_ops<Layout<float2, kGateTileBitsC64, kRegBitsC64>, float>(a, ops);
         return append_ops(ops, prog);
     }
     std::vector<GOp<double>> ops;
@@ -463,7 +463,7 @@ uint64_t build_gate_ops(sv_dtype dt, const GatePassArgs &a, bool whole, std::vec
 }
 
 void launch_gate_pass(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, uint64_t nops, cudaStream_t s) {
-    if (dt == SV_C64) launch_tile_gates<float2, kTileBitsC64, kRegBitsC64>(a, dev_ops, nops, s);
+    if (dt == SV_C64) launch_tile_gates<float2, kGateTileBitsC64, kRegBitsC64>(a, dev_ops, nops, s);
     else launch_tile_gates<double2, kTileBitsC128, kRegBitsC128>(a, dev_ops, nops, s);
 }
 

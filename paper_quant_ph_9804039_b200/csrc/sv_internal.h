@@ -59,6 +59,13 @@ constexpr int kCarryC64 = 3;
 constexpr int kCarryC128 = 2;
 
 inline int tile_bits(sv_dtype d) { return d == SV_C64 ? kTileBitsC64 : kTileBitsC128; }
+// gate-circuit tiles (gates.cu) may be smaller than the WHT tiles: more
+// co-resident CTAs hide the compute of many-gate passes behind memory
+#ifndef SV_GATE_TILE_BITS_C64
+#define SV_GATE_TILE_BITS_C64 13
+#endif
+constexpr int kGateTileBitsC64 = SV_GATE_TILE_BITS_C64;
+inline int gate_tile_bits(sv_dtype d) { return d == SV_C64 ? kGateTileBitsC64 : kTileBitsC128; }
 inline int carry_bits(sv_dtype d) { return d == SV_C64 ? kCarryC64 : kCarryC128; }
 inline size_t elem_bytes(sv_dtype d) { return d == SV_C64 ? 8 : 16; }
 
