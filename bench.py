@@ -185,6 +185,34 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def nvlink_report(sv, ctx, n, world, dtype, k, timeline):
+    """The NVLink roofline of the sharded WHT: each qubit swap
+    moves (1 - 1/P) S_l per GPU each way.  Fused exchange: the pass before a
+    swap stores those bytes straight into the peers (CUDA IPC over NVLink), so
+    its time bounds the NVLink rate from below; all-to-all: the collective's
+    own time.  Attributed from the library's per-launch CUDA events and its
+    host schedule (sv_plan_wht)."""
+    plan = [st["kind"] for st in sv.sv_plan_wht(n, world, dtype, k, True) if st["kind"] in (0, 1)]
+    seq = [ms for kind, ms in timeline if kind in (sv.SV_K_WHT_TILE, sv.SV_K_EXCHANGE)]
+    L = len(plan)
+    steps = len(seq) // L
+    assert steps >= 1 and steps * L == len(seq), (len(seq), L)
+    pre = [i for i in range(L - 1) if plan[i] == 0 and plan[i + 1] == 1]
+    t_pre = [seq[j * L + i] for j in range(steps) for i in pre]
+    t_swap = [seq[j * L + i] for j in range(steps) for i in range(L) if plan[i] == 1]
+    t_other = [seq[j * L + i] for j in range(steps) for i in range(L) if plan[i] == 0 and i not in pre]
+    S_l = (1 << n) // world * (8 if dtype == sv.SV_C64 else 16)
+    moved = (1.0 - 1.0 / world) * S_l
+    fused = sv.sv_get_exchange(ctx)
+    t_move = (sum(t_pre) / len(t_pre)) if fused else (sum(t_swap) / len(t_swap))
+    ach = moved / (t_move / 1e3) / 1e9
+    return {"bound": "nvlink", "mode": "fused peer stores" if fused else "ncclAlltoAll",
+            "bytes_per_swap_per_gpu": moved, "swaps_per_step": len(t_swap) // steps,
+            "preswap_pass_ms": sum(t_pre) / max(len(t_pre), 1), "other_pass_ms": sum(t_other) / max(len(t_other), 1),
+            "swap_step_ms": sum(t_swap) / max(len(t_swap), 1), "achieved": ach, "peak": 900.0, "unit": "GB/s",
+            "frac": ach / 900.0, "peak_source": "nominal NVLink 5 per direction (B200_PROFILING.md)"}
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -241,6 +269,12 @@ def run_ours(args):
     torch.cuda.synchronize()
     t_ms = svd.max_over_ranks(ev0.elapsed_time(ev1))
     prof = {sv.KERNEL_KIND_NAMES[i]: sv.sv_profile_read(ctx, i) for i in range(sv.SV_K_COUNT)}
+    nvlink = None
+    if world > 1 and diff != "mean":
+        try:
+            nvlink = nvlink_report(sv, ctx, n, world, dtype, k, sv.sv_profile_timeline(ctx))
+        except Exception as e:  # reporting only: never lose the bench line
+            nvlink = {"error": repr(e)[:200]}
     sv.sv_profile(ctx, False)
     N_amp = 1 << n
     esz = 8 if dtype == sv.SV_C64 else 16
@@ -306,6 +340,7 @@ def run_ours(args):
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
                 "clocks": clocks.summary(),
                 "phases_ms": {nm: v[1] for nm, v in prof.items() if v[0]},
+                "nvlink": nvlink,
                 "p_success": p_success}
         print(json.dumps(line), flush=True)
     sv.sv_free(ctx)

@@ -1,0 +1,51 @@
+"""bench.py host logic without a GPU: the NVLink attribution of a sharded run
+(nvlink_report) on a synthetic per-launch timeline laid out like the
+library's schedule, and the CLI contract (configs, defaults)."""
+import types
+
+import pytest
+
+import bench
+import paper_quant_ph_9804039_b200 as sv
+
+
+def shim(fused):
+    m = types.SimpleNamespace(**{k: getattr(sv, k) for k in dir(sv) if k.startswith("SV_")})
+    m.sv_plan_wht = sv.sv_plan_wht
+    m.sv_get_exchange = lambda ctx: fused
+    return m
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("fused", [True, False])
+def test_nvlink_report_attribution(world, fused):
+    n, k, steps = 32, 4, 3
+    plan = [st["kind"] for st in sv.sv_plan_wht(n, world, sv.SV_C64, k, True) if st["kind"] in (0, 1)]
+    pre = {i for i in range(len(plan) - 1) if plan[i] == 0 and plan[i + 1] == 1}
+    tl = []
+    for _ in range(steps):
+        tl.append((sv.SV_K_INIT, 1.0))  # sv_reset's launch: ignored
+        for i, kind in enumerate(plan):
+            if kind == 1:
+                tl.append((sv.SV_K_EXCHANGE, 3.0))
+            else:
+                tl.append((sv.SV_K_WHT_TILE, 9.0 if i in pre else 5.0))
+    r = bench.nvlink_report(shim(fused), None, n, world, sv.SV_C64, k, tl)
+    S_l = (1 << n) // world * 8
+    moved = (1 - 1 / world) * S_l
+    assert r["swaps_per_step"] == 2 * k
+    assert r["preswap_pass_ms"] == 9.0 and r["other_pass_ms"] == 5.0 and r["swap_step_ms"] == 3.0
+    t = 9.0 if fused else 3.0
+    assert r["achieved"] == pytest.approx(moved / (t / 1e3) / 1e9)
+    assert r["frac"] == pytest.approx(r["achieved"] / 900.0)
+
+
+def test_configs_and_defaults():
+    assert bench.CONFIGS["c4"][:5] == (32, "c64", 256, 16, "wht")  # BASELINE.json configs[3]
+    import sys
+    argv, sys.argv = sys.argv, ["bench.py"]
+    try:
+        args = bench.parse()
+    finally:
+        sys.argv = argv
+    assert (args.gpus, args.config, args.impl) == (1, "c4", "ours") and args.warmup >= 3
