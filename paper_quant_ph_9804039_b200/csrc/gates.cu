@@ -100,8 +100,12 @@ __device__ __forceinline__ void gate_apply(E (&x)[NR], const R (&m)[8], unsigned
             if (((unsigned int)j & jm) == jm) cmat_k<K>(x[j], x[j | (1 << I)], m);
 }
 
+#ifndef SV_GATE_KINDS
+#define SV_GATE_KINDS 2  // 2: all shapes; 1: general + phase; 0: general only (smaller code)
+#endif
 template <int I, int NR, typename E, typename R>
 __device__ __forceinline__ void gate_apply_kind(E (&x)[NR], const R (&m)[8], unsigned int jm, unsigned int kind) {
+#if SV_GATE_KINDS >= 2
     switch (kind) {
         case GK_DIAG: gate_apply<I, GK_DIAG>(x, m, jm); break;
         case GK_PHASE: gate_apply<I, GK_PHASE>(x, m, jm); break;
@@ -109,6 +113,13 @@ __device__ __forceinline__ void gate_apply_kind(E (&x)[NR], const R (&m)[8], uns
         case GK_SWAP: gate_apply<I, GK_SWAP>(x, m, jm); break;
         default: gate_apply<I, GK_GENERAL>(x, m, jm); break;
     }
+#elif SV_GATE_KINDS == 1
+    if (kind == GK_PHASE) gate_apply<I, GK_PHASE>(x, m, jm);
+    else gate_apply<I, GK_GENERAL>(x, m, jm);
+#else
+    (void)kind;
+    gate_apply<I, GK_GENERAL>(x, m, jm);
+#endif
 }
 
 template <class L, typename E, typename R>
