@@ -25,6 +25,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <complex>
 
 #include "wht_kernels.cuh"
 
@@ -50,7 +51,21 @@ enum GateKind : unsigned int {
     GK_PHASE = 2,     // x = y = 0, w = 1: (u, z v)
     GK_ANTI = 3,      // w = z = 0: (x v, y u)
     GK_SWAP = 4,      // w = z = 0, x = y = 1 (NOT): (v, u)
+    GK_LINPHASE = 5,  // merged run of phase gates on one target, <= 1 control each (below)
 };
+
+// GK_LINPHASE: the product of phase gates diag(1, z_g) on one target t, each
+// with at most one control c_g, multiplies amplitude i by
+//   prod_g z_g^(b_t(i) b_cg(i))  =  [b_t(i)] F(thread, tile) R(register bits),
+// a phase that factorises over the control bits (degree-2 phase polynomial,
+// as in the QFT).  The host merges a run of such gates (diagonal gates
+// commute) into ONE op; it needs no relayout (its target need not be a
+// register bit) and costs ~40 complex multiplies per thread instead of one
+// dispatched op per gate.  The op record is followed by `tm` entry records:
+// m[0], m[1] = z; ri = where the control lives (LP_*); jm = its register
+// index / tile bit / slot.  The op's own ri/jm say where the TARGET lives
+// (LP_REG with register index, or LP_THR with tile bit).
+enum LinWhere : unsigned int { LP_REG = 0, LP_THR = 1, LP_FREE = 2, LP_CONST = 3 };
 
 // (u, v) <- (w u + x v, y u + z v), complex.
 template <typename E, typename R>
@@ -161,7 +176,74 @@ __device__ __forceinline__ void load_op(const GOp<R> *op, R (&m)[8], unsigned in
     fm = __ldg(&op->fm);
 }
 
-template <typename E, int TB, int RB, bool XCHG>
+template <typename E, typename R>
+__device__ __forceinline__ void cmul_by(E &a, R br, R bi) {
+    const E t = a;
+    a.x = t.x * br - t.y * bi;
+    a.y = t.x * bi + t.y * br;
+}
+template <typename E>
+__device__ __forceinline__ E cprod(const E &a, const E &b) {
+    E r;
+    r.x = a.x * b.x - a.y * b.y;
+    r.y = a.x * b.y + a.y * b.x;
+    return r;
+}
+
+template <class L, typename E, typename R>
+__device__ __forceinline__ void apply_linphase(E (&x)[L::NR], const GOp<R> *ent, unsigned int cnt, unsigned int tcls,
+                                               unsigned int tbit, unsigned int et, unsigned long long base,
+                                               unsigned int nthr) {
+    constexpr int RB = L::kRB, LO = RB < 3 ? RB : 3, HI = RB - LO;
+    // entries: [0, RB) per-register-bit factors, [RB, RB + nthr) thread-bit
+    // factors, then the tile-uniform free-slot / constant factors -- those are
+    // the same for the whole CTA, so the lanes of a warp take them in
+    // parallel and combine them in a fixed tree (every lane gets lane 0's
+    // product: identical, deterministic)
+    const unsigned int lane = threadIdx.x & 31u;
+    E F;
+    F.x = (R)1;
+    F.y = (R)0;
+    for (unsigned int e = RB + nthr + lane; e < cnt; e += 32u) {
+        const unsigned int w = __ldg(&ent[e].ri), bit = __ldg(&ent[e].jm);
+        if (w == LP_CONST || ((base >> bit) & 1ull)) cmul_by(F, __ldg(&ent[e].m[0]), __ldg(&ent[e].m[1]));
+    }
+    if (cnt > RB + nthr) {  // any tile-uniform entries: every lane needs the full product
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            E t;
+            t.x = __shfl_down_sync(0xffffffffu, F.x, o);
+            t.y = __shfl_down_sync(0xffffffffu, F.y, o);
+            if (lane + o < 32u) F = cprod(F, t);
+        }
+        F.x = __shfl_sync(0xffffffffu, F.x, 0);
+        F.y = __shfl_sync(0xffffffffu, F.y, 0);
+    }
+    if (tcls == LP_THR && !((et >> tbit) & 1u)) return;  // target bit 0 for all of this thread's amplitudes
+    E P[RB];
+#pragma unroll
+    for (int i = 0; i < RB; ++i) { P[i].x = __ldg(&ent[i].m[0]); P[i].y = __ldg(&ent[i].m[1]); }
+    for (unsigned int e = RB; e < RB + nthr; ++e)
+        if ((et >> __ldg(&ent[e].jm)) & 1u) cmul_by(F, __ldg(&ent[e].m[0]), __ldg(&ent[e].m[1]));
+    // factor of register index j = F * prod_{i in bits(j)} P[i]: tables over
+    // the low LO and the high HI register bits
+    E lo[1 << LO], hi[1 << HI];
+    lo[0].x = (R)1;
+    lo[0].y = (R)0;
+#pragma unroll
+    for (int j = 1; j < (1 << LO); ++j) lo[j] = cprod(lo[j & (j - 1)], (j & 1) ? P[0] : ((j & 2) ? P[1] : P[RB > 2 ? 2 : 0]));
+    hi[0] = F;
+#pragma unroll
+    for (int j = 1; j < (1 << HI); ++j) hi[j] = cprod(hi[j & (j - 1)], (j & 1) ? P[LO < RB ? LO : 0] : P[LO + 1 < RB ? LO + 1 : 0]);
+#pragma unroll
+    for (int j = 0; j < L::NR; ++j)
+        if (tcls != LP_REG || ((j >> tbit) & 1)) {
+            const E f = cprod(lo[j & ((1 << LO) - 1)], hi[j >> LO]);
+            x[j] = cprod(x[j], f);
+        }
+}
+
+template <typename E, int TB, int RB, bool XCHG, bool LIN>
 __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB <= 7) ? 4 : 2)
     gate_tile_kernel(const KParams p, const GOp<typename RealOf<E>::T> *__restrict__ ops, int nops) {
     using L = Layout<E, TB, RB>;
@@ -188,6 +270,13 @@ __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB <= 7) ? 4 : 2)
             cur = ph;
         }
         const unsigned int et = cur == 0 ? eth[0] : (cur == 1 ? eth[1] : eth[2]);
+        if constexpr (LIN) {  // passes holding merged phase runs get their own instantiation
+            if (kind == GK_LINPHASE) {  // tm entry records follow
+                apply_linphase<L>(x, ops + k + 1, tm, ri, jm, et, base, (unsigned int)fm);
+                k += (int)tm;
+                continue;
+            }
+        }
         if ((et & tm) == tm && (base & fm) == fm) gate_dispatch<L>(x, m, ri, jm, kind);
     }
     E *gout = reinterpret_cast<E *>(p.out) + base;
@@ -262,18 +351,28 @@ void build_tile_ops(const GatePassArgs &a, std::vector<GOp<R>> &out) {
     int b = 0;
     for (int sl = 0; sl < 64; ++sl)
         if ((a.tile_mask >> sl) & 1) slot2bit[sl] = b++;
+    struct LinEntry {
+        int where;   // 0 tile bit, 1 free slot, 2 none
+        int bit;     // tile bit / slot
+        double zr, zi;
+        sv_gate src;           // the original gate (a short run is emitted gate by gate)
+        unsigned int tc;
+        unsigned long long fm;
+    };
     struct Pend {
-        sv_gate g;           // the gate (matrix possibly fused with later ones)
+        sv_gate g;           // the gate (matrix possibly fused with later ones); for a merged phase
+                             // run: diag(1, 1) with the union of the controls (commutation proxy)
         int bt;              // target tile bit
         unsigned int tc;     // controls on tile bits (tile-element space)
         unsigned long long fm;
+        std::vector<LinEntry> lin;  // non-empty: a merged run of phase gates (GK_LINPHASE)
     };
     std::vector<Pend> pend;
     for (uint64_t k = 0; k < a.count; ++k) {
         const sv_gate &g = a.gates[a.order[k]];
         const int pt = gate_phys(g.target, a.nl, a.g, a.swapped);
         SV_CHECK(slot2bit[pt] >= 0, SV_EINVAL, "internal: gate target outside its pass tile");
-        Pend pd{g, slot2bit[pt], 0u, 0ull};
+        Pend pd{g, slot2bit[pt], 0u, 0ull, {}};
         bool live = true;
         for (int q = 0; q < a.n; ++q) {
             if (!((g.controls >> q) & 1ull)) continue;
@@ -287,6 +386,34 @@ void build_tile_ops(const GatePassArgs &a, std::vector<GOp<R>> &out) {
             }
         }
         if (!live) continue;
+        // Phase gates diag(1, z) with at most one (live) control are merged
+        // into a run on their target (GK_LINPHASE) when only commuting ops lie
+        // between -- checked before the 2x2 fusion below.
+        const bool phase1 = gate_kind(g) == GK_PHASE && __builtin_popcount(pd.tc) + __builtin_popcountll(pd.fm) <= 1;
+        if (phase1) {
+            LinEntry le{2, 0, g.m[6], g.m[7], g, pd.tc, pd.fm};
+            if (pd.tc) { le.where = 0; le.bit = __builtin_ctz(pd.tc); }
+            else if (pd.fm) { le.where = 1; le.bit = __builtin_ctzll(pd.fm); }
+            bool merged = false;
+            CommuteSet between;
+            for (size_t i = pend.size(); i-- > 0;) {
+                Pend &e = pend[i];
+                if (!e.lin.empty() && e.bt == pd.bt && between.commutes(g)) {
+                    e.lin.push_back(le);
+                    e.g.controls |= g.controls;
+                    merged = true;
+                    break;
+                }
+                between.add(e.g);
+                if (!between.commutes(g)) break;
+            }
+            if (merged) continue;
+            pd.lin.push_back(le);
+            pd.g.m[6] = 1.0;  // proxy: diagonal, support = target + controls
+            pd.g.m[7] = 0.0;
+            pend.push_back(pd);
+            continue;
+        }
         // Fusion: a gate with the same target and controls as an earlier op
         // of this pass, with only commuting ops in between, is multiplied
         // into it (host fp64 2x2 product M_later * M_earlier).
@@ -294,7 +421,7 @@ void build_tile_ops(const GatePassArgs &a, std::vector<GOp<R>> &out) {
         CommuteSet between;
         for (size_t i = pend.size(); i-- > 0;) {
             sv_gate &e = pend[i].g;
-            if (e.target == g.target && e.controls == g.controls && between.commutes(g)) {
+            if (pend[i].lin.empty() && e.target == g.target && e.controls == g.controls && between.commutes(g)) {
                 double r[8];
                 for (int rr = 0; rr < 2; ++rr)
                     for (int cc = 0; cc < 2; ++cc) {
@@ -317,6 +444,21 @@ void build_tile_ops(const GatePassArgs &a, std::vector<GOp<R>> &out) {
         }
         if (!fused) pend.push_back(pd);
     }
+    // A merged phase run pays ~40 complex multiplies per thread for its
+    // factor tables: runs of fewer than kMinLinRun gates go back to one op
+    // per gate (all diagonal: they commute, so their order is free).
+    constexpr size_t kMinLinRun = 4;
+    {
+        std::vector<Pend> expanded;
+        for (Pend &pd : pend) {
+            if (pd.lin.empty() || pd.lin.size() >= kMinLinRun) {
+                expanded.push_back(std::move(pd));
+                continue;
+            }
+            for (const LinEntry &le : pd.lin) expanded.push_back(Pend{le.src, pd.bt, le.tc, le.fm, {}});
+        }
+        pend.swap(expanded);
+    }
     // Layout schedule: in the current layout run every ready op (commutes
     // with all earlier pending ops) whose target is a register bit; when none
     // is left, move to the layout that runs the most ready ops next.
@@ -324,7 +466,8 @@ void build_tile_ops(const GatePassArgs &a, std::vector<GOp<R>> &out) {
         CommuteSet skipped;
         int cnt = 0;
         for (size_t i = 0; i < pend.size(); ++i) {
-            if (skipped.commutes(pend[i].g) && L::is_reg(ph, pend[i].bt)) {
+            // a merged phase run needs no register target: it runs in any layout
+            if (skipped.commutes(pend[i].g) && (!pend[i].lin.empty() || L::is_reg(ph, pend[i].bt))) {
                 ++cnt;
                 if (take) take->push_back(i);
             } else {
@@ -352,6 +495,55 @@ void build_tile_ops(const GatePassArgs &a, std::vector<GOp<R>> &out) {
         std::vector<char> used(pend.size(), 0);
         for (size_t i : take) {
             const Pend &pd = pend[i];
+            if (!pd.lin.empty()) {
+                GOp<R> o{};
+                o.ph = (GK_LINPHASE << 8) | (unsigned int)cur;
+                o.ri = LP_THR;
+                o.jm = (unsigned int)pd.bt;
+                for (int r = 0; r < L::kRB; ++r)
+                    if (L::reg_bit(cur, r) == pd.bt) { o.ri = LP_REG; o.jm = (unsigned int)r; }
+                // host fp64 products: per register bit of this layout, per
+                // thread tile bit, per free slot, and the constant factor
+                std::complex<double> preg[16], pthr[16], pconst(1.0, 0.0);
+                std::vector<std::pair<int, std::complex<double>>> pfree;
+                for (int r = 0; r < 16; ++r) { preg[r] = 1.0; pthr[r] = 1.0; }
+                for (const LinEntry &le : pd.lin) {
+                    const std::complex<double> z(le.zr, le.zi);
+                    if (le.where == 2) { pconst *= z; continue; }
+                    if (le.where == 1) {
+                        bool found = false;
+                        for (auto &f : pfree)
+                            if (f.first == le.bit) { f.second *= z; found = true; }
+                        if (!found) pfree.push_back({le.bit, z});
+                        continue;
+                    }
+                    int reg = -1;
+                    for (int r = 0; r < L::kRB; ++r)
+                        if (L::reg_bit(cur, r) == le.bit) reg = r;
+                    if (reg >= 0) preg[reg] *= z;
+                    else pthr[le.bit] *= z;
+                }
+                std::vector<GOp<R>> ent;
+                auto rec = [&](unsigned int w, unsigned int bit, std::complex<double> z) {
+                    GOp<R> e{};
+                    e.m[0] = (R)z.real();
+                    e.m[1] = (R)z.imag();
+                    e.ri = w;
+                    e.jm = bit;
+                    ent.push_back(e);
+                };
+                for (int r = 0; r < L::kRB; ++r) rec(LP_REG, (unsigned int)r, preg[r]);
+                for (int t = 0; t < L::kTB; ++t)
+                    if (pthr[t] != std::complex<double>(1.0, 0.0)) rec(LP_THR, (unsigned int)t, pthr[t]);
+                o.fm = ent.size() - (size_t)L::kRB;  // thread-bit entries come first
+                if (pconst != std::complex<double>(1.0, 0.0)) rec(LP_CONST, 0u, pconst);
+                for (auto &f : pfree) rec(LP_FREE, (unsigned int)f.first, f.second);
+                o.tm = (unsigned int)ent.size();
+                out.push_back(o);
+                out.insert(out.end(), ent.begin(), ent.end());
+                used[i] = 1;
+                continue;
+            }
             GOp<R> o = op_coefs<R>(pd.g);
             o.ph |= (unsigned int)cur;
             o.ri = 0;
@@ -386,7 +578,7 @@ size_t append_ops(const std::vector<GOp<R>> &ops, std::vector<unsigned char> &pr
 }
 
 template <typename E, int TB, int RB>
-void launch_tile_gates(const GatePassArgs &a, const void *dev_ops, uint64_t nops, cudaStream_t s) {
+void launch_tile_gates(const GatePassArgs &a, const void *dev_ops, uint64_t nops, bool lin, cudaStream_t s) {
     using L = Layout<E, TB, RB>;
     using R = typename RealOf<E>::T;
     KParams kp{};
@@ -416,14 +608,14 @@ void launch_tile_gates(const GatePassArgs &a, const void *dev_ops, uint64_t nops
     SV_CHECK(nops <= 0x7fffffffull, SV_EINVAL, "too many gates in one pass");
     const unsigned long long ntiles = 1ull << f;
     SV_CHECK(ntiles <= 0x7fffffffull, SV_EINVAL, "too many tiles for one launch");
-    auto fn = kp.xchg ? gate_tile_kernel<E, TB, RB, true> : gate_tile_kernel<E, TB, RB, false>;
+    auto fn = lin ? (kp.xchg ? gate_tile_kernel<E, TB, RB, true, true> : gate_tile_kernel<E, TB, RB, false, true>)
+                  : (kp.xchg ? gate_tile_kernel<E, TB, RB, true, false> : gate_tile_kernel<E, TB, RB, false, false>);
     const int smem = (1 << TB) * (int)sizeof(E);
     static bool attr = false;
     if (!attr) {
-        SV_CUDA(cudaFuncSetAttribute(gate_tile_kernel<E, TB, RB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     smem));
-        SV_CUDA(cudaFuncSetAttribute(gate_tile_kernel<E, TB, RB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     smem));
+        for (auto f : {gate_tile_kernel<E, TB, RB, true, true>, gate_tile_kernel<E, TB, RB, false, true>,
+                       gate_tile_kernel<E, TB, RB, true, false>, gate_tile_kernel<E, TB, RB, false, false>})
+            SV_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;
     }
     fn<<<(unsigned int)ntiles, L::NT, smem, s>>>(kp, reinterpret_cast<const GOp<R> *>(dev_ops), (int)nops);
@@ -458,24 +650,33 @@ void launch_whole_gates(const GatePassArgs &a, const void *dev_ops, uint64_t nop
 
 }  // namespace
 
-uint64_t build_gate_ops(sv_dtype dt, const GatePassArgs &a, bool whole, std::vector<unsigned char> &prog) {
+uint64_t build_gate_ops(sv_dtype dt, const GatePassArgs &a, bool whole, std::vector<unsigned char> &prog,
+                        bool *has_lin) {
     // every op record is 16-byte aligned inside the program
     prog.resize((prog.size() + 15) & ~(size_t)15);
+    auto lin_in = [](const auto &ops) {
+        for (const auto &o : ops)
+            if ((o.ph >> 8) == GK_LINPHASE) return true;
+        return false;
+    };
     if (dt == SV_C64) {
         std::vector<GOp<float>> ops;
         if (whole) whole_ops<float2>(a, ops);
         else build_tile_ops<Layout<float2, kGateTileBitsC64, kRegBitsC64>, float>(a, ops);
+        if (has_lin) *has_lin = lin_in(ops);
         return append_ops(ops, prog);
     }
     std::vector<GOp<double>> ops;
     if (whole) whole_ops<double2>(a, ops);
     else build_tile_ops<Layout<double2, kTileBitsC128, kRegBitsC128>, double>(a, ops);
+    if (has_lin) *has_lin = lin_in(ops);
     return append_ops(ops, prog);
 }
 
-void launch_gate_pass(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, uint64_t nops, cudaStream_t s) {
-    if (dt == SV_C64) launch_tile_gates<float2, kGateTileBitsC64, kRegBitsC64>(a, dev_ops, nops, s);
-    else launch_tile_gates<double2, kTileBitsC128, kRegBitsC128>(a, dev_ops, nops, s);
+void launch_gate_pass(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, uint64_t nops, bool has_lin,
+                      cudaStream_t s) {
+    if (dt == SV_C64) launch_tile_gates<float2, kGateTileBitsC64, kRegBitsC64>(a, dev_ops, nops, has_lin, s);
+    else launch_tile_gates<double2, kTileBitsC128, kRegBitsC128>(a, dev_ops, nops, has_lin, s);
 }
 
 void launch_gate_whole(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, uint64_t nops, cudaStream_t s) {

@@ -384,11 +384,14 @@ void run_gates(sv_ctx *c, const sv_gate *gates, uint64_t count) {
     };
     std::vector<unsigned char> prog;
     std::vector<std::pair<size_t, uint64_t>> where(gp.steps.size(), {0, 0});
+    std::vector<char> lin(gp.steps.size(), 0);
     for (size_t i = 0; i < gp.steps.size(); ++i) {
         const GateStep &st = gp.steps[i];
         if (st.kind == GSTEP_SWAP) continue;
         const size_t off = (prog.size() + 15) & ~(size_t)15;
-        where[i] = {off, build_gate_ops(c->dt, args(st), st.kind == GSTEP_WHOLE, prog)};
+        bool hl = false;
+        where[i] = {off, build_gate_ops(c->dt, args(st), st.kind == GSTEP_WHOLE, prog, &hl)};
+        lin[i] = hl ? 1 : 0;
     }
     if (prog.size() > c->gprog_cap) {
         if (c->d_gprog) SV_CUDA(cudaFree(c->d_gprog));
@@ -439,7 +442,7 @@ void run_gates(sv_ctx *c, const sv_gate *gates, uint64_t count) {
                     a.xchg_dst[j] = to_recv ? c->peer_recv[j] : c->peer_state[j];
             }
         }
-        run(c, SV_K_GATE_TILE, [&] { launch_gate_pass(c->dt, a, ops, where[i].second, c->stream); });
+        run(c, SV_K_GATE_TILE, [&] { launch_gate_pass(c->dt, a, ops, where[i].second, lin[i] != 0, c->stream); });
         if (!c->fused_xchg) cur = c->state;
     }
     if (cur != c->state)

@@ -185,9 +185,12 @@ struct GatePassArgs {
 };
 // Append the op program of one pass (whole: the one-CTA kernel) to `prog`
 // (16-byte aligned records); returns the op count.  Ops whose rank-bit
-// controls fail on this rank are dropped.
-uint64_t build_gate_ops(sv_dtype dt, const GatePassArgs &a, bool whole, std::vector<unsigned char> &prog);
-void launch_gate_pass(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, uint64_t nops, cudaStream_t s);
+// controls fail on this rank are dropped.  *has_lin: the pass holds merged
+// phase runs (launched with the kernel instantiation that handles them).
+uint64_t build_gate_ops(sv_dtype dt, const GatePassArgs &a, bool whole, std::vector<unsigned char> &prog,
+                        bool *has_lin);
+void launch_gate_pass(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, uint64_t nops, bool has_lin,
+                      cudaStream_t s);
 void launch_gate_whole(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, uint64_t nops, cudaStream_t s);
 
 // ------------------------------------------------------------------------- //

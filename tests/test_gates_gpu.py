@@ -97,6 +97,39 @@ def test_fusable_runs_match_oracle(dtype):
     assert_close(run_gpu(a, dtype, gates), ref, dtype, gates.size, "fusable runs")
 
 
+def phase_run_circuit(n, seed):
+    """Runs of phase gates diag(1, e^{i theta}) on one target with at most one
+    control each (merged into one phase-polynomial op when >= 4 long), run
+    lengths 1..12, controls anywhere (register, thread or free tile slots,
+    none), interleaved with H / X on other qubits and a few 2-control phases."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for t in [0, 2, 5, 9, 12, n - 1, n // 2, 3, n - 2]:
+        for _ in range(int(rng.integers(1, 13))):
+            if rng.random() < 0.15:
+                out.append(C.record(t, C.phase(float(rng.uniform(-3, 3)))))
+            else:
+                c = int(rng.choice([q for q in range(n) if q != t]))
+                out.append(C.record(t, C.phase(float(rng.uniform(-3, 3))), [c]))
+            if rng.random() < 0.3:  # commuting (other target, not a control of the run) or not
+                q = int(rng.integers(0, n))
+                if q != t:
+                    out.append(C.record(q, C.H))
+        out.append(C.record(t, C.H))
+        cs = [q for q in range(n) if q != t][:2]
+        out.append(C.record(t, C.phase(0.7), cs))
+    return C.circuit(out)
+
+
+@pytest.mark.parametrize("dtype", DT, ids=DT_IDS)
+@pytest.mark.parametrize("n,world", [(16, 1), (21, 1), (19, 4)])
+def test_phase_runs_match_oracle(dtype, n, world):
+    gates = phase_run_circuit(n, n * 7 + world)
+    a = rand_state(n, dtype, 300 + n)
+    ref = orc.apply_gates(a.copy(), gates)
+    assert_close(run_gpu(a, dtype, gates, world=world), ref, dtype, gates.size, f"phase runs n={n} P={world}")
+
+
 @pytest.mark.parametrize("dtype", DT, ids=DT_IDS)
 def test_layered_circuit_matches_oracle(dtype):
     n = 20
