@@ -226,8 +226,13 @@ typedef struct {
 } sv_gate;
 
 /* Apply gates[0..count) to the state, in order (gates may be regrouped only
- * where they commute: different targets, neither controlled by the other's
- * target).  The host planner packs consecutive runs of gates on up to T
+ * where they commute: different targets and neither controlled by the other's
+ * target; a diagonal gate commutes with any gate whose target is outside its
+ * support; diagonal gates commute).  Results equal the gate-by-gate product up
+ * to rounding: the host multiplies same-target same-control gates separated
+ * only by commuting gates into one fp64 2x2, and merges runs of >= 4
+ * single-control phase gates on one target into one phase-polynomial op.
+ * The host planner packs consecutive runs of gates on up to T
  * local qubits into one tile pass each (one HBM read + write per pass, all of
  * the pass's gates on-chip); a gate on a parallel (rank) qubit first triggers
  * the qubit swap of section 3.1 / Fig. 8 ("when the computation needs to
