@@ -248,9 +248,11 @@ sv_status sv_apply_gates(sv_ctx *ctx, const sv_gate *gates, uint64_t count);
  * as in sv_plan_step, in PHYSICAL slots of the shard; its gates are
  * order[first .. first + count)), kind 1 = qubit-swap exchange (physical
  * slots [nl - g, nl) <-> the g rank bits), kind 2 = whole state in one CTA.
- * ops: 2x2 operations the pass runs after the host fuses each gate into an
- * earlier one with the same target and controls when only commuting gates
- * lie between them (fp64 product of the two matrices). */
+ * ops: operations the pass runs after the host merging (a gate is multiplied
+ * into an earlier one with the same target and controls when only commuting
+ * gates lie between them; runs of >= 4 single-control phase gates on one
+ * target become one phase-polynomial op); lin_ops: how many of them are such
+ * merged phase runs. */
 typedef struct {
     int kind;
     int tile_bits;
@@ -259,6 +261,7 @@ typedef struct {
     uint64_t first;
     uint64_t count;
     uint64_t ops;
+    uint64_t lin_ops;
 } sv_gate_plan_step;
 
 /* The schedule sv_apply_gates enqueues on every rank for an n-qubit state over

@@ -49,7 +49,7 @@ class sv_plan_step(ctypes.Structure):
 class sv_gate_plan_step(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int), ("tile_bits", ctypes.c_int), ("tile_mask", ctypes.c_uint64),
                 ("proc_mask", ctypes.c_uint64), ("first", ctypes.c_uint64), ("count", ctypes.c_uint64),
-                ("ops", ctypes.c_uint64)]
+                ("ops", ctypes.c_uint64), ("lin_ops", ctypes.c_uint64)]
 
 
 if not os.path.exists(LIB_PATH):

@@ -131,6 +131,7 @@ class B200Params:
     bw_reduce: float = 6.981e+12      # read-only sum pass (S_l)
     t_gate: float = 6.638e-13          # seconds per amplitude pair per general 2x2 op (compute term)
     t_diag: float = 4.509e-13          # ... per diagonal op (phase / controlled phase)
+    t_lin: float = 1.2e-12          # ... per merged phase-polynomial op (a run of >= 4 single-control phases)
     bw_nvlink: float = 900e9       # per direction, NVLink 5 (nominal)
     bw_copy: float = 6.351e+12        # device-local copy (emulated exchange), bytes moved / s
     t_lat: float = 15e-6           # one NCCL collective
@@ -211,6 +212,11 @@ def _is_diag(g) -> bool:
     return m[2] == 0.0 and m[3] == 0.0 and m[4] == 0.0 and m[5] == 0.0
 
 
+def _is_phase1(g) -> bool:
+    m = g["m"]
+    return _is_diag(g) and m[0] == 1.0 and m[1] == 0.0 and bin(int(g["controls"])).count("1") <= 1
+
+
 def predict_gates(n: int, world: int, dtype: int, gates, prm: B200Params, emulated: bool = False) -> dict:
     """sv_apply_gates: each pass costs its HBM round trip plus its on-chip
     work, ops x pairs x t_op(kind) -- Eq. 4's l s^(n_b - 1) t_op next to the
@@ -230,10 +236,12 @@ def predict_gates(n: int, world: int, dtype: int, gates, prm: B200Params, emulat
             nswap += 1
             continue
         idx = order[st["first"]:st["first"] + st["count"]]
-        nd = sum(1 for j in idx if _is_diag(gates[int(j)]))
-        # host fusion shrinks the op count; spread it over the two kinds
-        scale = st["ops"] / max(st["count"], 1)
-        t_ops = scale * (nd * prm.t_diag + (st["count"] - nd) * prm.t_gate) * (N_l / 2.0)
+        # merged phase runs cost t_lin each; the other ops split over the
+        # diagonal / general shapes of the gates that are not single-control phases
+        rest = [gates[int(j)] for j in idx if not _is_phase1(gates[int(j)])] or [gates[int(j)] for j in idx]
+        fd = sum(1 for g in rest if _is_diag(g)) / len(rest)
+        lin = st.get("lin_ops", 0)
+        t_ops = (lin * prm.t_lin + (st["ops"] - lin) * (fd * prm.t_diag + (1.0 - fd) * prm.t_gate)) * (N_l / 2.0)
         if st["kind"] == 0:
             t_pass += 2.0 * S_l / prm.bw(pass_class(st["tile_mask"], False)) + t_ops + prm.t_launch
             npass += 1

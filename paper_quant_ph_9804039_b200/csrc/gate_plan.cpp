@@ -38,26 +38,56 @@ static void validate_gate(int n, const sv_gate &g, uint64_t j) {
              "gate " + std::to_string(j) + ": a gate cannot control its own target");
 }
 
-// Ops a pass runs after the host fusion of gates.cu (build_tile_ops): a gate
-// with the same target and controls as an earlier op of the pass, with only
-// commuting ops in between, is multiplied into it.
-uint64_t fused_op_count(const sv_gate *gates, const uint64_t *order, uint64_t count) {
-    std::vector<const sv_gate *> ops;
+// Ops a pass runs after the host merging of gates.cu (build_tile_ops):
+//  * a phase gate diag(1, z) with at most one control joins an earlier run
+//    on the same target when only commuting gates lie between; runs of >= 4
+//    become one phase-polynomial op (*lin counts them), shorter runs stay
+//    one op per gate;
+//  * any other gate with the same target and controls as an earlier op, with
+//    only commuting ops in between, is multiplied into it.
+static bool phase1_gate(const sv_gate &g) {
+    return g.m[0] == 1.0 && g.m[1] == 0.0 && gate_diag(g) && __builtin_popcountll(g.controls) <= 1;
+}
+
+uint64_t fused_op_count(const sv_gate *gates, const uint64_t *order, uint64_t count, uint64_t *lin) {
+    struct Op {
+        const sv_gate *g;
+        sv_gate proxy;   // merged phase run: target + union of controls, diagonal
+        uint64_t run;    // > 0: a phase run of this many gates
+    };
+    std::vector<Op> ops;
     for (uint64_t k = 0; k < count; ++k) {
         const sv_gate &g = gates[order[k]];
-        bool fused = false;
+        bool done = false;
         CommuteSet between;
         for (size_t i = ops.size(); i-- > 0;) {
-            if (ops[i]->target == g.target && ops[i]->controls == g.controls && between.commutes(g)) {
-                fused = true;
+            const sv_gate &e = ops[i].run ? ops[i].proxy : *ops[i].g;
+            if (phase1_gate(g) && ops[i].run && e.target == g.target && between.commutes(g)) {
+                ops[i].run += 1;
+                ops[i].proxy.controls |= g.controls;
+                done = true;
                 break;
             }
-            between.add(*ops[i]);
+            if (!phase1_gate(g) && !ops[i].run && e.target == g.target && e.controls == g.controls &&
+                between.commutes(g)) {
+                done = true;
+                break;
+            }
+            between.add(e);
             if (!between.commutes(g)) break;
         }
-        if (!fused) ops.push_back(&g);
+        if (done) continue;
+        Op o{&g, g, phase1_gate(g) ? 1u : 0u};
+        if (o.run) { o.proxy.m[6] = 1.0; o.proxy.m[7] = 0.0; }
+        ops.push_back(o);
     }
-    return ops.size();
+    uint64_t n = 0, nl = 0;
+    for (const Op &o : ops) {
+        if (o.run >= 4) { ++n; ++nl; }
+        else n += o.run ? o.run : 1;
+    }
+    if (lin) *lin = nl;
+    return n;
 }
 
 GatePlan plan_gates(int n, int g, sv_dtype dtype, const sv_gate *gates, uint64_t count) {
@@ -135,7 +165,7 @@ GatePlan plan_gates(int n, int g, sv_dtype dtype, const sv_gate *gates, uint64_t
             swapped ^= 1;
             continue;
         }
-        s.ops = fused_op_count(gates, p.order.data() + s.first, s.count);
+        s.ops = fused_op_count(gates, p.order.data() + s.first, s.count, &s.lin_ops);
         // tile = processed slots + the lowest other slots (carry first) up to T
         s.proc = proc;
         s.tile = proc;

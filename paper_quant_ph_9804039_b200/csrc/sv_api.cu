@@ -1055,6 +1055,7 @@ sv_status sv_plan_gates(int n, int world, sv_dtype dtype, const sv_gate *gates, 
             o.first = s.first;
             o.count = s.count;
             o.ops = s.ops;
+            o.lin_ops = s.lin_ops;
         }
         if (order)
             for (size_t j = 0; j < gp.order.size(); ++j) order[j] = gp.order[j];

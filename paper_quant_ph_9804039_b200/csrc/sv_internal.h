@@ -120,6 +120,7 @@ struct GateStep {
     uint64_t first = 0;  // gates order[first .. first + count)
     uint64_t count = 0;
     uint64_t ops = 0;    // ops after the host fusion of same-target gates (gates.cu)
+    uint64_t lin_ops = 0;  // of which merged phase runs (phase-polynomial ops)
 };
 
 struct GatePlan {
