@@ -58,6 +58,10 @@ struct sv_ctx {
     double *d_deco = nullptr;           // decoherence: {sum, scale, survival[k]}
     unsigned char *d_gprog = nullptr;   // gate circuits: op programs of every pass of a call
     size_t gprog_cap = 0;
+    unsigned char *h_gprog = nullptr;   // pinned staging of the program (truly asynchronous upload)
+    size_t h_gprog_cap = 0;
+    cudaEvent_t gprog_ev = nullptr;     // the last upload from h_gprog has completed
+    bool gprog_pending = false;
     size_t deco_cap = 0;
     double *d_samp = nullptr;           // sampler: chunk prefixes + rank totals + window
     uint64_t *d_shots = nullptr;        // sampler: device output for host-returning calls
@@ -394,14 +398,29 @@ void run_gates(sv_ctx *c, const sv_gate *gates, uint64_t count) {
         lin[i] = hl ? 1 : 0;
     }
     if (prog.size() > c->gprog_cap) {
-        if (c->d_gprog) SV_CUDA(cudaFree(c->d_gprog));
+        if (c->d_gprog) SV_CUDA(cudaFree(c->d_gprog));  // (cudaFree waits for the kernels still using it)
         c->d_gprog = nullptr;
         c->gprog_cap = 0;
         dmalloc((void **)&c->d_gprog, prog.size(), "gate program");
         c->gprog_cap = prog.size();
     }
-    if (!prog.empty())
-        SV_CUDA(cudaMemcpyAsync(c->d_gprog, prog.data(), prog.size(), cudaMemcpyHostToDevice, c->stream));
+    if (!prog.empty()) {
+        // stage in pinned memory so the upload (and the call) stays asynchronous;
+        // the staging buffer is reused once the previous upload has completed
+        if (c->gprog_ev == nullptr) SV_CUDA(cudaEventCreateWithFlags(&c->gprog_ev, cudaEventDisableTiming));
+        if (c->gprog_pending) SV_CUDA(cudaEventSynchronize(c->gprog_ev));
+        if (prog.size() > c->h_gprog_cap) {
+            if (c->h_gprog) SV_CUDA(cudaFreeHost(c->h_gprog));
+            c->h_gprog = nullptr;
+            c->h_gprog_cap = 0;
+            SV_CUDA(cudaMallocHost((void **)&c->h_gprog, prog.size()));
+            c->h_gprog_cap = prog.size();
+        }
+        memcpy(c->h_gprog, prog.data(), prog.size());
+        SV_CUDA(cudaMemcpyAsync(c->d_gprog, c->h_gprog, prog.size(), cudaMemcpyHostToDevice, c->stream));
+        SV_CUDA(cudaEventRecord(c->gprog_ev, c->stream));
+        c->gprog_pending = true;
+    }
     void *cur = c->state, *next = nullptr;
     for (size_t i = 0; i < gp.steps.size(); ++i) {
         const GateStep &st = gp.steps[i];
@@ -653,6 +672,8 @@ void destroy(sv_ctx *c) {
     cudaFree(c->d_samp);
     cudaFree(c->d_deco);
     cudaFree(c->d_gprog);
+    if (c->h_gprog) cudaFreeHost(c->h_gprog);
+    if (c->gprog_ev) cudaEventDestroy(c->gprog_ev);
     cudaFree(c->d_shots);
     if (c->comm) ncclCommDestroy(c->comm);
     cudaFree(c->state);

@@ -189,6 +189,24 @@ def test_emulated_sharding_matches_oracle(dtype, n, world, fused):
                  f"n={n} P={world} fused={fused}")
 
 
+@pytest.mark.parametrize("dtype", DT, ids=DT_IDS)
+def test_many_asynchronous_calls(dtype):
+    """Back-to-back sv_apply_gates calls without synchronisation (pinned,
+    asynchronous program uploads; the device program buffer grows between
+    calls) equal the oracle on the concatenated circuit."""
+    n = 17
+    chunks = [C.random_circuit(n, c, 40 + i, max_controls=2) for i, c in enumerate([3, 50, 7, 200, 1, 90, 30])]
+    chunks.append(C.qft_circuit(n))
+    a = rand_state(n, dtype, 41)
+    ref = orc.apply_gates(a.copy(), np.concatenate(chunks))
+    with sv.sv_init(n, 0, dtype, sv.SV_INIT_ZERO_STATE) as c:
+        sv.sv_set_amplitudes(c, a)
+        for g in chunks:
+            sv.sv_apply_gates(c, g)
+        got = sv.sv_get_amplitudes(c).astype(np.complex128)
+    assert_close(got, ref, dtype, sum(g.size for g in chunks), "async chunks")
+
+
 def test_empty_circuit_and_errors():
     a = rand_state(15, sv.SV_C64, 1)
     assert np.array_equal(run_gpu(a, sv.SV_C64, C.circuit([])), a)
