@@ -396,6 +396,14 @@ def test_errors():
         with pytest.raises(sv.SvError) as e:
             sv.sv_probabilities(c)
         assert e.value.code == sv.SV_ETOOBIG
+    # beyond the 180 GB of one B200: n = 35 complex64 = 256 GiB -> SV_ENOMEM, no leak, device still usable
+    with pytest.raises(sv.SvError) as e:
+        sv.sv_init(35, 0, sv.SV_C64)
+    assert e.value.code == sv.SV_ENOMEM
+    with sv.sv_init(20, 0, sv.SV_C64) as c:
+        sv.sv_set_marked(c, [5])
+        sv.sv_iterate(c, 2)
+        assert sv.sv_measure_marked_mass(c) > 0
 
 
 @pytest.mark.parametrize("diff", [sv.SV_DIFFUSE_WHT, sv.SV_DIFFUSE_MEAN], ids=["wht", "mean"])
