@@ -151,6 +151,48 @@ __global__ void __launch_bounds__(288, 1) k_tma(const __grid_constant__ CUtensor
     }
 }
 
+// (d) persistent, 1 CTA/SM, 256 threads: LDGSTS (cp.async 8 B) of tile i+1
+// into the second shared-memory stage while tile i goes out with STG
+__global__ void __launch_bounds__(256, 1) k_ldgsts(uint64_t *buf, Geo g, unsigned long long ntiles) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *st[2] = {reinterpret_cast<uint64_t *>(smem), reinterpret_cast<uint64_t *>(smem + 65536)};
+    const int tid = threadIdx.x;
+    unsigned long long ot = 0;
+    for (int b = 0; b < 8; ++b)
+        if ((tid >> b) & 1) ot += 1ull << g.tslot[b];
+    unsigned long long oreg[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        unsigned long long o = ot;
+#pragma unroll
+        for (int b = 0; b < 5; ++b)
+            if ((j >> b) & 1) o += 1ull << g.tslot[8 + b];
+        oreg[j] = o;
+    }
+    auto issue = [&](unsigned long long t, uint64_t *dst) {
+        const unsigned long long base = tile_base(t, g);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(su32(dst + tid + 256 * j)),
+                         "l"(buf + base + oreg[j]) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    unsigned long long t = blockIdx.x;
+    if (t < ntiles) issue(t, st[0]);
+    for (int it = 0; t < ntiles; t += gridDim.x, ++it) {
+        const unsigned long long tn = t + gridDim.x;
+        if (tn < ntiles) issue(tn, st[(it + 1) & 1]);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();
+        uint64_t *x = st[it & 1];
+        const unsigned long long base = tile_base(t, g);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) buf[base + oreg[j]] = x[tid + 256 * j] ^ 0x8000000000000000ull;
+        __syncthreads();
+    }
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                              const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -167,6 +209,7 @@ int main() {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     CK(cudaFuncSetAttribute(k_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072));
     CK(cudaFuncSetAttribute(k_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072));
+    CK(cudaFuncSetAttribute(k_ldgsts, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072));
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
@@ -208,11 +251,12 @@ int main() {
         }
         const unsigned long long ntiles = N >> TB;
         const double bytes = 2.0 * N * 8;
-        for (int mode = 0; mode < 3; ++mode) {
+        for (int mode = 0; mode < 4; ++mode) {
             auto launch = [&]() {
                 if (mode == 0) k_ldg<<<(unsigned)ntiles, 256>>>(buf, g);
                 else if (mode == 1) k_tma<false><<<sms, 288, 131072>>>(tm, buf, g, ntiles, rank, cf0, cf1, f0bits);
-                else k_tma<true><<<sms, 288, 131072>>>(tm, buf, g, ntiles, rank, cf0, cf1, f0bits);
+                else if (mode == 2) k_tma<true><<<sms, 288, 131072>>>(tm, buf, g, ntiles, rank, cf0, cf1, f0bits);
+                else k_ldgsts<<<sms, 256, 131072>>>(buf, g, ntiles);
             };
             launch();
             CK(cudaDeviceSynchronize());
@@ -223,7 +267,7 @@ int main() {
             float ms;
             cudaEventElapsedTime(&ms, a, b);
             printf("%s  %-28s %8.1f GB/s  (%.3f ms/pass)\n", pat == 0 ? "strided 64B x 64KiB" : "contiguous 64KiB   ",
-                   mode == 0 ? "LDG/STG 2 CTA/SM" : (mode == 1 ? "TMA load + STG, pipelined" : "TMA load + TMA store"),
+                   mode == 0 ? "LDG/STG 2 CTA/SM" : (mode == 1 ? "TMA load + STG, pipelined" : (mode == 2 ? "TMA load + TMA store" : "LDGSTS 2-stage + STG, 1 CTA/SM")),
                    bytes * 5 / (ms / 1e3) / 1e9, ms / 5);
         }
     }
