@@ -52,6 +52,8 @@ enum GateKind : unsigned int {
     GK_ANTI = 3,      // w = z = 0: (x v, y u)
     GK_SWAP = 4,      // w = z = 0, x = y = 1 (NOT): (v, u)
     GK_LINPHASE = 5,  // merged run of phase gates on one target, <= 1 control each (below)
+    GK_DIAGT = 6,     // diagonal gate whose target is a THREAD bit of the current layout:
+                      // every amplitude of the thread gets w (bit 0) or z (bit 1); ri = target tile bit
 };
 
 // GK_LINPHASE: the product of phase gates diag(1, z_g) on one target t, each
@@ -277,6 +279,18 @@ __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB <= 7) ? 4 : 2)
                 continue;
             }
         }
+        if (kind == GK_DIAGT) {  // diagonal, target on a thread bit: no relayout needed
+            if ((et & tm) == tm && (base & fm) == fm) {
+                const bool one = (et >> ri) & 1u;
+                const R fr = one ? m[6] : m[0], fi = one ? m[7] : m[1];
+                if (!(fr == (R)1 && fi == (R)0)) {
+#pragma unroll
+                    for (int j = 0; j < L::NR; ++j)
+                        if (((unsigned int)j & jm) == jm) cmul_by(x[j], fr, fi);
+                }
+            }
+            continue;
+        }
         if ((et & tm) == tm && (base & fm) == fm) gate_dispatch<L>(x, m, ri, jm, kind);
     }
     E *gout = reinterpret_cast<E *>(p.out) + base;
@@ -466,8 +480,9 @@ void build_tile_ops(const GatePassArgs &a, std::vector<GOp<R>> &out) {
         CommuteSet skipped;
         int cnt = 0;
         for (size_t i = 0; i < pend.size(); ++i) {
-            // a merged phase run needs no register target: it runs in any layout
-            if (skipped.commutes(pend[i].g) && (!pend[i].lin.empty() || L::is_reg(ph, pend[i].bt))) {
+            // a merged phase run or a diagonal gate needs no register target: it runs in any layout
+            if (skipped.commutes(pend[i].g) &&
+                (!pend[i].lin.empty() || gate_diag(pend[i].g) || L::is_reg(ph, pend[i].bt))) {
                 ++cnt;
                 if (take) take->push_back(i);
             } else {
@@ -547,8 +562,14 @@ void build_tile_ops(const GatePassArgs &a, std::vector<GOp<R>> &out) {
             GOp<R> o = op_coefs<R>(pd.g);
             o.ph |= (unsigned int)cur;
             o.ri = 0;
+            bool treg = false;
             for (int r = 0; r < L::kRB; ++r)
-                if (L::reg_bit(cur, r) == pd.bt) o.ri = (unsigned int)r;
+                if (L::reg_bit(cur, r) == pd.bt) { o.ri = (unsigned int)r; treg = true; }
+            if (!treg) {  // only diagonal gates are scheduled off a register target
+                SV_CHECK(gate_diag(pd.g), SV_EINVAL, "internal: non-diagonal gate without a register target");
+                o.ph = (GK_DIAGT << 8) | (unsigned int)cur;
+                o.ri = (unsigned int)pd.bt;
+            }
             o.jm = 0;
             o.tm = 0;
             for (int tbit = 0; tbit < L::kTB; ++tbit) {

@@ -34,7 +34,8 @@ def main():
     n = args.n
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     work = {
-        "h_layers_x4": C.circuit([C.record(q, C.H) for q in range(n)] * 4),
+        "u_layer": C.circuit([C.record(q, C.random_unitary(np.random.default_rng(q))) for q in range(n)]),
+        "h_layers_x4": C.circuit([C.record(q, C.H) for q in range(n)] * 4),  # H^4 fuses to an exact diagonal
         "qft": C.qft_circuit(n),
         "layered_x4": C.layered_circuit(n, 4, 1),
         "random_300": C.random_circuit(n, 300, 2, max_controls=2),
