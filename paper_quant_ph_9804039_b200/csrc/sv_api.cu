@@ -58,6 +58,17 @@ struct sv_ctx {
     double *d_deco = nullptr;           // decoherence: {sum, scale, survival[k]}
     unsigned char *d_gprog = nullptr;   // gate circuits: op programs of every pass of a call
     size_t gprog_cap = 0;
+    // CUDA graphs of launch-bound WHT schedules (small states, one GPU):
+    // (k, fused exchange, marked epoch) -> executable graph
+    struct GraphEntry {
+        int k;
+        bool fused;
+        uint64_t epoch;
+        cudaGraphExec_t exec;
+    };
+    std::vector<GraphEntry> graphs;
+    uint64_t marked_epoch = 0;
+    bool use_graphs = true;             // SV_GRAPHS=0 disables
     unsigned char *h_gprog = nullptr;   // pinned staging of the program (truly asynchronous upload)
     size_t h_gprog_cap = 0;
     cudaEvent_t gprog_ev = nullptr;     // the last upload from h_gprog has completed
@@ -468,6 +479,45 @@ void run_gates(sv_ctx *c, const sv_gate *gates, uint64_t count) {
         SV_CUDA(cudaMemcpyAsync(c->state, cur, c->nres * elem_bytes(c->dt), cudaMemcpyDeviceToDevice, c->stream));
 }
 
+// Launch-bound regime (states of a few MiB: a tile pass is a few us, about
+// its launch latency): replay the k-iteration schedule as one CUDA graph,
+// captured on first use and cached per (k, exchange mode, marked set).  Not
+// while profiling (events per launch), not with NCCL (multi-process), not for
+// the one-CTA path (a single launch already).
+void run_wht_graphed(sv_ctx *c, int k) {
+    constexpr uint64_t kGraphMaxBytes = 64ull << 20;
+    const bool small = c->nres * elem_bytes(c->dt) <= kGraphMaxBytes;
+    if (!c->use_graphs || c->prof || c->comm != nullptr || c->plan.whole || !small || k < 2) {
+        run_wht_schedule(c, k, true);
+        return;
+    }
+    for (const auto &ge : c->graphs)
+        if (ge.k == k && ge.fused == c->fused_xchg && ge.epoch == c->marked_epoch) {
+            SV_CUDA(cudaGraphLaunch(ge.exec, c->stream));
+            return;
+        }
+    cudaGraph_t graph = nullptr;
+    SV_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+        run_wht_schedule(c, k, true);
+    } catch (...) {
+        cudaStreamEndCapture(c->stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+    }
+    SV_CUDA(cudaStreamEndCapture(c->stream, &graph));
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    SV_CUDA(e);
+    if (c->graphs.size() >= 8) {
+        cudaGraphExecDestroy(c->graphs.front().exec);
+        c->graphs.erase(c->graphs.begin());
+    }
+    c->graphs.push_back({k, c->fused_xchg, c->marked_epoch, exec});
+    SV_CUDA(cudaGraphLaunch(exec, c->stream));
+}
+
 MeanArgs mean_args(sv_ctx *c, bool with_oracle) {
     MeanArgs m;
     m.a = c->state;
@@ -515,6 +565,7 @@ void run_mean(sv_ctx *c, int k, bool with_oracle) {
 }
 
 void store_marked(sv_ctx *c, const uint64_t *marked, uint64_t m) {
+    c->marked_epoch += 1;  // captured WHT graphs bake the marked-set pointers and counts
     const uint64_t N = 1ull << c->n;
     SV_CHECK(m <= N, SV_EINVAL, "marked set larger than 2^n");
     SV_CHECK(m == 0 || marked != nullptr, SV_EINVAL, "marked is NULL");
@@ -671,6 +722,7 @@ void destroy(sv_ctx *c) {
     cudaFree(c->d_coefs);
     cudaFree(c->d_samp);
     cudaFree(c->d_deco);
+    for (auto &ge : c->graphs) cudaGraphExecDestroy(ge.exec);
     cudaFree(c->d_gprog);
     if (c->h_gprog) cudaFreeHost(c->h_gprog);
     if (c->gprog_ev) cudaEventDestroy(c->gprog_ev);
@@ -735,6 +787,7 @@ sv_status sv_init(sv_ctx **out, int n, uint64_t seed, sv_dtype dtype, sv_init_ki
         dmalloc((void **)&c->d_gbar, 2 * sizeof(unsigned int), "grid barrier");
         SV_CUDA(cudaMemsetAsync(c->d_gbar, 0, 2 * sizeof(unsigned int), c->stream));
         if (const char *e = getenv("SV_MEAN_RESIDENT")) c->mean_resident = strcmp(e, "0") != 0;
+        if (const char *e = getenv("SV_GRAPHS")) c->use_graphs = strcmp(e, "0") != 0;
         SV_CUDA(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned int), c->stream));
         SV_CUDA(cudaMemsetAsync(c->d_sums, 0, 8 * sizeof(double), c->stream));
         c->mgrid = std::min(mean_grid(c->nres, dtype), kMaxGrid);
@@ -851,7 +904,7 @@ sv_status sv_iterate(sv_ctx *c, int k, sv_diffusion d) {
         SV_CHECK(k >= 0, SV_EINVAL, "k must be >= 0");
         SV_CHECK(c->has_marked, SV_ESTATE, "sv_iterate before any marked set (sv_set_marked / sv_apply_oracle)");
         SV_CUDA(cudaSetDevice(c->device));
-        if (d == SV_DIFFUSE_WHT) run_wht_schedule(c, k, true);
+        if (d == SV_DIFFUSE_WHT) run_wht_graphed(c, k);
         else if (d == SV_DIFFUSE_MEAN) run_mean(c, k, true);
         else throw Error{SV_EINVAL, "unknown diffusion"};
     });

@@ -467,3 +467,29 @@ def test_mean_resident_and_launched_paths(dtype, n, m, k, monkeypatch):
         fits = chunk <= 232448 - 1024  # opt-in shared memory per block minus the kernel's reserve
         assert launches == (1 if (env == "1" and fits) else k), (env, launches)
         assert_close(got, ref, dtype, f"mean resident={env} n={n}", n=n, k=k)
+
+
+@pytest.mark.parametrize("dtype", DT, ids=DT_IDS)
+def test_graph_replay_matches_launched(dtype, monkeypatch):
+    """Small states replay sv_iterate's WHT schedule as a cached CUDA graph:
+    bitwise equal to the launched schedule (SV_GRAPHS=0), and a new marked set
+    (or a new k) is captured afresh instead of replaying a stale graph."""
+    n = 18
+    a0 = rand_state(n, dtype)
+    sets = [orc.marked_from_seed(n, 3, 1), orc.marked_from_seed(n, 40, 2)]
+    res = {}
+    for env in ("1", "0"):
+        monkeypatch.setenv("SV_GRAPHS", env)
+        with ctx_with(a0, dtype) as c:
+            out = []
+            for mk, k in ((sets[0], 5), (sets[0], 5), (sets[1], 5), (sets[1], 3)):
+                sv.sv_set_marked(c, mk)
+                sv.sv_iterate(c, k, sv.SV_DIFFUSE_WHT)
+                out.append(sv.sv_get_amplitudes(c))
+            res[env] = out
+    for g, l in zip(res["1"], res["0"]):
+        np.testing.assert_array_equal(g, l)
+    ref = a0.copy()
+    for mk, k in ((sets[0], 5), (sets[0], 5), (sets[1], 5), (sets[1], 3)):
+        ref = orc.iterate(ref, mk, k, orc.WHT)
+    assert_close(res["1"][-1], ref, dtype, "graph replay", n=n, k=18)
