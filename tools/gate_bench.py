@@ -59,8 +59,14 @@ def main():
             t = sum(best) / 1e3
             passes = [{"gates": int(s["count"]), "proc_bits": bin(s["proc_mask"]).count("1"), "ms": ms,
                        "gbs": 2 * S / (ms / 1e3) / 1e9} for s, ms in zip([s for s in steps if s["kind"] == 0], best)]
+            # ALU side of the roofline: a general complex 2x2 on one pair = 16 FMA = 32 FLOP
+            # (diagonal / merged ops counted the same: an upper bound on the useful work)
+            ops = sum(int(s["ops"]) for s in steps if s["kind"] == 0)
+            flop = ops * (1 << (n - 1)) * 32.0
+            fp32_peak = 148 * 128 * 2 * 1.965e9  # non-tensor FP32 FMA peak, B200 (148 SMs x 128 lanes)
             res["workloads"][name] = {
-                "gates": int(gates.size), "passes": len(best), "ms": 1e3 * t,
+                "gates": int(gates.size), "ops_after_host_merging": ops, "passes": len(best), "ms": 1e3 * t,
+                "fp32_tflops_upper": flop / t / 1e12, "fp32_frac_upper": flop / t / fp32_peak,
                 "gate_amp_updates_per_s": (1 << n) * gates.size / t,
                 "avg_pass_gbs": 2 * S * len(best) / t / 1e9,
                 "avg_pass_frac": 2 * S * len(best) / t / 1e9 / peak,
