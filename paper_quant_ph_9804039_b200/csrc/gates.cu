@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB <= 7) ? 4 : 2)
     __shared__ E *s_dst[XCHG ? 8 : 1];
     if constexpr (XCHG) load_xdst(p, threadIdx.x, s_dst);
     const int tid = threadIdx.x;
-    const unsigned long long base = tile_base(blockIdx.x, p.free_mask);
+    const unsigned long long base = tile_base(blockIdx.x, p);
     E x[L::NR];
     global_load<L, 0>(x, reinterpret_cast<const E *>(p.in) + base, p, tid);
     const unsigned int eth[3] = {L::ethr(0, tid), L::ethr(1, tid), L::ethr(2, tid)};
@@ -626,6 +626,7 @@ void launch_tile_gates(const GatePassArgs &a, const void *dev_ops, uint64_t nops
         }
     }
     SV_CHECK(b == TB, SV_EINVAL, "internal: gate tile mask does not have T slots");
+    kp_set_free_runs(kp);
     SV_CHECK(nops <= 0x7fffffffull, SV_EINVAL, "too many gates in one pass");
     const unsigned long long ntiles = 1ull << f;
     SV_CHECK(ntiles <= 0x7fffffffull, SV_EINVAL, "too many tiles for one launch");

@@ -52,6 +52,7 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
     }
     SV_CHECK(b == TB, SV_EINVAL, "internal: tile mask does not have T slots");
     SV_CHECK(kp.slot[0] == 0, SV_EINVAL, "internal: tile must contain slot 0");
+    kp_set_free_runs(kp);
     if (a.mid == MID_ORACLE)
         SV_CHECK(a.tilemap != nullptr && (a.n_marked == 0 || a.marked != nullptr), SV_EINVAL,
                  "internal: oracle pass without its tile lookup");

@@ -161,6 +161,11 @@ struct KParams {
     int has_origin;
     unsigned int proc;       // processed tile bits
     unsigned long long free_mask;  // slots not in the tile; tile id bits scatter into them
+    // the free slots as runs of consecutive slots (host-built, kp_set_free_runs):
+    // tile id bits [off, off + len) land at slots [start, start + len); nruns = 0:
+    // more than kMaxRuns runs -> bit-by-bit scatter
+    int nruns;
+    unsigned char run_start[8], run_len[8];
     signed char slot[16];          // tile bit -> slot
     // fused qubit-swap exchange (global_store_xchg): 0 = plain store
     int xchg, xnl, xg, xrank;      // local index bits, rank bits, own rank (-1: emulated)
@@ -522,8 +527,11 @@ __device__ __forceinline__ void apply_scale(E (&x)[NR], double s) {
     for (int j = 0; j < NR; ++j) scale(x[j], (R)s);
 }
 
-// Tile base: scatter the tile id into the free slots (software pdep).
-__device__ __forceinline__ unsigned long long tile_base(unsigned long long tile, unsigned long long fm) {
+// Tile base: scatter the tile id into the free slots (software pdep).  The
+// free slots of a pass are a few runs of consecutive slots, so the scatter is
+// one shift-mask-shift per run (the former bit-by-bit loop was a ~100-
+// instruction dependent chain in front of every CTA's first load).
+__device__ __forceinline__ unsigned long long tile_base_bits(unsigned long long tile, unsigned long long fm) {
     unsigned long long base = 0;
     while (fm) {
         const unsigned long long low = fm & (~fm + 1ull);
@@ -532,6 +540,38 @@ __device__ __forceinline__ unsigned long long tile_base(unsigned long long tile,
         fm ^= low;
     }
     return base;
+}
+__device__ __forceinline__ unsigned long long tile_base(unsigned long long tile, const KParams &p) {
+    if (p.nruns == 0) return tile_base_bits(tile, p.free_mask);
+    unsigned long long base = 0;
+    int off = 0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        if (r < p.nruns) {
+            const int len = p.run_len[r];
+            base |= ((tile >> off) & ((1ull << len) - 1ull)) << p.run_start[r];
+            off += len;
+        }
+    }
+    return base;
+}
+
+// Host: the runs of a free-slot mask (<= 8, else nruns = 0).
+inline void kp_set_free_runs(KParams &kp) {
+    kp.nruns = 0;
+    unsigned long long fm = kp.free_mask;
+    int n = 0;
+    for (int sl = 0; sl < 64;) {
+        if (!((fm >> sl) & 1ull)) { ++sl; continue; }
+        int len = 0;
+        while (sl + len < 64 && ((fm >> (sl + len)) & 1ull)) ++len;
+        if (n == 8) { kp.nruns = 0; return; }
+        kp.run_start[n] = (unsigned char)sl;
+        kp.run_len[n] = (unsigned char)len;
+        ++n;
+        sl += len;
+    }
+    kp.nruns = n;
 }
 
 // Oracle tiles: one bitmap word says whether this tile holds a marked index
@@ -650,7 +690,7 @@ __global__ void __launch_bounds__(1 << (TB - RB), SV_TILE_MIN_BLOCKS) wht_tile2_
     __shared__ float2 *s_dst[XCHG ? 8 : 1];
     if constexpr (XCHG) load_xdst(p, threadIdx.x, s_dst);
     const int tid = threadIdx.x;
-    const unsigned long long base = tile_base(blockIdx.x, p.free_mask);
+    const unsigned long long base = tile_base(blockIdx.x, p);
     float2 x[L::NR];
     global_load<L, 0>(x, reinterpret_cast<const float2 *>(p.in) + base, p, tid);
     if constexpr (NOISY) {  // renormalisation (decoherence) rides only on the general-2x2 flavour
@@ -673,7 +713,7 @@ __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB >= 9) ? 1 : SV_TILE_M
     const int tid = threadIdx.x;
     // U == 0: the contiguous group, tile t = slots [0, T) at t * 2^T
     const unsigned long long base =
-        (U == 0) ? ((unsigned long long)blockIdx.x << TB) : tile_base(blockIdx.x, p.free_mask);
+        (U == 0) ? ((unsigned long long)blockIdx.x << TB) : tile_base(blockIdx.x, p);
     E x[L::NR];
     global_load<L, 0, (U == 0)>(x, reinterpret_cast<const E *>(p.in) + base, p, tid);
     if constexpr (NOISY) {  // renormalisation (decoherence) rides only on the general-2x2 flavour
