@@ -135,7 +135,8 @@ def main():
     n = 30
     work = {"QFT": C.qft_circuit(n), "layered_x4": C.layered_circuit(n, 4, 1),
             "random_300": C.random_circuit(n, 300, 2, max_controls=2),
-            "h_layers_x4": C.circuit([C.record(q, C.H) for q in range(n)] * 4)}
+            # one random unitary per qubit (H layers would be degenerate: H^4 fuses to a diagonal)
+            "u_layer": C.circuit([C.record(q, C.random_unitary(np.random.default_rng(q))) for q in range(n)])}
     for name, g in work.items():
         row(f"gates {name} n={n} (c64)", 1, observe_gates(n, g), CM.predict_gates(n, 1, 0, g, prm)["t"])
     for P in (2, 4):
