@@ -8,13 +8,13 @@
 
 namespace sv {
 
-template void launch_tile_dispatch<false>(sv_dtype, const KParamsT<false> &, int, int, int, unsigned long long,
+template void launch_tile_dispatch<0>(sv_dtype, const KParamsT<0> &, int, int, int, unsigned long long,
                                           cudaStream_t);
 
 void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
     const int TB = tile_bits(dt);
     KParams kp{};
-    KParamsT<true> kc{};  // coefficients of the general-2x2 flavour
+    KParamsT<1> kc{};  // coefficients of the general-2x2 flavour
     kp.in = a.in;
     kp.out = a.out;
     kp.marked = reinterpret_cast<const unsigned long long *>(a.marked);
@@ -67,12 +67,34 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
              SV_EINVAL, "internal: a fully processed tile must be the contiguous one");
     const unsigned long long ntiles = 1ull << f;
     if (a.noisy) {
-        static_cast<KParams &>(kc) = kp;
-        launch_tile_dispatch<true>(dt, kc, a.pre, a.post, u, ntiles, s);
+        // pure angle errors ([c s; s -c] on every processed bit, no decoherence
+        // contraction) take the tan form: [[1, t], [t, -1]] and one factor c per bit
+        bool tan_form = true;
+        double pass_scale = 1.0;
+        for (int bb = 0; bb < TB && tan_form; ++bb) {
+            if (!((proc >> bb) & 1u)) continue;
+            for (int h = 0; h < 2; ++h) {
+                if ((h == 0 && !a.pre) || (h == 1 && !a.post)) continue;
+                const double *m = kc.coef[h][bb];
+                if (!(m[1] == m[2] && m[3] == -m[0] && fabs(m[0]) > 0.25)) { tan_form = false; break; }
+                pass_scale *= m[0];
+            }
+        }
+        if (tan_form) {
+            KParamsT<2> ka{};
+            static_cast<KParams &>(ka) = kp;
+            for (int h = 0; h < 2; ++h)
+                for (int bb = 0; bb < 16; ++bb) ka.coef[h][bb][0] = kc.coef[h][bb][0] != 0.0 ? kc.coef[h][bb][1] / kc.coef[h][bb][0] : 0.0;
+            ka.pass_scale = pass_scale;
+            launch_tile_dispatch<2>(dt, ka, a.pre, a.post, u, ntiles, s);
+        } else {
+            static_cast<KParams &>(kc) = kp;
+            launch_tile_dispatch<1>(dt, kc, a.pre, a.post, u, ntiles, s);
+        }
     } else {
-        KParamsT<false> ki{};
+        KParamsT<0> ki{};
         static_cast<KParams &>(ki) = kp;
-        launch_tile_dispatch<false>(dt, ki, a.pre, a.post, u, ntiles, s);
+        launch_tile_dispatch<0>(dt, ki, a.pre, a.post, u, ntiles, s);
     }
 }
 

@@ -178,12 +178,18 @@ struct KParams {
 // [w x; y z] row-major.  The ideal flavour's parameter block stays small
 // (measured on B200: the 1 KiB coefficient block in every launch's
 // parameters cost the contiguous c4 pass ~10%).
-template <bool NOISY>
+// NOISY: 0 = ideal butterflies; 1 = general real 2x2 per stage (angle
+// errors with decoherence contractions, G19/G22); 2 = angle errors only:
+// U(phi) = c [[1, t], [t, -1]] with t = tan(phi), the per-stage factors c
+// multiplied once into the loaded tile (pass_scale) -- 2 packed FMAs per
+// butterfly instead of 4.
+template <int NOISY>
 struct KParamsT : KParams {
     double coef[2][16][4];
+    double pass_scale;
 };
 template <>
-struct KParamsT<false> : KParams {};
+struct KParamsT<0> : KParams {};
 
 // Publish the exchange destinations in shared memory (constant indices only:
 // a runtime-indexed kernel-parameter array would be copied to local memory).
@@ -252,6 +258,33 @@ __device__ __forceinline__ void bfly_gen<float2>(float2 &x, float2 &y, const dou
     y = *reinterpret_cast<float2 *>(&u);
 }
 
+// Angle-error butterfly without its factor c: (u, v) -> (u + t v, t u - v).
+template <typename E>
+__device__ __forceinline__ void bfly_tan(E &x, E &y, double td) {
+    using R = decltype(E{}.x);
+    const R t = (R)td;
+    const E a = x;
+    x.x = a.x + t * y.x;
+    x.y = a.y + t * y.y;
+    y.x = t * a.x - y.x;
+    y.y = t * a.y - y.y;
+}
+
+template <>
+__device__ __forceinline__ void bfly_tan<float2>(float2 &x, float2 &y, double td) {
+    const float t = (float)td;
+    const float2 T = make_float2(t, t);
+    const unsigned long long a = *reinterpret_cast<unsigned long long *>(&x);
+    const unsigned long long b = *reinterpret_cast<unsigned long long *>(&y);
+    const unsigned long long t2 = *reinterpret_cast<const unsigned long long *>(&T);
+    unsigned long long u, v;
+    asm("fma.rn.f32x2 %0, %3, %4, %2;\n\t"          // u = t b + a
+        "fma.rn.f32x2 %1, %3, %2, %5;"               // v = t a - b
+        : "=&l"(u), "=&l"(v) : "l"(a), "l"(t2), "l"(b), "l"(b ^ 0x8000000080000000ull));
+    x = *reinterpret_cast<float2 *>(&u);
+    y = *reinterpret_cast<float2 *>(&v);
+}
+
 template <typename E, typename R>
 __device__ __forceinline__ void scale(E &x, R s) {
     x.x *= s;
@@ -270,7 +303,7 @@ __device__ __forceinline__ void scale<float2, float>(float2 &x, float s) {
 // Stages of layout PH.  The processed tile bits are always [U, TB): the
 // unprocessed slots of a tile are its lowest ones (plan.cpp make_group), so
 // U is a template parameter and the unrolled stage code has no branches.
-template <class L, int PH, int U, bool NOISY, int HALF, typename E>
+template <class L, int PH, int U, int NOISY, int HALF, typename E>
 __device__ __forceinline__ void run_stages(E (&x)[L::NR], const KParamsT<NOISY> &p) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -280,7 +313,9 @@ __device__ __forceinline__ void run_stages(E (&x)[L::NR], const KParamsT<NOISY> 
 #pragma unroll
                 for (int j = 0; j < L::NR; ++j)
                     if (!(j & (1 << i))) {
-                        if constexpr (NOISY)
+                        if constexpr (NOISY == 2)
+                            bfly_tan(x[j], x[j | (1 << i)], p.coef[HALF][b][0]);
+                        else if constexpr (NOISY == 1)
                             bfly_gen(x[j], x[j | (1 << i)], p.coef[HALF][b]);
                         else
                             bfly(x[j], x[j | (1 << i)]);
@@ -602,7 +637,7 @@ __device__ __forceinline__ bool oracle_lookup(const KParams &p, unsigned long lo
 
 // Everything after the tile is in registers (layout A): stage sets, the
 // elementwise op, relayouts through `sm`, and the coalesced global store.
-template <class L, bool PRE, bool POST, int U, bool NOISY, bool XCHG, typename E>
+template <class L, bool PRE, bool POST, int U, int NOISY, bool XCHG, typename E>
 __device__ __forceinline__ void tile_body(E (&x)[L::NR], E *sm, const KParamsT<NOISY> &p, unsigned long long base, E *gout,
                                           int tid, E *const *sdst, bool has_marked, const unsigned long long *s_mlo,
                                           const unsigned long long *s_mcnt) {
@@ -641,7 +676,7 @@ __device__ __forceinline__ void tile_body(E (&x)[L::NR], E *sm, const KParamsT<N
 
 // tile_body for the two-layout strided family (Layout2): A -> B stages,
 // the op in B, B -> A stages; without processed bits in B it stays in A.
-template <class L, bool PRE, bool POST, int U, bool NOISY, bool XCHG, typename E>
+template <class L, bool PRE, bool POST, int U, int NOISY, bool XCHG, typename E>
 __device__ __forceinline__ void tile_body2(E (&x)[L::NR], E *sm, const KParamsT<NOISY> &p, unsigned long long base, E *gout,
                                            int tid, E *const *sdst, bool has_marked, const unsigned long long *s_mlo,
                                            const unsigned long long *s_mcnt) {
@@ -681,7 +716,7 @@ __device__ __forceinline__ void tile_body2(E (&x)[L::NR], E *sm, const KParamsT<
 }
 
 // Strided complex64 tiles (U >= 3) with the two-layout family.
-template <int TB, int RB, bool PRE, bool POST, int U, bool NOISY, bool XCHG>
+template <int TB, int RB, bool PRE, bool POST, int U, int NOISY, bool XCHG>
 __global__ void __launch_bounds__(1 << (TB - RB), SV_TILE_MIN_BLOCKS) wht_tile2_kernel(const KParamsT<NOISY> p) {
     using L = Layout2<TB, RB>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -693,16 +728,17 @@ __global__ void __launch_bounds__(1 << (TB - RB), SV_TILE_MIN_BLOCKS) wht_tile2_
     const unsigned long long base = tile_base(blockIdx.x, p);
     float2 x[L::NR];
     global_load<L, 0>(x, reinterpret_cast<const float2 *>(p.in) + base, p, tid);
-    if constexpr (NOISY) {  // renormalisation (decoherence) rides only on the general-2x2 flavour
+    if constexpr (NOISY) {  // renormalisation (decoherence) rides only on the general-2x2 flavours
         if (p.scale_in) apply_scale(x, *p.scale_in);
     }
+    if constexpr (NOISY == 2) apply_scale(x, p.pass_scale);  // the product of the pass's factors c
     const bool has_marked = (p.mid == MID_ORACLE) && oracle_lookup(p, blockIdx.x, tid, &s_mlo, &s_mcnt);
     tile_body2<L, PRE, POST, U, NOISY, XCHG>(x, sm, p, base, reinterpret_cast<float2 *>(p.out) + base, tid, s_dst, has_marked, &s_mlo,
                                 &s_mcnt);
 }
 
 // One CTA per tile: 128-bit loads straight into registers (layout A).
-template <typename E, int TB, int RB, bool PRE, bool POST, int U, bool NOISY, bool XCHG>
+template <typename E, int TB, int RB, bool PRE, bool POST, int U, int NOISY, bool XCHG>
 __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB >= 9) ? 1 : SV_TILE_MIN_BLOCKS) wht_tile_kernel(const KParamsT<NOISY> p) {
     using L = Layout<E, TB, RB>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -716,14 +752,15 @@ __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB >= 9) ? 1 : SV_TILE_M
         (U == 0) ? ((unsigned long long)blockIdx.x << TB) : tile_base(blockIdx.x, p);
     E x[L::NR];
     global_load<L, 0, (U == 0)>(x, reinterpret_cast<const E *>(p.in) + base, p, tid);
-    if constexpr (NOISY) {  // renormalisation (decoherence) rides only on the general-2x2 flavour
+    if constexpr (NOISY) {  // renormalisation (decoherence) rides only on the general-2x2 flavours
         if (p.scale_in) apply_scale(x, *p.scale_in);
     }
+    if constexpr (NOISY == 2) apply_scale(x, p.pass_scale);  // the product of the pass's factors c
     const bool has_marked = (p.mid == MID_ORACLE) && oracle_lookup(p, blockIdx.x, tid, &s_mlo, &s_mcnt);
     tile_body<L, PRE, POST, U, NOISY, XCHG>(x, sm, p, base, reinterpret_cast<E *>(p.out) + base, tid, s_dst, has_marked, &s_mlo, &s_mcnt);
 }
 
-template <typename E, int TB, int RB, bool PRE, bool POST, int U, bool NOISY, bool XCHG>
+template <typename E, int TB, int RB, bool PRE, bool POST, int U, int NOISY, bool XCHG>
 static void launch_tile_x(const KParamsT<NOISY> &kp, unsigned long long ntiles, cudaStream_t s) {
     using L = Layout<E, TB, RB>;
     auto fn = wht_tile_kernel<E, TB, RB, PRE, POST, U, NOISY, XCHG>;
@@ -743,13 +780,13 @@ static void launch_tile_x(const KParamsT<NOISY> &kp, unsigned long long ntiles, 
     SV_CUDA(cudaGetLastError());
 }
 
-template <typename E, int TB, int RB, bool PRE, bool POST, int U, bool NOISY>
+template <typename E, int TB, int RB, bool PRE, bool POST, int U, int NOISY>
 static void launch_tile_t(const KParamsT<NOISY> &kp, unsigned long long ntiles, cudaStream_t s) {
     if (kp.xchg) launch_tile_x<E, TB, RB, PRE, POST, U, NOISY, true>(kp, ntiles, s);
     else launch_tile_x<E, TB, RB, PRE, POST, U, NOISY, false>(kp, ntiles, s);
 }
 
-template <typename E, int TB, int RB, int U, bool NOISY>
+template <typename E, int TB, int RB, int U, int NOISY>
 static void launch_tile_u(const KParamsT<NOISY> &kp, int pre, int post, int u, unsigned long long ntiles, cudaStream_t s) {
     if constexpr (U < TB) {
         if (u != U) return launch_tile_u<E, TB, RB, U + 1, NOISY>(kp, pre, post, u, ntiles, s);
@@ -766,14 +803,16 @@ static void launch_tile_u(const KParamsT<NOISY> &kp, int pre, int post, int u, u
 
 namespace sv {
 // Both dtypes, one stage flavour (instantiated in wht.cu / wht_noisy.cu).
-template <bool NOISY>
+template <int NOISY>
 void launch_tile_dispatch(sv_dtype dt, const KParamsT<NOISY> &kp, int pre, int post, int u, unsigned long long ntiles,
                           cudaStream_t s) {
     if (dt == SV_C64) launch_tile_u<float2, kTileBitsC64, kRegBitsC64, 0, NOISY>(kp, pre, post, u, ntiles, s);
     else launch_tile_u<double2, kTileBitsC128, kRegBitsC128, 0, NOISY>(kp, pre, post, u, ntiles, s);
 }
-extern template void launch_tile_dispatch<false>(sv_dtype, const KParamsT<false> &, int, int, int, unsigned long long,
+extern template void launch_tile_dispatch<0>(sv_dtype, const KParamsT<0> &, int, int, int, unsigned long long,
                                                  cudaStream_t);
-extern template void launch_tile_dispatch<true>(sv_dtype, const KParamsT<true> &, int, int, int, unsigned long long,
+extern template void launch_tile_dispatch<1>(sv_dtype, const KParamsT<1> &, int, int, int, unsigned long long,
                                                 cudaStream_t);
+extern template void launch_tile_dispatch<2>(sv_dtype, const KParamsT<2> &, int, int, int, unsigned long long,
+                                              cudaStream_t);
 }  // namespace sv

@@ -7,6 +7,6 @@
 
 namespace sv {
 
-template void launch_tile_dispatch<true>(sv_dtype, const KParamsT<true> &, int, int, int, unsigned long long, cudaStream_t);
+template void launch_tile_dispatch<1>(sv_dtype, const KParamsT<1> &, int, int, int, unsigned long long, cudaStream_t);
 
 }  // namespace sv
