@@ -319,6 +319,21 @@ def run_ours(args):
     e2e = {"value": N_amp * k * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(M * 8),
            "d2h_bytes_per_step": 8, "p_success": p_success}
 
+    # the B200 refit of the paper's analytical model (costmodel.py) for this
+    # step, next to the measurement: its prediction error is the Table 5/6 analog
+    model = None
+    try:
+        from paper_quant_ph_9804039_b200 import costmodel as cm
+        prm = cm.B200Params()
+        if diff == "mean":
+            pred = cm.predict_mean(n, world, dtype, k, prm)["t"]
+        else:
+            pred = cm.predict_wht(n, world, dtype, k, prm)["t"]
+        model = {"predicted_ms_per_step": 1e3 * pred, "measured_over_predicted": (t_ms / args.steps) / (1e3 * pred),
+                 "note": "costmodel.B200Params defaults (calibrated at n=30, 1 GPU); noisy flavours use ideal pass classes"}
+    except Exception as e:  # reporting only
+        model = {"error": repr(e)[:200]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_s, k_s = 26, 2
@@ -341,6 +356,7 @@ def run_ours(args):
                 "clocks": clocks.summary(),
                 "phases_ms": {nm: v[1] for nm, v in prof.items() if v[0]},
                 "nvlink": nvlink,
+                "model": model,
                 "p_success": p_success}
         print(json.dumps(line), flush=True)
     sv.sv_free(ctx)
