@@ -126,14 +126,14 @@ class B200Params:
     round-1 measurements, profiles/r1_costmodel_b200.json)."""
     # achieved HBM bytes/s (2 S_l per pass) per pass class; "default" covers
     # classes not calibrated
-    bw_pass: dict = dataclasses.field(default_factory=lambda: dict({'run4': 6384000000000.0, 'run13': 6996000000000.0, 'run5_fused': 6412000000000.0, 'run4_fused': 6337000000000.0, 'default': 6656000000000.0}))
-    bw_mean: float = 5.82e+12        # fused flip + invert-about-mean pass (2 S_l)
-    bw_reduce: float = 7.065e+12      # read-only sum pass (S_l)
-    t_gate: float = 6.926e-13          # seconds per amplitude pair per general 2x2 op (compute term)
-    t_diag: float = 1.862e-13          # ... per diagonal op (phase / controlled phase)
-    t_lin: float = 9.901e-13          # ... per merged phase-polynomial op (a run of >= 4 single-control phases)
+    bw_pass: dict = dataclasses.field(default_factory=lambda: dict({'run4': 6390000000000.0, 'run13': 7010000000000.0, 'run5_fused': 6415000000000.0, 'run4_fused': 6340000000000.0, 'run3': 3021000000000.0, 'run3_fused': 4211000000000.0, 'default': 4906000000000.0}))
+    bw_mean: float = 5.44e+12        # fused flip + invert-about-mean pass (2 S_l)
+    bw_reduce: float = 5.363e+12      # read-only sum pass (S_l)
+    t_gate: float = 6.956e-13          # seconds per amplitude pair per general 2x2 op (compute term)
+    t_diag: float = 1.887e-13          # ... per diagonal op (phase / controlled phase)
+    t_lin: float = 9.864e-13          # ... per merged phase-polynomial op (a run of >= 4 single-control phases)
     bw_nvlink: float = 900e9       # per direction, NVLink 5 (nominal)
-    bw_copy: float = 6.331e+12        # device-local copy (emulated exchange), bytes moved / s
+    bw_copy: float = 6.351e+12        # device-local copy (emulated exchange), bytes moved / s
     t_lat: float = 15e-6           # one NCCL collective
     t_launch: float = 2e-6         # per kernel launch gap
 

@@ -4,7 +4,7 @@ Calculated run times", section 3.5.2).
 
 python tools/costmodel_validate.py [--out gpurun_out/costmodel_validation.json] [--quick]
 
-Calibration (n = 30, complex64): per-class WHT pass bandwidths, the mean /
+Calibration (complex64; n = 30 and 33 for the pass classes): per-class WHT pass bandwidths, the mean /
 reduce pass bandwidths, the per-pair gate cost t_gate from a compute-bound
 gate pass, the emulated exchange copy bandwidth.  Validation: other sizes
 (n = 28, 32, 34), the mean diffusion, gate circuits, emulated sharding.
@@ -41,21 +41,30 @@ def profiled(ctx, fn):
     return sum(ms for _, ms in tl), tl
 
 
-def calibrate(n=30):
+def calibrate(n=30, class_sizes=(30, 33)):
     prm = CM.B200Params()
     S = (1 << n) * 8
+    # pass-class bandwidths from n = 30 and n = 33 (whose strided groups have
+    # the 64-B-run classes n = 32 uses; n = 28, 32, 34 stay held out)
+    by = collections.defaultdict(list)
+    tot_b = tot_t = 0.0
+    for nc in class_sizes:
+        Sc = (1 << nc) * 8
+        with sv.sv_init(nc, 1, sv.SV_C64, sv.SV_INIT_UNIFORM) as c:
+            sv.sv_set_marked(c, sv.sv_marked_from_seed(nc, 16, 1))
+            k = 4
+            _, tl = profiled(c, lambda: sv.sv_iterate(c, k, sv.SV_DIFFUSE_WHT))
+            plan = [s for s in sv.sv_plan_wht(nc, 1, sv.SV_C64, k, True) if s["kind"] == 0]
+            passes = [ms for kind, ms in tl if kind == sv.SV_K_WHT_TILE]
+            assert len(plan) == len(passes)
+            for st, ms in zip(plan, passes):
+                by[CM.pass_class(st["tile_mask"], bool(st["pre"] and st["post"]))].append(2 * Sc / (ms / 1e3))
+            tot_b += 2 * Sc * len(passes)
+            tot_t += sum(passes) / 1e3
+    prm.bw_pass = {cls: float(np.mean(v)) for cls, v in by.items()}
+    prm.bw_pass["default"] = tot_b / tot_t
     with sv.sv_init(n, 1, sv.SV_C64, sv.SV_INIT_UNIFORM) as c:
         sv.sv_set_marked(c, sv.sv_marked_from_seed(n, 16, 1))
-        k = 4
-        _, tl = profiled(c, lambda: sv.sv_iterate(c, k, sv.SV_DIFFUSE_WHT))
-        plan = [s for s in sv.sv_plan_wht(n, 1, sv.SV_C64, k, True) if s["kind"] == 0]
-        passes = [ms for kind, ms in tl if kind == sv.SV_K_WHT_TILE]
-        assert len(plan) == len(passes)
-        by = collections.defaultdict(list)
-        for st, ms in zip(plan, passes):
-            by[CM.pass_class(st["tile_mask"], bool(st["pre"] and st["post"]))].append(ms)
-        prm.bw_pass = {cls: 2 * S / (np.mean(v) / 1e3) for cls, v in by.items()}
-        prm.bw_pass["default"] = 2 * S * len(passes) / (sum(passes) / 1e3)
         _, tl = profiled(c, lambda: sv.sv_iterate(c, 8, sv.SV_DIFFUSE_MEAN))
         red = [ms for kind, ms in tl if kind == sv.SV_K_REDUCE]
         mean = [ms for kind, ms in tl if kind == sv.SV_K_MEAN]
@@ -143,7 +152,7 @@ def main():
         row(f"WHT n=30 k=4 emulated P={P} (a2a copies)", P, observe_wht(30, 4, world=P, fused=False),
             CM.predict_wht(30, P, 0, 4, prm, emulated=True, fused_exchange=False)["t"])
     rel = [abs(r["relative_difference"]) for r in rows]
-    out = {"calibration": {"n": 30, "dtype": "c64", "bw_pass": prm.bw_pass, "bw_mean": prm.bw_mean,
+    out = {"calibration": {"n": 30, "pass_class_sizes": [30, 33], "dtype": "c64", "bw_pass": prm.bw_pass, "bw_mean": prm.bw_mean,
                            "bw_reduce": prm.bw_reduce, "t_gate": prm.t_gate, "t_diag": prm.t_diag, "t_lin": prm.t_lin, "bw_copy": prm.bw_copy,
                            "t_launch": prm.t_launch, "bw_nvlink_nominal": prm.bw_nvlink, "t_lat_assumed": prm.t_lat},
            "paper_terms": {"t_op_per_pair_per_pass_s": prm.as_machine_params(0).t_op2, "t_t": 0.0,
