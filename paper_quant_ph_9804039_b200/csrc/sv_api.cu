@@ -491,6 +491,13 @@ void run_wht_graphed(sv_ctx *c, int k) {
         run_wht_schedule(c, k, true);
         return;
     }
+    // bounded graphs: k iterations = consecutive calls of at most kGraphIters
+    // (each call is the same product; one extra unfused pass per chunk)
+    constexpr int kGraphIters = 256;
+    if (k > kGraphIters) {
+        for (int done = 0; done < k; done += kGraphIters) run_wht_graphed(c, std::min(kGraphIters, k - done));
+        return;
+    }
     for (const auto &ge : c->graphs)
         if (ge.k == k && ge.fused == c->fused_xchg && ge.epoch == c->marked_epoch) {
             SV_CUDA(cudaGraphLaunch(ge.exec, c->stream));

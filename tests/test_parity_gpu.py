@@ -493,3 +493,15 @@ def test_graph_replay_matches_launched(dtype, monkeypatch):
     for mk, k in ((sets[0], 5), (sets[0], 5), (sets[1], 5), (sets[1], 3)):
         ref = orc.iterate(ref, mk, k, orc.WHT)
     assert_close(res["1"][-1], ref, dtype, "graph replay", n=n, k=18)
+
+
+def test_graph_replay_long_k_is_chunked():
+    """k beyond one bounded graph (256 iterations) runs as consecutive chunks."""
+    n, k = 16, 600
+    a0 = rand_state(n, sv.SV_C128)
+    mk = orc.marked_from_seed(n, 2, 3)
+    with ctx_with(a0, sv.SV_C128) as c:
+        sv.sv_set_marked(c, mk)
+        sv.sv_iterate(c, k, sv.SV_DIFFUSE_WHT)
+        got = sv.sv_get_amplitudes(c)
+    assert_close(got, orc.iterate(a0.copy(), mk, k, orc.WHT), sv.SV_C128, "chunked graphs", n=n, k=k)
