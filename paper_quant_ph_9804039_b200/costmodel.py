@@ -126,14 +126,15 @@ class B200Params:
     round-1 measurements, profiles/r1_costmodel_b200.json)."""
     # achieved HBM bytes/s (2 S_l per pass) per pass class; "default" covers
     # classes not calibrated
-    bw_pass: dict = dataclasses.field(default_factory=lambda: dict({'run4': 6390000000000.0, 'run13': 7010000000000.0, 'run5_fused': 6415000000000.0, 'run4_fused': 6340000000000.0, 'run3': 3021000000000.0, 'run3_fused': 4211000000000.0, 'default': 4906000000000.0}))
-    bw_mean: float = 5.44e+12        # fused flip + invert-about-mean pass (2 S_l)
-    bw_reduce: float = 5.363e+12      # read-only sum pass (S_l)
-    t_gate: float = 6.956e-13          # seconds per amplitude pair per general 2x2 op (compute term)
-    t_diag: float = 1.887e-13          # ... per diagonal op (phase / controlled phase)
-    t_lin: float = 9.864e-13          # ... per merged phase-polynomial op (a run of >= 4 single-control phases)
+    bw_pass: dict = dataclasses.field(default_factory=lambda: dict({'run4': 6383000000000.0, 'run13': 7010000000000.0, 'run5_fused': 6404000000000.0, 'run4_fused': 6334000000000.0, 'run3': 3020000000000.0, 'run3_fused': 4209000000000.0, 'default': 4905000000000.0}))
+    bw_mean: float = 5.934e+12        # fused flip + invert-about-mean pass (2 S_l)
+    bw_reduce: float = 6.909e+12      # read-only sum pass (S_l)
+    t_gate: float = 5.993e-13          # seconds per amplitude pair per general 2x2 op (compute term)
+    t_diag: float = 1.76e-13          # ... per diagonal op (phase / controlled phase)
+    t_lin: float = 1.081e-12          # ... per merged phase-polynomial op (a run of >= 4 single-control phases)
+    rho: float = 0                  # gate passes: fraction of min(memory, compute) hidden by overlap
     bw_nvlink: float = 900e9       # per direction, NVLink 5 (nominal)
-    bw_copy: float = 6.351e+12        # device-local copy (emulated exchange), bytes moved / s
+    bw_copy: float = 6.337e+12        # device-local copy (emulated exchange), bytes moved / s
     t_lat: float = 15e-6           # one NCCL collective
     t_launch: float = 2e-6         # per kernel launch gap
 
@@ -217,11 +218,16 @@ def _is_phase1(g) -> bool:
     return _is_diag(g) and m[0] == 1.0 and m[1] == 0.0 and bin(int(g["controls"])).count("1") <= 1
 
 
+def gate_pass_time(t_mem: float, t_ops: float, rho: float) -> float:
+    return t_mem + t_ops - rho * min(t_mem, t_ops)
+
+
 def predict_gates(n: int, world: int, dtype: int, gates, prm: B200Params, emulated: bool = False) -> dict:
-    """sv_apply_gates: each pass costs its HBM round trip plus its on-chip
-    work, ops x pairs x t_op(kind) -- Eq. 4's l s^(n_b - 1) t_op next to the
-    memory term (a CTA's load, compute and store phases barely overlap at 2
-    CTAs / SM); swaps as in predict_wht (unfused all-to-all)."""
+    """sv_apply_gates: each pass costs its HBM round trip t_mem plus its
+    on-chip work t_ops = ops x pairs x t_op(kind) -- Eq. 4's l s^(n_b - 1) t_op
+    next to the memory term -- less the part the two co-resident CTAs per SM
+    overlap: t_mem + t_ops - rho min(t_mem, t_ops), rho calibrated on one
+    balanced pass; swaps as in predict_wht (unfused all-to-all)."""
     from . import _sv as sv
 
     steps, order = sv.sv_plan_gates(n, world, dtype, gates)
@@ -243,7 +249,8 @@ def predict_gates(n: int, world: int, dtype: int, gates, prm: B200Params, emulat
         lin = st.get("lin_ops", 0)
         t_ops = (lin * prm.t_lin + (st["ops"] - lin) * (fd * prm.t_diag + (1.0 - fd) * prm.t_gate)) * (N_l / 2.0)
         if st["kind"] == 0:
-            t_pass += 2.0 * S_l / prm.bw(pass_class(st["tile_mask"], False)) + t_ops + prm.t_launch
+            t_mem = 2.0 * S_l / prm.bw(pass_class(st["tile_mask"], False))
+            t_pass += gate_pass_time(t_mem, t_ops, prm.rho) + prm.t_launch
             npass += 1
         else:
             t_pass += t_ops + prm.t_launch

@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <complex>
+#include <memory>
 
 #include "wht_kernels.cuh"
 
@@ -166,16 +167,24 @@ __device__ __forceinline__ void relayout_dyn(E (&x)[L::NR], E *sm, int tid, unsi
     }
 }
 
-template <typename R>
+// Op-program reads: GLB = the program in global memory (read-only path);
+// else it is a __grid_constant__ kernel parameter (constant bank).
+template <bool GLB, typename T>
+__device__ __forceinline__ T ldop(const T *q) {
+    if constexpr (GLB) return __ldg(q);
+    else return *q;
+}
+
+template <bool GLB, typename R>
 __device__ __forceinline__ void load_op(const GOp<R> *op, R (&m)[8], unsigned int &ph, unsigned int &ri,
                                         unsigned int &jm, unsigned int &tm, unsigned long long &fm) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) m[e] = __ldg(&op->m[e]);
-    ph = __ldg(&op->ph);
-    ri = __ldg(&op->ri);
-    jm = __ldg(&op->jm);
-    tm = __ldg(&op->tm);
-    fm = __ldg(&op->fm);
+    for (int e = 0; e < 8; ++e) m[e] = ldop<GLB>(&op->m[e]);
+    ph = ldop<GLB>(&op->ph);
+    ri = ldop<GLB>(&op->ri);
+    jm = ldop<GLB>(&op->jm);
+    tm = ldop<GLB>(&op->tm);
+    fm = ldop<GLB>(&op->fm);
 }
 
 template <typename E, typename R>
@@ -192,7 +201,7 @@ __device__ __forceinline__ E cprod(const E &a, const E &b) {
     return r;
 }
 
-template <class L, typename E, typename R>
+template <class L, bool GLB, typename E, typename R>
 __device__ __forceinline__ void apply_linphase(E (&x)[L::NR], const GOp<R> *ent, unsigned int cnt, unsigned int tcls,
                                                unsigned int tbit, unsigned int et, unsigned long long base,
                                                unsigned int nthr) {
@@ -207,8 +216,8 @@ __device__ __forceinline__ void apply_linphase(E (&x)[L::NR], const GOp<R> *ent,
     F.x = (R)1;
     F.y = (R)0;
     for (unsigned int e = RB + nthr + lane; e < cnt; e += 32u) {
-        const unsigned int w = __ldg(&ent[e].ri), bit = __ldg(&ent[e].jm);
-        if (w == LP_CONST || ((base >> bit) & 1ull)) cmul_by(F, __ldg(&ent[e].m[0]), __ldg(&ent[e].m[1]));
+        const unsigned int w = ldop<GLB>(&ent[e].ri), bit = ldop<GLB>(&ent[e].jm);
+        if (w == LP_CONST || ((base >> bit) & 1ull)) cmul_by(F, ldop<GLB>(&ent[e].m[0]), ldop<GLB>(&ent[e].m[1]));
     }
     if (cnt > RB + nthr) {  // any tile-uniform entries: every lane needs the full product
 #pragma unroll
@@ -224,9 +233,9 @@ __device__ __forceinline__ void apply_linphase(E (&x)[L::NR], const GOp<R> *ent,
     if (tcls == LP_THR && !((et >> tbit) & 1u)) return;  // target bit 0 for all of this thread's amplitudes
     E P[RB];
 #pragma unroll
-    for (int i = 0; i < RB; ++i) { P[i].x = __ldg(&ent[i].m[0]); P[i].y = __ldg(&ent[i].m[1]); }
+    for (int i = 0; i < RB; ++i) { P[i].x = ldop<GLB>(&ent[i].m[0]); P[i].y = ldop<GLB>(&ent[i].m[1]); }
     for (unsigned int e = RB; e < RB + nthr; ++e)
-        if ((et >> __ldg(&ent[e].jm)) & 1u) cmul_by(F, __ldg(&ent[e].m[0]), __ldg(&ent[e].m[1]));
+        if ((et >> ldop<GLB>(&ent[e].jm)) & 1u) cmul_by(F, ldop<GLB>(&ent[e].m[0]), ldop<GLB>(&ent[e].m[1]));
     // factor of register index j = F * prod_{i in bits(j)} P[i]: tables over
     // the low LO and the high HI register bits
     E lo[1 << LO], hi[1 << HI];
@@ -245,26 +254,18 @@ __device__ __forceinline__ void apply_linphase(E (&x)[L::NR], const GOp<R> *ent,
         }
 }
 
-template <typename E, int TB, int RB, bool XCHG, bool LIN>
-__global__ void __launch_bounds__(1 << (TB - RB), (TB - RB <= 7) ? 4 : 2)
-    gate_tile_kernel(const KParams p, const GOp<typename RealOf<E>::T> *__restrict__ ops, int nops) {
-    using L = Layout<E, TB, RB>;
-    using R = typename RealOf<E>::T;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    E *sm = reinterpret_cast<E *>(smem_raw);
-    __shared__ E *s_dst[XCHG ? 8 : 1];
-    if constexpr (XCHG) load_xdst(p, threadIdx.x, s_dst);
-    const int tid = threadIdx.x;
-    const unsigned long long base = tile_base(blockIdx.x, p);
-    E x[L::NR];
-    global_load<L, 0>(x, reinterpret_cast<const E *>(p.in) + base, p, tid);
+// The pass's op program on one tile held in registers (layout A on entry);
+// returns the layout the tile is left in.
+template <class L, bool LIN, bool GLB, typename E, typename R>
+__device__ __forceinline__ unsigned int run_gate_ops(E (&x)[L::NR], E *sm, int tid, unsigned long long base,
+                                                     const GOp<R> *__restrict__ ops, int nops) {
     const unsigned int eth[3] = {L::ethr(0, tid), L::ethr(1, tid), L::ethr(2, tid)};
     unsigned int cur = 0;
     for (int k = 0; k < nops; ++k) {
         R m[8];
         unsigned int ph, ri, jm, tm;
         unsigned long long fm;
-        load_op(ops + k, m, ph, ri, jm, tm, fm);
+        load_op<GLB>(ops + k, m, ph, ri, jm, tm, fm);
         const unsigned int kind = ph >> 8;
         ph &= 0xffu;
         if (ph != cur) {
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB <= 7) ? 4 : 2)
         const unsigned int et = cur == 0 ? eth[0] : (cur == 1 ? eth[1] : eth[2]);
         if constexpr (LIN) {  // passes holding merged phase runs get their own instantiation
             if (kind == GK_LINPHASE) {  // tm entry records follow
-                apply_linphase<L>(x, ops + k + 1, tm, ri, jm, et, base, (unsigned int)fm);
+                apply_linphase<L, GLB>(x, ops + k + 1, tm, ri, jm, et, base, (unsigned int)fm);
                 k += (int)tm;
                 continue;
             }
@@ -293,10 +294,50 @@ __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB <= 7) ? 4 : 2)
         }
         if ((et & tm) == tm && (base & fm) == fm) gate_dispatch<L>(x, m, ri, jm, kind);
     }
+    return cur;
+}
+
+template <class L, bool XCHG, typename E>
+__device__ __forceinline__ void gate_tile_store(const E (&x)[L::NR], unsigned int cur, const KParams &p,
+                                                unsigned long long base, int tid, E *const *s_dst) {
     E *gout = reinterpret_cast<E *>(p.out) + base;
     if (cur == 0) pass_store<L, 0, XCHG>(x, gout, base, p, tid, s_dst);
     else if (cur == 1) pass_store<L, 1, XCHG>(x, gout, base, p, tid, s_dst);
     else pass_store<L, 2, XCHG>(x, gout, base, p, tid, s_dst);
+}
+
+template <class L, bool XCHG, bool LIN, bool GLB, typename E, typename R>
+__device__ __forceinline__ void gate_tile_body(const KParams &p, const GOp<R> *ops, int nops) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    E *sm = reinterpret_cast<E *>(smem_raw);
+    __shared__ E *s_dst[XCHG ? 8 : 1];
+    if constexpr (XCHG) load_xdst(p, threadIdx.x, s_dst);
+    const int tid = threadIdx.x;
+    const unsigned long long base = tile_base(blockIdx.x, p);
+    E x[L::NR];
+    global_load<L, 0>(x, reinterpret_cast<const E *>(p.in) + base, p, tid);
+    const unsigned int cur = run_gate_ops<L, LIN, GLB>(x, sm, tid, base, ops, nops);
+    gate_tile_store<L, XCHG>(x, cur, p, base, tid, s_dst);
+}
+
+// One CTA per tile; the op program in global memory.
+template <typename E, int TB, int RB, bool XCHG, bool LIN>
+__global__ void __launch_bounds__(1 << (TB - RB), (TB - RB <= 7) ? 4 : 2)
+    gate_tile_kernel(const KParams p, const GOp<typename RealOf<E>::T> *__restrict__ ops, int nops) {
+    gate_tile_body<Layout<E, TB, RB>, XCHG, LIN, true, E>(p, ops, nops);
+}
+
+// The same with the op program as a kernel parameter (constant bank: uniform
+// loads, no global round trip per op) -- passes of up to kParamOps records.
+constexpr size_t kParamProgBytes = 24576;
+template <typename R>
+struct GProg {
+    GOp<R> op[kParamProgBytes / sizeof(GOp<R>)];
+};
+template <typename E, int TB, int RB, bool XCHG, bool LIN>
+__global__ void __launch_bounds__(1 << (TB - RB), (TB - RB <= 7) ? 4 : 2)
+    gate_tile_kernel_p(const KParams p, const __grid_constant__ GProg<typename RealOf<E>::T> prog, int nops) {
+    gate_tile_body<Layout<E, TB, RB>, XCHG, LIN, false, E>(p, prog.op, nops);
 }
 
 // Whole state (n <= T) in one CTA: every gate as a V/2-pair loop over shared
@@ -314,7 +355,7 @@ __global__ void __launch_bounds__(512) gate_whole_kernel(E *a, int n, const GOp<
         R m[8];
         unsigned int ph, q, jm, tm;
         unsigned long long cm;
-        load_op(ops + k, m, ph, q, jm, tm, cm);
+        load_op<true>(ops + k, m, ph, q, jm, tm, cm);
         const unsigned int kind = ph >> 8;
         const unsigned int bit = 1u << q;
         for (unsigned int pr = tid; pr < N / 2; pr += nt) {
@@ -598,8 +639,18 @@ size_t append_ops(const std::vector<GOp<R>> &ops, std::vector<unsigned char> &pr
     return ops.size();
 }
 
+// SV_GATE_PARAM_OPS=0: always read the op program from global memory (A/B).
+inline bool gate_param_ops() {
+    static const int mode = [] {
+        const char *e = getenv("SV_GATE_PARAM_OPS");
+        return e ? atoi(e) : 1;
+    }();
+    return mode != 0;
+}
+
 template <typename E, int TB, int RB>
-void launch_tile_gates(const GatePassArgs &a, const void *dev_ops, uint64_t nops, bool lin, cudaStream_t s) {
+void launch_tile_gates(const GatePassArgs &a, const void *dev_ops, const void *host_ops, uint64_t nops, bool lin,
+                       cudaStream_t s) {
     using L = Layout<E, TB, RB>;
     using R = typename RealOf<E>::T;
     KParams kp{};
@@ -630,17 +681,29 @@ void launch_tile_gates(const GatePassArgs &a, const void *dev_ops, uint64_t nops
     SV_CHECK(nops <= 0x7fffffffull, SV_EINVAL, "too many gates in one pass");
     const unsigned long long ntiles = 1ull << f;
     SV_CHECK(ntiles <= 0x7fffffffull, SV_EINVAL, "too many tiles for one launch");
-    auto fn = lin ? (kp.xchg ? gate_tile_kernel<E, TB, RB, true, true> : gate_tile_kernel<E, TB, RB, false, true>)
-                  : (kp.xchg ? gate_tile_kernel<E, TB, RB, true, false> : gate_tile_kernel<E, TB, RB, false, false>);
     const int smem = (1 << TB) * (int)sizeof(E);
     static bool attr = false;
     if (!attr) {
         for (auto f : {gate_tile_kernel<E, TB, RB, true, true>, gate_tile_kernel<E, TB, RB, false, true>,
                        gate_tile_kernel<E, TB, RB, true, false>, gate_tile_kernel<E, TB, RB, false, false>})
             SV_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        for (auto f : {gate_tile_kernel_p<E, TB, RB, true, true>, gate_tile_kernel_p<E, TB, RB, false, true>,
+                       gate_tile_kernel_p<E, TB, RB, true, false>, gate_tile_kernel_p<E, TB, RB, false, false>})
+            SV_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;
     }
-    fn<<<(unsigned int)ntiles, L::NT, smem, s>>>(kp, reinterpret_cast<const GOp<R> *>(dev_ops), (int)nops);
+    constexpr uint64_t cap = sizeof(GProg<R>) / sizeof(GOp<R>);
+    if (host_ops != nullptr && nops <= cap && gate_param_ops()) {
+        auto prog = std::make_unique<GProg<R>>();
+        memcpy(prog->op, host_ops, nops * sizeof(GOp<R>));
+        auto fn = lin ? (kp.xchg ? gate_tile_kernel_p<E, TB, RB, true, true> : gate_tile_kernel_p<E, TB, RB, false, true>)
+                      : (kp.xchg ? gate_tile_kernel_p<E, TB, RB, true, false> : gate_tile_kernel_p<E, TB, RB, false, false>);
+        fn<<<(unsigned int)ntiles, L::NT, smem, s>>>(kp, *prog, (int)nops);
+    } else {
+        auto fn = lin ? (kp.xchg ? gate_tile_kernel<E, TB, RB, true, true> : gate_tile_kernel<E, TB, RB, false, true>)
+                      : (kp.xchg ? gate_tile_kernel<E, TB, RB, true, false> : gate_tile_kernel<E, TB, RB, false, false>);
+        fn<<<(unsigned int)ntiles, L::NT, smem, s>>>(kp, reinterpret_cast<const GOp<R> *>(dev_ops), (int)nops);
+    }
     SV_CUDA(cudaGetLastError());
 }
 
@@ -695,10 +758,10 @@ uint64_t build_gate_ops(sv_dtype dt, const GatePassArgs &a, bool whole, std::vec
     return append_ops(ops, prog);
 }
 
-void launch_gate_pass(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, uint64_t nops, bool has_lin,
-                      cudaStream_t s) {
-    if (dt == SV_C64) launch_tile_gates<float2, kGateTileBitsC64, kRegBitsC64>(a, dev_ops, nops, has_lin, s);
-    else launch_tile_gates<double2, kTileBitsC128, kRegBitsC128>(a, dev_ops, nops, has_lin, s);
+void launch_gate_pass(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, const void *host_ops, uint64_t nops,
+                      bool has_lin, cudaStream_t s) {
+    if (dt == SV_C64) launch_tile_gates<float2, kGateTileBitsC64, kRegBitsC64>(a, dev_ops, host_ops, nops, has_lin, s);
+    else launch_tile_gates<double2, kTileBitsC128, kRegBitsC128>(a, dev_ops, host_ops, nops, has_lin, s);
 }
 
 void launch_gate_whole(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, uint64_t nops, cudaStream_t s) {

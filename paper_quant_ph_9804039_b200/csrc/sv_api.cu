@@ -472,7 +472,9 @@ void run_gates(sv_ctx *c, const sv_gate *gates, uint64_t count) {
                     a.xchg_dst[j] = to_recv ? c->peer_recv[j] : c->peer_state[j];
             }
         }
-        run(c, SV_K_GATE_TILE, [&] { launch_gate_pass(c->dt, a, ops, where[i].second, lin[i] != 0, c->stream); });
+        run(c, SV_K_GATE_TILE, [&] {
+            launch_gate_pass(c->dt, a, ops, prog.data() + where[i].first, where[i].second, lin[i] != 0, c->stream);
+        });
         if (!c->fused_xchg) cur = c->state;
     }
     if (cur != c->state)

@@ -190,8 +190,11 @@ struct GatePassArgs {
 // phase runs (launched with the kernel instantiation that handles them).
 uint64_t build_gate_ops(sv_dtype dt, const GatePassArgs &a, bool whole, std::vector<unsigned char> &prog,
                         bool *has_lin);
-void launch_gate_pass(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, uint64_t nops, bool has_lin,
-                      cudaStream_t s);
+// dev_ops: the pass's records in device memory; host_ops: the same records on
+// the host (NULL = none) -- a program that fits the kernel-parameter space is
+// passed by value (constant bank) instead.
+void launch_gate_pass(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, const void *host_ops, uint64_t nops,
+                      bool has_lin, cudaStream_t s);
 void launch_gate_whole(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, uint64_t nops, cudaStream_t s);
 
 // ------------------------------------------------------------------------- //

@@ -151,6 +151,27 @@ def test_many_gates_on_few_qubits_one_pass(dtype):
     assert_close(run_gpu(a, dtype, gates), ref, dtype, 400, "one long pass")
 
 
+# A pass's op program rides in the kernel's parameter space (constant bank)
+# when it fits 24 KiB (384 complex64 / 256 complex128 records), else it is
+# read from global memory: one pass on each side of the boundary.
+PARAM_CAP = {sv.SV_C64: 384, sv.SV_C128: 256}
+
+
+@pytest.mark.parametrize("dtype", DT, ids=DT_IDS)
+@pytest.mark.parametrize("side", ["param", "global"])
+def test_op_program_param_and_global_paths(dtype, side):
+    n = 18
+    count = PARAM_CAP[dtype] if side == "param" else 2 * PARAM_CAP[dtype]
+    gates = C.random_circuit(n, count, 21, max_controls=2, qubits=[0, 2, 3, 6, 8, 11, 13, 16, 17])
+    steps, _ = sv.sv_plan_gates(n, 1, dtype, gates)
+    assert len(steps) == 1
+    ops = steps[0]["ops"]
+    assert (ops <= PARAM_CAP[dtype]) == (side == "param"), ops
+    a = rand_state(n, dtype, 22)
+    ref = orc.apply_gates(a.copy(), gates)
+    assert_close(run_gpu(a, dtype, gates), ref, dtype, count, f"{side} op program ({ops} ops)")
+
+
 @pytest.mark.parametrize("dtype", DT, ids=DT_IDS)
 @pytest.mark.parametrize("n", [4, 13, 16, 20])
 def test_qft_equals_fft(dtype, n):

@@ -78,16 +78,33 @@ def calibrate(n=30, class_sizes=(30, 33)):
     lin_runs = []
     for t in range(3, 13):  # QFT-like: 12 single-control phases per target -> one phase-polynomial op each
         lin_runs += [C.record(t, C.phase(0.1 * c + 0.05), [c]) for c in list(range(0, t)) + list(range(13, 15))][:12]
-    for attr, gates in (("t_gate", C.random_circuit(ng, 400, 5, max_controls=2, qubits=range(3, 13), p_control=1.0)),
-                        ("t_diag", C.circuit([C.record(3 + (i % 10), C.phase(0.1 * i + 0.05), [i % 3, 13 + i % 5])
-                                              for i in range(400)])),
-                        ("t_lin", C.circuit(lin_runs * 4))):
+    # (300 gates: the pass's op program stays within the kernel-parameter
+    # space the held-out workloads use, <= 384 records)
+    heavy = {"t_gate": C.random_circuit(ng, 300, 5, max_controls=2, qubits=range(3, 13), p_control=1.0),
+             "t_diag": C.circuit([C.record(3 + (i % 10), C.phase(0.1 * i + 0.05), [i % 3, 13 + i % 5])
+                                  for i in range(300)]),
+             "t_lin": C.circuit(lin_runs * 4)}
+    # overlap: one balanced pass (8 singly-controlled general 2x2 on tile
+    # qubits; compute ~ memory), solved jointly with the heavy passes
+    balanced = C.circuit([C.record(3 + 2 * (i % 5), C.random_unitary(np.random.default_rng(40 + i)), [4 + 2 * (i % 4)])
+                          for i in range(8)])
+    obs = {}
+    for attr, gates in list(heavy.items()) + [("rho", balanced)]:
         with sv.sv_init(ng, 1, sv.SV_C64, sv.SV_INIT_GAUSSIAN) as c:
             tot, _ = profiled(c, lambda: sv.sv_apply_gates(c, gates))
         steps, _ = sv.sv_plan_gates(ng, 1, sv.SV_C64, gates)
         assert len(steps) == 1
         ops = steps[0]["lin_ops"] if attr == "t_lin" else steps[0]["ops"]
-        setattr(prm, attr, max(tot / 1e3 - t_mem, 0.0) / (ops * (1 << (ng - 1))))
+        obs[attr] = (tot / 1e3, ops)
+    pairs = 1 << (ng - 1)
+    prm.rho = 0.0
+    for _ in range(20):  # heavy passes: t_ops > t_mem, so t = (1 - rho) t_mem + t_ops
+        for attr in heavy:
+            t, ops = obs[attr]
+            setattr(prm, attr, max(t - (1.0 - prm.rho) * t_mem, 0.0) / (ops * pairs))
+        t, ops = obs["rho"]
+        t_ops = ops * pairs * prm.t_gate
+        prm.rho = float(min(max((t_mem + t_ops - t) / max(min(t_mem, t_ops), 1e-12), 0.0), 1.0))
     # emulated exchange copy bandwidth (unfused mode: device-local chunk copies)
     ne = 28
     with sv.sv_init(ne, 1, sv.SV_C64, sv.SV_INIT_UNIFORM, world=2) as c:
@@ -153,7 +170,7 @@ def main():
             CM.predict_wht(30, P, 0, 4, prm, emulated=True, fused_exchange=False)["t"])
     rel = [abs(r["relative_difference"]) for r in rows]
     out = {"calibration": {"n": 30, "pass_class_sizes": [30, 33], "dtype": "c64", "bw_pass": prm.bw_pass, "bw_mean": prm.bw_mean,
-                           "bw_reduce": prm.bw_reduce, "t_gate": prm.t_gate, "t_diag": prm.t_diag, "t_lin": prm.t_lin, "bw_copy": prm.bw_copy,
+                           "bw_reduce": prm.bw_reduce, "t_gate": prm.t_gate, "t_diag": prm.t_diag, "t_lin": prm.t_lin, "rho": prm.rho, "bw_copy": prm.bw_copy,
                            "t_launch": prm.t_launch, "bw_nvlink_nominal": prm.bw_nvlink, "t_lat_assumed": prm.t_lat},
            "paper_terms": {"t_op_per_pair_per_pass_s": prm.as_machine_params(0).t_op2, "t_t": 0.0,
                            "t_b_s_per_byte": 1.0 / prm.bw_nvlink, "t_lr": 0.0},
