@@ -126,15 +126,15 @@ class B200Params:
     round-1 measurements, profiles/r1_costmodel_b200.json)."""
     # achieved HBM bytes/s (2 S_l per pass) per pass class; "default" covers
     # classes not calibrated
-    bw_pass: dict = dataclasses.field(default_factory=lambda: dict({'run4': 6383000000000.0, 'run13': 7010000000000.0, 'run5_fused': 6404000000000.0, 'run4_fused': 6334000000000.0, 'run3': 3020000000000.0, 'run3_fused': 4209000000000.0, 'default': 4905000000000.0}))
-    bw_mean: float = 5.934e+12        # fused flip + invert-about-mean pass (2 S_l)
-    bw_reduce: float = 6.909e+12      # read-only sum pass (S_l)
-    t_gate: float = 5.993e-13          # seconds per amplitude pair per general 2x2 op (compute term)
-    t_diag: float = 1.76e-13          # ... per diagonal op (phase / controlled phase)
-    t_lin: float = 1.081e-12          # ... per merged phase-polynomial op (a run of >= 4 single-control phases)
+    bw_pass: dict = dataclasses.field(default_factory=lambda: dict({'run4': 6369000000000.0, 'run13': 7010000000000.0, 'run5_fused': 6400000000000.0, 'run4_fused': 6338000000000.0, 'run3': 3020000000000.0, 'run3_fused': 4193000000000.0, 'default': 4888000000000.0}))
+    bw_mean: float = 5.495e+12        # fused flip + invert-about-mean pass (2 S_l)
+    bw_reduce: float = 5.211e+12      # read-only sum pass (S_l)
+    t_gate: float = 5.752e-13          # seconds per amplitude pair per general 2x2 op (compute term)
+    t_diag: float = 1.248e-13          # ... per diagonal op (phase / controlled phase)
+    t_lin: float = 1.109e-12          # ... per merged phase-polynomial op (a run of >= 4 single-control phases)
     rho: float = 0                  # gate passes: fraction of min(memory, compute) hidden by overlap
     bw_nvlink: float = 900e9       # per direction, NVLink 5 (nominal)
-    bw_copy: float = 6.337e+12        # device-local copy (emulated exchange), bytes moved / s
+    bw_copy: float = 6.341e+12        # device-local copy (emulated exchange), bytes moved / s
     t_lat: float = 15e-6           # one NCCL collective
     t_launch: float = 2e-6         # per kernel launch gap
 

@@ -32,9 +32,16 @@
 
 namespace sv {
 
+// Coefficients per op record: w, x, y, z as (re, im); complex64 records add
+// the pairs (-w.im, w.im), (-x.im, x.im), (-y.im, y.im), (-z.im, z.im) so the
+// packed FFMA2 form reads them as 64-bit uniform operands (no per-pair
+// re-assembly).
+template <typename R>
+constexpr int kNM = sizeof(R) == 4 ? 16 : 8;
+
 template <typename R>
 struct alignas(16) GOp {
-    R m[8];                  // w, x, y, z as (re, im)
+    R m[kNM<R>];             // w, x, y, z as (re, im) [+ complex64: the (-im, im) pairs]
     unsigned int ph;         // register layout (0 = A, 1 = B, 2 = C) | kind << 8
     unsigned int ri;         // register index of the target tile bit (whole kernel: target slot)
     unsigned int jm;         // controls that are register bits of ph (register-index space)
@@ -71,8 +78,26 @@ enum GateKind : unsigned int {
 enum LinWhere : unsigned int { LP_REG = 0, LP_THR = 1, LP_FREE = 2, LP_CONST = 3 };
 
 // (u, v) <- (w u + x v, y u + z v), complex.
+#ifndef SV_GATE_PACKED
+#define SV_GATE_PACKED 1
+#endif
 template <typename E, typename R>
-__device__ __forceinline__ void cmat(E &u, E &v, const R (&m)[8]) {
+__device__ __forceinline__ void cmat(E &u, E &v, const R (&m)[kNM<R>]) {
+#if SV_GATE_PACKED
+    if constexpr (sizeof(R) == 4) {  // complex64: packed (re, im) FMUL2 / FFMA2, 8 instead of 16 per pair
+        const float2 a = u, b = v;
+        const float2 as = make_float2(a.y, a.x), bs = make_float2(b.y, b.x);
+        float2 t = __fmul2_rn(make_float2(m[0], m[0]), a);
+        t = __ffma2_rn(make_float2(m[8], m[9]), as, t);
+        t = __ffma2_rn(make_float2(m[2], m[2]), b, t);
+        u = __ffma2_rn(make_float2(m[10], m[11]), bs, t);
+        t = __fmul2_rn(make_float2(m[4], m[4]), a);
+        t = __ffma2_rn(make_float2(m[12], m[13]), as, t);
+        t = __ffma2_rn(make_float2(m[6], m[6]), b, t);
+        v = __ffma2_rn(make_float2(m[14], m[15]), bs, t);
+        return;
+    }
+#endif
     const E a = u, b = v;
     u.x = m[0] * a.x - m[1] * a.y + m[2] * b.x - m[3] * b.y;
     u.y = m[0] * a.y + m[1] * a.x + m[2] * b.y + m[3] * b.x;
@@ -88,8 +113,31 @@ __device__ __forceinline__ void cscale(E &c, R re, R im) {
     c.y = re * a.y + im * a.x;
 }
 
+// complex64: c <- coefficient q of the record times c, packed: (re, re) * c
+// + (-im, im) * swap(c)
+template <int Q>
+__device__ __forceinline__ float2 cscale_p(const float2 c, const float (&m)[16]) {
+    const float2 t = __fmul2_rn(make_float2(m[2 * Q], m[2 * Q]), c);
+    return __ffma2_rn(make_float2(m[8 + 2 * Q], m[9 + 2 * Q]), make_float2(c.y, c.x), t);
+}
+
 template <unsigned int K, typename E, typename R>
-__device__ __forceinline__ void cmat_k(E &u, E &v, const R (&m)[8]) {
+__device__ __forceinline__ void cmat_k(E &u, E &v, const R (&m)[kNM<R>]) {
+#if SV_GATE_PACKED
+    if constexpr (sizeof(R) == 4 && K != GK_GENERAL && K != GK_SWAP) {
+        if constexpr (K == GK_DIAG) {
+            u = cscale_p<0>(u, m);
+            v = cscale_p<3>(v, m);
+        } else if constexpr (K == GK_PHASE) {
+            v = cscale_p<3>(v, m);
+        } else {  // GK_ANTI
+            const float2 a = u;
+            u = cscale_p<1>(v, m);
+            v = cscale_p<2>(a, m);
+        }
+        return;
+    }
+#endif
     if constexpr (K == GK_GENERAL) {
         cmat(u, v, m);
     } else if constexpr (K == GK_DIAG) {
@@ -111,7 +159,7 @@ __device__ __forceinline__ void cmat_k(E &u, E &v, const R (&m)[8]) {
 }
 
 template <int I, unsigned int K, int NR, typename E, typename R>
-__device__ __forceinline__ void gate_apply(E (&x)[NR], const R (&m)[8], unsigned int jm) {
+__device__ __forceinline__ void gate_apply(E (&x)[NR], const R (&m)[kNM<R>], unsigned int jm) {
 #pragma unroll
     for (int j = 0; j < NR; ++j)
         if (!(j & (1 << I)))
@@ -122,7 +170,7 @@ __device__ __forceinline__ void gate_apply(E (&x)[NR], const R (&m)[8], unsigned
 #define SV_GATE_KINDS 2  // 2: all shapes; 1: general + phase; 0: general only (smaller code)
 #endif
 template <int I, int NR, typename E, typename R>
-__device__ __forceinline__ void gate_apply_kind(E (&x)[NR], const R (&m)[8], unsigned int jm, unsigned int kind) {
+__device__ __forceinline__ void gate_apply_kind(E (&x)[NR], const R (&m)[kNM<R>], unsigned int jm, unsigned int kind) {
 #if SV_GATE_KINDS >= 2
     switch (kind) {
         case GK_DIAG: gate_apply<I, GK_DIAG>(x, m, jm); break;
@@ -141,7 +189,7 @@ __device__ __forceinline__ void gate_apply_kind(E (&x)[NR], const R (&m)[8], uns
 }
 
 template <class L, typename E, typename R>
-__device__ __forceinline__ void gate_dispatch(E (&x)[L::NR], const R (&m)[8], unsigned int ri, unsigned int jm,
+__device__ __forceinline__ void gate_dispatch(E (&x)[L::NR], const R (&m)[kNM<R>], unsigned int ri, unsigned int jm,
                                               unsigned int kind) {
     switch (ri) {
         case 0: gate_apply_kind<0>(x, m, jm, kind); break;
@@ -176,10 +224,10 @@ __device__ __forceinline__ T ldop(const T *q) {
 }
 
 template <bool GLB, typename R>
-__device__ __forceinline__ void load_op(const GOp<R> *op, R (&m)[8], unsigned int &ph, unsigned int &ri,
+__device__ __forceinline__ void load_op(const GOp<R> *op, R (&m)[kNM<R>], unsigned int &ph, unsigned int &ri,
                                         unsigned int &jm, unsigned int &tm, unsigned long long &fm) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) m[e] = ldop<GLB>(&op->m[e]);
+    for (int e = 0; e < kNM<R>; ++e) m[e] = ldop<GLB>(&op->m[e]);
     ph = ldop<GLB>(&op->ph);
     ri = ldop<GLB>(&op->ri);
     jm = ldop<GLB>(&op->jm);
@@ -195,6 +243,12 @@ __device__ __forceinline__ void cmul_by(E &a, R br, R bi) {
 }
 template <typename E>
 __device__ __forceinline__ E cprod(const E &a, const E &b) {
+#if SV_GATE_PACKED
+    if constexpr (sizeof(a.x) == 4) {  // complex64: (b.re, b.re) * a + (-b.im, b.im) * swap(a)
+        const float2 t = __fmul2_rn(make_float2(b.x, b.x), a);
+        return __ffma2_rn(make_float2(-b.y, b.y), make_float2(a.y, a.x), t);
+    }
+#endif
     E r;
     r.x = a.x * b.x - a.y * b.y;
     r.y = a.x * b.y + a.y * b.x;
@@ -262,7 +316,7 @@ __device__ __forceinline__ unsigned int run_gate_ops(E (&x)[L::NR], E *sm, int t
     const unsigned int eth[3] = {L::ethr(0, tid), L::ethr(1, tid), L::ethr(2, tid)};
     unsigned int cur = 0;
     for (int k = 0; k < nops; ++k) {
-        R m[8];
+        R m[kNM<R>];
         unsigned int ph, ri, jm, tm;
         unsigned long long fm;
         load_op<GLB>(ops + k, m, ph, ri, jm, tm, fm);
@@ -352,7 +406,7 @@ __global__ void __launch_bounds__(512) gate_whole_kernel(E *a, int n, const GOp<
     for (unsigned int i = tid; i < N; i += nt) s[i] = a[i];
     __syncthreads();
     for (int k = 0; k < nops; ++k) {
-        R m[8];
+        R m[kNM<R>];
         unsigned int ph, q, jm, tm;
         unsigned long long cm;
         load_op<true>(ops + k, m, ph, q, jm, tm, cm);
@@ -393,6 +447,11 @@ template <typename R>
 GOp<R> op_coefs(const sv_gate &g) {
     GOp<R> o{};
     for (int e = 0; e < 8; ++e) o.m[e] = (R)g.m[e];
+    if constexpr (kNM<R> == 16)
+        for (int q = 0; q < 4; ++q) {
+            o.m[8 + 2 * q] = -(R)g.m[2 * q + 1];
+            o.m[9 + 2 * q] = (R)g.m[2 * q + 1];
+        }
     o.ph = gate_kind(g) << 8;
     return o;
 }

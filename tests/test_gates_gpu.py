@@ -152,9 +152,10 @@ def test_many_gates_on_few_qubits_one_pass(dtype):
 
 
 # A pass's op program rides in the kernel's parameter space (constant bank)
-# when it fits 24 KiB (384 complex64 / 256 complex128 records), else it is
+# when it fits 24 KiB (256 records of 96 B: complex64 records carry the packed
+# coefficient pairs, complex128 records the fp64 coefficients), else it is
 # read from global memory: one pass on each side of the boundary.
-PARAM_CAP = {sv.SV_C64: 384, sv.SV_C128: 256}
+PARAM_CAP = {sv.SV_C64: 256, sv.SV_C128: 256}
 
 
 @pytest.mark.parametrize("dtype", DT, ids=DT_IDS)

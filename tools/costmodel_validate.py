@@ -70,17 +70,17 @@ def calibrate(n=30, class_sizes=(30, 33)):
         mean = [ms for kind, ms in tl if kind == sv.SV_K_MEAN]
         prm.bw_reduce = S / (np.mean(red) / 1e3)
         prm.bw_mean = 2 * S / (np.mean(mean) / 1e3)
-    # gate compute: one compute-heavy pass at n = 26 on 10 target qubits
+    # gate compute: one compute-heavy pass at n = 28 on 10 target qubits
     # (controls differ, so little fuses), general unitaries and controlled
     # phases; t_op(kind) = (pass time - HBM round trip) / (ops x pairs)
-    ng = 26
+    ng = 28
     t_mem = 2 * (1 << ng) * 8 / prm.bw("run13")
     lin_runs = []
     for t in range(3, 13):  # QFT-like: 12 single-control phases per target -> one phase-polynomial op each
         lin_runs += [C.record(t, C.phase(0.1 * c + 0.05), [c]) for c in list(range(0, t)) + list(range(13, 15))][:12]
     # (300 gates: the pass's op program stays within the kernel-parameter
-    # space the held-out workloads use, <= 384 records)
-    heavy = {"t_gate": C.random_circuit(ng, 300, 5, max_controls=2, qubits=range(3, 13), p_control=1.0),
+    # space the held-out workloads use, <= 256 records)
+    heavy = {"t_gate": C.random_circuit(ng, 300, 5, max_controls=2, qubits=range(3, 13), p_control=0.5),
              "t_diag": C.circuit([C.record(3 + (i % 10), C.phase(0.1 * i + 0.05), [i % 3, 13 + i % 5])
                                   for i in range(300)]),
              "t_lin": C.circuit(lin_runs * 4)}
