@@ -112,12 +112,19 @@ TILE_BITS = {0: 13, 1: 12}
 
 def pass_class(tile_mask: int, fused: bool) -> str:
     """Bandwidth class of a tile pass: the contiguous run length of its tile
-    (low consecutive slots) and whether two stage sets are fused around an
-    elementwise op (twice the on-chip work)."""
+    (low consecutive slots), whether its first strided slot is >= 18 ("far":
+    a >= 2 MiB stride between the 64-128-B runs, which the DRAM serves at ~2/3
+    of the near-stride rate, profiles/r1_strided_rw_probe.txt) and whether two
+    stage sets are fused around an elementwise op (twice the on-chip work)."""
     run = 0
     while (tile_mask >> run) & 1:
         run += 1
-    return f"run{run}{'_fused' if fused else ''}"
+    rest, s = tile_mask >> run, run
+    while rest and not rest & 1:
+        rest >>= 1
+        s += 1
+    far = "_far" if rest and s >= 18 else ""
+    return f"run{run}{far}{'_fused' if fused else ''}"
 
 
 @dataclasses.dataclass
@@ -126,30 +133,35 @@ class B200Params:
     round-1 measurements, profiles/r1_costmodel_b200.json)."""
     # achieved HBM bytes/s (2 S_l per pass) per pass class; "default" covers
     # classes not calibrated
-    bw_pass: dict = dataclasses.field(default_factory=lambda: dict({'run4': 6369000000000.0, 'run13': 7010000000000.0, 'run5_fused': 6400000000000.0, 'run4_fused': 6338000000000.0, 'run3': 3020000000000.0, 'run3_fused': 4193000000000.0, 'default': 4888000000000.0}))
-    bw_mean: float = 5.495e+12        # fused flip + invert-about-mean pass (2 S_l)
-    bw_reduce: float = 5.211e+12      # read-only sum pass (S_l)
-    t_gate: float = 5.752e-13          # seconds per amplitude pair per general 2x2 op (compute term)
-    t_diag: float = 1.248e-13          # ... per diagonal op (phase / controlled phase)
-    t_lin: float = 1.109e-12          # ... per merged phase-polynomial op (a run of >= 4 single-control phases)
+    bw_pass: dict = dataclasses.field(default_factory=lambda: dict({'run4': 6367000000000.0, 'run13': 7010000000000.0, 'run5_far_fused': 6403000000000.0, 'run4_fused': 6336000000000.0, 'run3_far': 3020000000000.0, 'run3_fused': 5104000000000.0, 'run3_far_fused': 3015000000000.0, 'default': 4905000000000.0}))
+    bw_mean: float = 5.47e+12        # fused flip + invert-about-mean pass (2 S_l)
+    bw_reduce: float = 5.235e+12      # read-only sum pass (S_l)
+    t_gate: float = 5.748e-13          # seconds per amplitude pair per general 2x2 op (compute term)
+    t_diag: float = 1.241e-13          # ... per diagonal op (phase / controlled phase)
+    t_lin: float = 1.104e-12          # ... per merged phase-polynomial op (a run of >= 4 single-control phases)
     rho: float = 0                  # gate passes: fraction of min(memory, compute) hidden by overlap
     bw_nvlink: float = 900e9       # per direction, NVLink 5 (nominal)
-    bw_copy: float = 6.341e+12        # device-local copy (emulated exchange), bytes moved / s
+    bw_copy: float = 6.351e+12        # device-local copy (emulated exchange), bytes moved / s
     t_lat: float = 15e-6           # one NCCL collective
     t_launch: float = 2e-6         # per kernel launch gap
 
     def bw(self, cls: str) -> float:
-        """Calibrated bandwidth of a class, else of the calibrated class with
-        the same fusion flag and the nearest run length, else the default."""
+        """Calibrated bandwidth of a class, else of the same run length and
+        stride bucket with the other fusion flag, else of the calibrated class
+        with the same flags and the nearest run length, else the default."""
         if cls in self.bw_pass:
             return self.bw_pass[cls]
         fused = cls.endswith("_fused")
+        far = "_far" in cls
         run = int(cls[3:].split("_")[0])
+        other = f"run{run}{'_far' if far else ''}{'' if fused else '_fused'}"
+        if other in self.bw_pass:
+            return self.bw_pass[other]
         best = None
         for c, v in self.bw_pass.items():
             if not c.startswith("run") or c.endswith("_fused") != fused:
                 continue
-            d = abs(int(c[3:].split("_")[0]) - run)
+            d = 2 * abs(int(c[3:].split("_")[0]) - run) + (("_far" in c) != far)
             if best is None or d < best[0]:
                 best = (d, v)
         return best[1] if best else self.bw_pass.get("default", 5.6e12)
