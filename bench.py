@@ -135,17 +135,39 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline_sample(n: int, m: int, k: int, seed: int):
+def sample_shape(n_full: int, M: int, k_full: int, n_s: int, k_s: int):
+    """The bounded CPU sample of a config: n_s qubits with the marked set
+    scaled to the same density (>= 1), or the config itself when it is no
+    larger than the sample (c1, c2: the whole workload, k capped at k_s x 2^(n_s - n))."""
+    if n_full <= n_s:
+        return n_full, M, max(1, min(k_full, k_s << (n_s - n_full)))
+    return n_s, max(1, M >> (n_full - n_s)), k_s
+
+
+def oracle_iterate(orc, a, marked, k: int, diff: str, seed: int):
+    if diff == "wht-noisy":
+        orc.iterate_noisy(a, marked, k, 0.01, seed, 0)
+    elif diff == "wht-decoherent":
+        orc.iterate_decoherent(a, marked, k, 0.01, 1e-3, seed, 0)
+    else:
+        orc.iterate(a, marked, k, orc.MEAN if diff == "mean" else orc.WHT)
+
+
+def cpu_baseline_sample(n: int, m: int, k: int, seed: int, diff: str = "wht"):
     """The oracle as it stands (plain C, one thread) on a bounded sample of the
-    workload: same recipe at n qubits (uniform start, seeded marked set, WHT)."""
+    workload: same recipe at n qubits (uniform start, seeded marked set, same
+    diffusion)."""
     from oracle import oracle as orc
 
     marked = orc.marked_from_seed(n, m, seed)
-    a = orc.init_uniform(n)
-    t0 = time.perf_counter()
-    orc.iterate(a, marked, k, orc.WHT)
-    dt = time.perf_counter() - t0
-    return (1 << n) * k / dt, dt
+    dt, reps = 0.0, 0
+    while reps == 0 or dt < 2.0:  # small configs: repeat the whole run for >= 2 s of timed work
+        a = orc.init_uniform(n)
+        t0 = time.perf_counter()
+        oracle_iterate(orc, a, marked, k, diff, seed)
+        dt += time.perf_counter() - t0
+        reps += 1
+    return (1 << n) * k * reps / dt, dt
 
 
 def run_reference(args):
@@ -154,8 +176,9 @@ def run_reference(args):
     if rank != 0:
         return
     n_full, _, M, k_full, diff, seed, _, desc = CONFIGS[args.config]
-    n_s, k_s = 24, 1  # bounded sample per step: one WHT iteration at n=24 (~1-2 s)
-    m_s = max(1, M >> (n_full - n_s))
+    # bounded sample per step: one iteration at n=24 (~1-2 s), or the whole
+    # (smaller) config
+    n_s, m_s, k_s = sample_shape(n_full, M, k_full, 24, 1)
     from oracle import oracle as orc
 
     orc.build()
@@ -164,12 +187,7 @@ def run_reference(args):
     for i in range(args.warmup + args.steps):
         a = orc.init_uniform(n_s)
         t0 = time.perf_counter()
-        if diff == "wht-noisy":
-            orc.iterate_noisy(a, marked, k_s, 0.01, seed, 0)
-        elif diff == "wht-decoherent":
-            orc.iterate_decoherent(a, marked, k_s, 0.01, 1e-3, seed, 0)
-        else:
-            orc.iterate(a, marked, k_s, orc.MEAN if diff == "mean" else orc.WHT)
+        oracle_iterate(orc, a, marked, k_s, diff, seed)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
@@ -336,11 +354,10 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n_s, k_s = 26, 2
-        m_s = max(1, M >> (n - n_s))
-        v, dt = cpu_baseline_sample(n_s, m_s, k_s, seed)
+        n_s, m_s, k_s = sample_shape(n, M, k, 26, 2)
+        v, dt = cpu_baseline_sample(n_s, m_s, k_s, seed, diff)
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"plain C oracle, 1 thread, n={n_s} M={m_s} k={k_s} WHT iterations ({dt:.1f} s)"}
+               "sample": f"plain C oracle, 1 thread, n={n_s} M={m_s} k={k_s} {diff} iterations ({dt:.1f} s)"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -118,8 +118,38 @@ __global__ void __launch_bounds__(512) whole_state_kernel(E *a, int n, int k, in
     const unsigned int N = 1u << n, tid = threadIdx.x, nt = blockDim.x;
     for (unsigned int i = tid; i < N; i += nt) s[i] = a[i];
     __syncthreads();
+    // Two stages (qubits q, q + 1) per shared-memory round trip and barrier:
+    // each thread owns quads (i, i|b, i|2b, i|3b), applies qubit q's 2x2 to
+    // (0,1), (2,3), then qubit q+1's to (0,2), (1,3) -- the same pair
+    // operations in the same per-pair order as stage-by-stage.
     auto transform = [&](int it, int w) {
-        for (int q = 0; q < n; ++q) {
+        int q = 0;
+        for (; q + 1 < n; q += 2) {
+            const unsigned int b0 = 1u << q, b1 = 2u << q;
+            const double *c0 = coefs ? coefs + ((size_t)(2 * it + w) * n + q) * 4 : nullptr;
+            const double *c1 = c0 ? c0 + 4 : nullptr;
+            for (unsigned int pr = tid; pr < N / 4; pr += nt) {
+                const unsigned int i = ((pr >> q) << (q + 2)) | (pr & (b0 - 1));
+                E v0 = s[i], v1 = s[i | b0], v2 = s[i | b1], v3 = s[i | b0 | b1];
+                if (c0) {
+                    bfly_gen(v0, v1, c0);
+                    bfly_gen(v2, v3, c0);
+                    bfly_gen(v0, v2, c1);
+                    bfly_gen(v1, v3, c1);
+                } else {
+                    bfly(v0, v1);
+                    bfly(v2, v3);
+                    bfly(v0, v2);
+                    bfly(v1, v3);
+                }
+                s[i] = v0;
+                s[i | b0] = v1;
+                s[i | b1] = v2;
+                s[i | b0 | b1] = v3;
+            }
+            __syncthreads();
+        }
+        if (q < n) {  // odd n: the last qubit alone
             const unsigned int bit = 1u << q;
             const double *cq = coefs ? coefs + ((size_t)(2 * it + w) * n + q) * 4 : nullptr;
             for (unsigned int pr = tid; pr < N / 2; pr += nt) {

@@ -49,3 +49,18 @@ def test_configs_and_defaults():
     finally:
         sys.argv = argv
     assert (args.gpus, args.config, args.impl) == (1, "c4", "ours") and args.warmup >= 3
+
+
+@pytest.mark.parametrize("cfg", sorted(bench.CONFIGS))
+def test_cpu_sample_shape_is_bounded_and_valid(cfg):
+    """The oracle's bounded sample of every config: at most the sample size,
+    a marked set the generator accepts (1 <= m <= 2^n), k >= 1; configs smaller
+    than the sample run whole."""
+    n, _, M, k = bench.CONFIGS[cfg][:4]
+    for n_s, k_s in ((26, 2), (24, 1)):
+        ns, ms, ks = bench.sample_shape(n, M, k, n_s, k_s)
+        assert 1 <= ns <= max(n_s, n) and 1 <= ms <= (1 << ns) and ks >= 1
+        if n <= n_s:
+            assert (ns, ms) == (n, M) and ks <= k
+        else:
+            assert (ns, ks) == (n_s, k_s)
