@@ -313,11 +313,23 @@ def run_ours(args):
     kdesc = {"wht_tile": "wht_tile_kernel / wht_tile2_kernel",
              "mean": ("mean_resident_kernel (state held in shared memory for all k iterations; "
                       "bytes = 2 S per iteration, served on-chip)") if resident else "mean_kernel",
-             "wht_whole": "whole_state_kernel (one CTA; bytes = one load + store of the state)"}[kname]
+             "wht_whole": "whole_state_kernel (one CTA on one SM, state in shared memory)"}[kname]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": ncu_traffic(args.config, world), "kernel": f"{kname} ({kdesc})",
                 "algorithmic_bytes_per_launch": algo_bytes, "launches": launches, "avg_launch_ms": 1e3 * avg_s,
                 "share_of_step": kms / max(t_ms, 1e-9), "peak_source": peak_src}
+    if kname == "wht_whole":
+        # one CTA on one SM, state in shared memory: the bound is that SM's
+        # add rate -- k iterations x 2n stages x N/2 butterflies x 4 real adds
+        flops = k * 2 * n * (N_amp // 2) * 4
+        lanes = 64 if dtype == sv.SV_C128 else 128  # FP64 / FP32 lanes per SM (B200: 37 / 74 TFLOP/s over 148 SMs)
+        peak_g = lanes * 1.965  # GFLOP/s of adds at the 1965 MHz max SM clock
+        ach_g = flops / avg_s / 1e9
+        roofline = {"bound": "alu", "achieved": ach_g, "peak": peak_g, "unit": "GFLOP/s", "frac": ach_g / peak_g,
+                    "traffic": None, "kernel": f"{kname} ({kdesc})", "algorithmic_flops_per_launch": flops,
+                    "launches": launches, "avg_launch_ms": 1e3 * avg_s, "share_of_step": kms / max(t_ms, 1e-9),
+                    "peak_source": (f"one SM: {lanes} {'FP64' if lanes == 64 else 'FP32'} lanes x 1.965 GHz "
+                                    "(B200 vector peaks 37 / 74 TFLOP/s / 148 SMs / 2 flops per FMA)")}
     gpu_launches = int(sum(v[0] for name, v in prof.items() if name not in ("exchange", "allreduce")))
 
     # ---- end to end through the C ABI: pinned host inputs in, host scalar out

@@ -2,6 +2,8 @@
 // ideal-stage instantiation, the whole-state kernel and layout introspection.
 // The kernels themselves are in wht_kernels.cuh.
 #include <cuda_runtime.h>
+
+#include <type_traits>
 #include <math.h>
 
 #include "wht_kernels.cuh"
@@ -106,6 +108,12 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
 // in transform w of iteration it; F0 then carries no 2^{-n} (f0_scale = 1).
 // survival != nullptr: renormalise after every iteration (G22) and record the
 // pre-renormalisation sum |a|^2 of iteration it in survival[it].
+// stages per round trip: 0 = per dtype (measured on B200, 25 iterations:
+// complex128 n=10 / 12: 2 -> 102 / 316 us (1: 120 / 464, 3: 104 / 356,
+// 4: 110 / 317); complex64 n=13: 3 -> 409 us (1: 526, 2: 424, 4: 572))
+#ifndef SV_WHOLE_MAXR
+#define SV_WHOLE_MAXR 0
+#endif
 template <typename E>
 __global__ void __launch_bounds__(512) whole_state_kernel(E *a, int n, int k, int with_oracle, int diffusion,
                                                           const unsigned long long *marked,
@@ -118,46 +126,48 @@ __global__ void __launch_bounds__(512) whole_state_kernel(E *a, int n, int k, in
     const unsigned int N = 1u << n, tid = threadIdx.x, nt = blockDim.x;
     for (unsigned int i = tid; i < N; i += nt) s[i] = a[i];
     __syncthreads();
-    // Two stages (qubits q, q + 1) per shared-memory round trip and barrier:
-    // each thread owns quads (i, i|b, i|2b, i|3b), applies qubit q's 2x2 to
-    // (0,1), (2,3), then qubit q+1's to (0,2), (1,3) -- the same pair
-    // operations in the same per-pair order as stage-by-stage.
-    auto transform = [&](int it, int w) {
-        int q = 0;
-        for (; q + 1 < n; q += 2) {
-            const unsigned int b0 = 1u << q, b1 = 2u << q;
-            const double *c0 = coefs ? coefs + ((size_t)(2 * it + w) * n + q) * 4 : nullptr;
-            const double *c1 = c0 ? c0 + 4 : nullptr;
-            for (unsigned int pr = tid; pr < N / 4; pr += nt) {
-                const unsigned int i = ((pr >> q) << (q + 2)) | (pr & (b0 - 1));
-                E v0 = s[i], v1 = s[i | b0], v2 = s[i | b1], v3 = s[i | b0 | b1];
-                if (c0) {
-                    bfly_gen(v0, v1, c0);
-                    bfly_gen(v2, v3, c0);
-                    bfly_gen(v0, v2, c1);
-                    bfly_gen(v1, v3, c1);
-                } else {
-                    bfly(v0, v1);
-                    bfly(v2, v3);
-                    bfly(v0, v2);
-                    bfly(v1, v3);
-                }
-                s[i] = v0;
-                s[i | b0] = v1;
-                s[i | b1] = v2;
-                s[i | b0 | b1] = v3;
+    // Up to kMaxR stages (qubits q .. q + RR - 1) per shared-memory round trip
+    // and barrier: each thread owns a group of 2^RR amplitudes differing in
+    // those qubits, keeps them in registers and applies the RR stages in qubit
+    // order -- the same pair operations in the same per-pair order as
+    // stage-by-stage, so results are bit-identical.
+    auto phase = [&](auto rr, int it, int w, int q) {
+        constexpr int RR = decltype(rr)::value;
+        constexpr unsigned int G = 1u << RR;
+        const unsigned int lowm = (1u << q) - 1u;
+        for (unsigned int pr = tid; pr < (N >> RR); pr += nt) {
+            const unsigned int i0 = ((pr >> q) << (q + RR)) | (pr & lowm);
+            E v[G];
+#pragma unroll
+            for (unsigned int g = 0; g < G; ++g) v[g] = s[i0 | (g << q)];
+#pragma unroll
+            for (int r = 0; r < RR; ++r) {
+                const double *c = coefs ? coefs + ((size_t)(2 * it + w) * n + q + r) * 4 : nullptr;
+#pragma unroll
+                for (unsigned int g = 0; g < G; ++g)
+                    if (!(g & (1u << r))) {
+                        if (c) bfly_gen(v[g], v[g | (1u << r)], c);
+                        else bfly(v[g], v[g | (1u << r)]);
+                    }
             }
-            __syncthreads();
+#pragma unroll
+            for (unsigned int g = 0; g < G; ++g) s[i0 | (g << q)] = v[g];
         }
-        if (q < n) {  // odd n: the last qubit alone
-            const unsigned int bit = 1u << q;
-            const double *cq = coefs ? coefs + ((size_t)(2 * it + w) * n + q) * 4 : nullptr;
-            for (unsigned int pr = tid; pr < N / 2; pr += nt) {
-                const unsigned int i = ((pr >> q) << (q + 1)) | (pr & (bit - 1));
-                if (cq) bfly_gen(s[i], s[i | bit], cq);
-                else bfly(s[i], s[i | bit]);
+        __syncthreads();
+    };
+    auto transform = [&](int it, int w) {
+        for (int q = 0; q < n;) {
+            // as many stages as keep >= 256 threads busy (N / 2^rr groups), at most 4
+            constexpr int kMaxR = SV_WHOLE_MAXR > 0 ? SV_WHOLE_MAXR : (sizeof(E) == 8 ? 3 : 2);
+            int rr = n - q >= kMaxR ? kMaxR : n - q;
+            while (rr > 1 && (N >> rr) < 256u) --rr;
+            switch (rr) {
+                case 4: phase(std::integral_constant<int, 4>{}, it, w, q); break;
+                case 3: phase(std::integral_constant<int, 3>{}, it, w, q); break;
+                case 2: phase(std::integral_constant<int, 2>{}, it, w, q); break;
+                default: phase(std::integral_constant<int, 1>{}, it, w, q); break;
             }
-            __syncthreads();
+            q += rr;
         }
     };
     const int reps = k;
