@@ -107,6 +107,12 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         if self.proc is not None:
+            # a timed region shorter than nvidia-smi's start-up + first period
+            # (c1, c2: milliseconds) gets one sample taken right after it
+            t_end = time.perf_counter()
+            self.late = not self.lines
+            while not self.lines and time.perf_counter() - t_end < 2.0 and self.proc.poll() is None:
+                time.sleep(0.01)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -131,8 +137,11 @@ class ClockSampler:
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+               "samples": len(sm)}
+        if getattr(self, "late", False):
+            out["note"] = "timed region shorter than the first nvidia-smi sample: sampled right after it"
+        return out
 
 
 def sample_shape(n_full: int, M: int, k_full: int, n_s: int, k_s: int):
@@ -348,6 +357,15 @@ def run_ours(args):
     e2e_s = svd.max_over_ranks(time.perf_counter() - t0)
     e2e = {"value": N_amp * k * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(M * 8),
            "d2h_bytes_per_step": 8, "p_success": p_success}
+    # correctness of the timed result at full size: from the uniform start the
+    # ideal iteration has the closed form sin^2((2k+1) theta), sin theta =
+    # sqrt(M/N) (both diffusions); noisy runs and the Gaussian start have none
+    check = None
+    if init == "uniform" and diff in ("wht", "mean"):
+        import math
+        cf = math.sin((2 * k + 1) * math.asin(math.sqrt(M / N_amp))) ** 2
+        check = {"p_success": p_success, "closed_form": cf, "abs_err": abs(p_success - cf),
+                 "what": "marked mass after k iterations from the uniform start vs sin^2((2k+1) theta)"}
 
     # the B200 refit of the paper's analytical model (costmodel.py) for this
     # step, next to the measurement: its prediction error is the Table 5/6 analog
@@ -386,7 +404,7 @@ def run_ours(args):
                 "phases_ms": {nm: v[1] for nm, v in prof.items() if v[0]},
                 "nvlink": nvlink,
                 "model": model,
-                "p_success": p_success}
+                "p_success": p_success, "check": check}
         print(json.dumps(line), flush=True)
     sv.sv_free(ctx)
     if world > 1:
