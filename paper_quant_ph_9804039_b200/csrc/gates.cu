@@ -339,6 +339,16 @@ __device__ __forceinline__ unsigned int run_gate_ops(E (&x)[L::NR], E *sm, int t
                 const bool one = (et >> ri) & 1u;
                 const R fr = one ? m[6] : m[0], fi = one ? m[7] : m[1];
                 if (!(fr == (R)1 && fi == (R)0)) {
+#if SV_GATE_PACKED
+                    if constexpr (sizeof(R) == 4) {  // packed: (fr, fr) * x + (-fi, fi) * swap(x)
+                        const float2 pr = make_float2(fr, fr), pi = make_float2(-fi, fi);
+#pragma unroll
+                        for (int j = 0; j < L::NR; ++j)
+                            if (((unsigned int)j & jm) == jm)
+                                x[j] = __ffma2_rn(pi, make_float2(x[j].y, x[j].x), __fmul2_rn(pr, x[j]));
+                        continue;
+                    }
+#endif
 #pragma unroll
                     for (int j = 0; j < L::NR; ++j)
                         if (((unsigned int)j & jm) == jm) cmul_by(x[j], fr, fi);
