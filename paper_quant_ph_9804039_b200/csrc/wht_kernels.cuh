@@ -273,16 +273,11 @@ __device__ __forceinline__ void bfly_tan(E &x, E &y, double td) {
 template <>
 __device__ __forceinline__ void bfly_tan<float2>(float2 &x, float2 &y, double td) {
     const float t = (float)td;
-    const float2 T = make_float2(t, t);
-    const unsigned long long a = *reinterpret_cast<unsigned long long *>(&x);
-    const unsigned long long b = *reinterpret_cast<unsigned long long *>(&y);
-    const unsigned long long t2 = *reinterpret_cast<const unsigned long long *>(&T);
-    unsigned long long u, v;
-    asm("fma.rn.f32x2 %0, %3, %4, %2;\n\t"          // u = t b + a
-        "fma.rn.f32x2 %1, %3, %2, %5;"               // v = t a - b
-        : "=&l"(u), "=&l"(v) : "l"(a), "l"(t2), "l"(b), "l"(b ^ 0x8000000080000000ull));
-    x = *reinterpret_cast<float2 *>(&u);
-    y = *reinterpret_cast<float2 *>(&v);
+    const float2 T = make_float2(t, t), a = x, b = y;
+    // intrinsics (not inline asm) so ptxas folds the negation of b into the
+    // FFMA2 operand instead of a LOP3 per butterfly
+    x = __ffma2_rn(T, b, a);                          // u = t b + a
+    y = __ffma2_rn(T, a, make_float2(-b.x, -b.y));    // v = t a - b
 }
 
 template <typename E, typename R>

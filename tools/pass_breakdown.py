@@ -25,14 +25,20 @@ def main():
     ap.add_argument("--m", type=int, default=256)
     ap.add_argument("--dtype", default="c64")
     ap.add_argument("--world", type=int, default=1, help="emulated shards on one GPU")
+    ap.add_argument("--sigma", type=float, default=0.0, help="> 0: sv_iterate_noisy (NEXT-1 angle errors), same schedule")
     a = ap.parse_args()
     dt = sv.SV_C64 if a.dtype == "c64" else sv.SV_C128
     eb = 8 if dt == sv.SV_C64 else 16
     ctx = sv.sv_init(a.n, 0, dt, sv.SV_INIT_UNIFORM, world=a.world)
     sv.sv_set_marked(ctx, sv.sv_marked_from_seed(a.n, a.m, 1))
-    sv.sv_iterate(ctx, 1, sv.SV_DIFFUSE_WHT)  # warm-up
+    def run(k):
+        if a.sigma > 0:
+            sv.sv_iterate_noisy(ctx, k, a.sigma, 7, 0)
+        else:
+            sv.sv_iterate(ctx, k, sv.SV_DIFFUSE_WHT)
+    run(1)  # warm-up
     sv.sv_profile(ctx, True)
-    sv.sv_iterate(ctx, a.k, sv.SV_DIFFUSE_WHT)
+    run(a.k)
     tl = sv.sv_profile_timeline(ctx)
     plan = sv.sv_plan_wht(a.n, a.world, dt, a.k, True)
     agg = collections.OrderedDict()
@@ -51,7 +57,7 @@ def main():
     bytes_pass = 2 * (1 << a.n) * eb
     out = {k: {"launches": len(v), "mean_ms": sum(v) / len(v), "GBps": bytes_pass / (sum(v) / len(v) / 1e3) / 1e9}
            for k, v in agg.items()}
-    print(json.dumps({"n": a.n, "k": a.k, "world": a.world, "passes": out, "total_ms": sum(ms for _, ms in tl)},
+    print(json.dumps({"n": a.n, "k": a.k, "world": a.world, "sigma": a.sigma, "passes": out, "total_ms": sum(ms for _, ms in tl)},
                      indent=1))
 
 
