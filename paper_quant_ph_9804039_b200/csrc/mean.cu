@@ -18,8 +18,17 @@
 
 namespace sv {
 
-constexpr int kMeanThreads = 256;
-constexpr int kMeanPer = 8;                                    // 16-byte vectors per thread per chunk
+#ifndef SV_MEAN_PER
+#define SV_MEAN_PER 8
+#endif
+#ifndef SV_MEAN_PIPE
+#define SV_MEAN_PIPE 1
+#endif
+#ifndef SV_MEAN_THREADS
+#define SV_MEAN_THREADS 256
+#endif
+constexpr int kMeanThreads = SV_MEAN_THREADS;
+constexpr int kMeanPer = SV_MEAN_PER;                          // 16-byte vectors per thread per chunk
 constexpr unsigned long long kChunkVec = kMeanThreads * kMeanPer;  // 2048 vectors = 32 KiB
 
 template <typename E> struct Vec;                 // one 16-byte vector
@@ -61,14 +70,40 @@ __global__ void __launch_bounds__(kMeanThreads) mean_kernel(MeanArgs a) {
     }
     V *p = reinterpret_cast<V *>(a.a);
     double sr = 0.0, si = 0.0;
+#if SV_MEAN_PIPE
+    // software pipeline: the next chunk's loads are issued before this
+    // chunk's stores (program order; the chunks are disjoint)
+    V nxt[kMeanPer];
+    if (blockIdx.x < nchunks) {
+        const unsigned long long w0 = blockIdx.x * kChunkVec + threadIdx.x;
+#pragma unroll
+        for (int u = 0; u < kMeanPer; ++u) {
+            const unsigned long long v = w0 + (unsigned long long)u * kMeanThreads;
+            if (v < nvec) nxt[u] = __ldcg(p + v);
+        }
+    }
+#endif
     for (unsigned long long c = blockIdx.x; c < nchunks; c += gridDim.x) {
         const unsigned long long v0 = c * kChunkVec + threadIdx.x;
         V buf[kMeanPer];
+#if SV_MEAN_PIPE
+#pragma unroll
+        for (int u = 0; u < kMeanPer; ++u) buf[u] = nxt[u];
+        if (c + gridDim.x < nchunks) {
+            const unsigned long long w0 = (c + gridDim.x) * kChunkVec + threadIdx.x;
+#pragma unroll
+            for (int u = 0; u < kMeanPer; ++u) {
+                const unsigned long long v = w0 + (unsigned long long)u * kMeanThreads;
+                if (v < nvec) nxt[u] = __ldcg(p + v);
+            }
+        }
+#else
 #pragma unroll
         for (int u = 0; u < kMeanPer; ++u) {
             const unsigned long long v = v0 + (unsigned long long)u * kMeanThreads;
             if (v < nvec) buf[u] = __ldcg(p + v);
         }
+#endif
         const bool any = a.n_marked != 0 && ((__ldg(&a.chunkmap[c >> 5]) >> (c & 31)) & 1u);
 #pragma unroll
         for (int u = 0; u < kMeanPer; ++u) {
