@@ -6,22 +6,30 @@
 // exceeds u_s times the total.
 //
 // Device plan (three launches, fp64, fixed order => deterministic):
-//   1. chunk_sum_kernel: one warp per 4096-amplitude chunk, 128 rows of 32
-//      lanes, row sums by a fixed xor-butterfly, accumulated in row order
-//      (HBM-bound read of the state);
+//   1. chunk_sum_kernel: one warp per 4096-amplitude chunk, 32 rows of 128
+//      amplitudes; lane l of a row owns its 4 consecutive amplitudes 4l..4l+3
+//      and sums them in order, the row sum is a fixed xor-butterfly over the
+//      lanes, rows are accumulated in row order (HBM-bound read of the state,
+//      32-64 contiguous bytes per lane);
 //   2. chunk_scan_kernel: one block, exclusive prefix of the chunk sums;
 //   3. sample_kernel: one warp per shot, binary search over the chunk
 //      prefixes, then the chunk's rows in the SAME order as kernel 1 until the
 //      running sum passes the target; the crossing lane comes from an
-//      inclusive warp scan of the row.
+//      inclusive warp scan of the lane sums, the amplitude from that lane's
+//      4 in order.
 #include <cuda_runtime.h>
 
 #include "sv_internal.h"
 
 namespace sv {
 
-constexpr int kSampChunk = 4096;  // amplitudes per chunk
-constexpr int kRows = kSampChunk / 32;
+constexpr int kSampChunk = 4096;        // amplitudes per chunk
+constexpr int kPerLane = 4;             // consecutive amplitudes per lane per row
+constexpr int kRowLen = 32 * kPerLane;  // 128 amplitudes per row
+constexpr int kRows = kSampChunk / kRowLen;
+#ifndef SV_SAMP_BATCH
+#define SV_SAMP_BATCH 8  // rows per batch of loads in the chunk-sum sweep
+#endif
 
 __device__ __forceinline__ uint64_t smix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -42,6 +50,44 @@ __device__ __forceinline__ double warp_xor_sum(double v) {
     return v;
 }
 
+// The lane's 4 probabilities of row r (fixed order), and their sum.
+template <typename E>
+__device__ __forceinline__ double lane_probs(const E *a, uint64_t i0, uint64_t N, double (&p)[kPerLane]) {
+#pragma unroll
+    for (int e = 0; e < kPerLane; ++e) p[e] = prob(a, i0 + e, N);
+    double q = p[0];
+#pragma unroll
+    for (int e = 1; e < kPerLane; ++e) q = __dadd_rn(q, p[e]);
+    return q;
+}
+
+// The same for a row lying entirely below N: vector loads, no guards.
+__device__ __forceinline__ double lane_probs_full(const float2 *a, uint64_t i0, double (&p)[kPerLane]) {
+    const float4 v0 = __ldcg(reinterpret_cast<const float4 *>(a + i0));
+    const float4 v1 = __ldcg(reinterpret_cast<const float4 *>(a + i0) + 1);
+    const float f[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+    for (int e = 0; e < kPerLane; ++e) {
+        const double re = (double)f[2 * e], im = (double)f[2 * e + 1];
+        p[e] = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+    }
+    double q = p[0];
+#pragma unroll
+    for (int e = 1; e < kPerLane; ++e) q = __dadd_rn(q, p[e]);
+    return q;
+}
+__device__ __forceinline__ double lane_probs_full(const double2 *a, uint64_t i0, double (&p)[kPerLane]) {
+#pragma unroll
+    for (int e = 0; e < kPerLane; ++e) {
+        const double2 v = __ldcg(a + i0 + e);
+        p[e] = __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));
+    }
+    double q = p[0];
+#pragma unroll
+    for (int e = 1; e < kPerLane; ++e) q = __dadd_rn(q, p[e]);
+    return q;
+}
+
 template <typename E>
 __global__ void __launch_bounds__(256) chunk_sum_kernel(const E *a, uint64_t N, double *sums, uint64_t nchunks) {
     const int lane = threadIdx.x & 31;
@@ -49,12 +95,22 @@ __global__ void __launch_bounds__(256) chunk_sum_kernel(const E *a, uint64_t N, 
     for (uint64_t c = blockIdx.x * wpb + threadIdx.x / 32; c < nchunks; c += (uint64_t)gridDim.x * wpb) {
         double acc = 0.0;
         const uint64_t base = c * kSampChunk;
-        for (int r0 = 0; r0 < kRows; r0 += 8) {
-            double p[8];  // 8 rows of loads in flight, then the same row order
+        if (base + kSampChunk <= N) {  // warp-uniform: the whole chunk is below N
+            for (int r0 = 0; r0 < kRows; r0 += SV_SAMP_BATCH) {
+                double q[SV_SAMP_BATCH];  // a batch of rows' loads in flight, then the same row order
 #pragma unroll
-            for (int r = 0; r < 8; ++r) p[r] = prob(a, base + (r0 + r) * 32 + lane, N);
+                for (int r = 0; r < SV_SAMP_BATCH; ++r) {
+                    double p[kPerLane];
+                    q[r] = lane_probs_full(a, base + (r0 + r) * kRowLen + kPerLane * lane, p);
+                }
 #pragma unroll
-            for (int r = 0; r < 8; ++r) acc = __dadd_rn(acc, warp_xor_sum(p[r]));
+                for (int r = 0; r < SV_SAMP_BATCH; ++r) acc = __dadd_rn(acc, warp_xor_sum(q[r]));
+            }
+        } else {
+            for (int r = 0; r < kRows; ++r) {
+                double p[kPerLane];
+                acc = __dadd_rn(acc, warp_xor_sum(lane_probs(a, base + r * kRowLen + kPerLane * lane, N, p)));
+            }
         }
         if (lane == 0) sums[c] = acc;
     }
@@ -127,19 +183,46 @@ __global__ void __launch_bounds__(256) sample_kernel(const E *a, uint64_t N, con
         uint64_t pick = (base + kSampChunk <= N ? base + kSampChunk : N) - 1;
         uint64_t last_nz = base;
         for (int r = 0; r < kRows; ++r) {
-            const uint64_t i = base + r * 32 + lane;
-            const double p = prob(a, i, N);
-            const double row = warp_xor_sum(p);
-            const unsigned nzm = __ballot_sync(0xffffffffu, p > 0.0);
-            if (nzm) last_nz = base + r * 32 + (31 - __clz(nzm));
+            const uint64_t i0 = base + r * kRowLen + kPerLane * lane;
+            double p[kPerLane];
+            const double q = base + kSampChunk <= N ? lane_probs_full(a, i0, p) : lane_probs(a, i0, N, p);
+            const double row = warp_xor_sum(q);
+            int lz = -1;  // the lane's last nonzero amplitude
+#pragma unroll
+            for (int e = 0; e < kPerLane; ++e)
+                if (p[e] > 0.0) lz = e;
+            const unsigned nzm = __ballot_sync(0xffffffffu, lz >= 0);
+            if (nzm) {
+                const int ll = 31 - __clz(nzm);
+                const int lze = __shfl_sync(0xffffffffu, lz, ll);
+                last_nz = base + r * kRowLen + kPerLane * ll + lze;
+            }
             if (__dadd_rn(run, row) > target) {
-                double inc = p;  // inclusive scan of the row (fixed order)
+                double inc = q;  // inclusive scan of the lane sums (fixed order)
                 for (int o = 1; o < 32; o <<= 1) {
                     const double v = __shfl_up_sync(0xffffffffu, inc, o);
                     if (lane >= o) inc = __dadd_rn(inc, v);
                 }
-                const unsigned m = __ballot_sync(0xffffffffu, __dadd_rn(run, inc) > target && p > 0.0);
-                pick = m ? base + r * 32 + (__ffs(m) - 1) : last_nz;
+                double exc = __shfl_up_sync(0xffffffffu, inc, 1);
+                if (lane == 0) exc = 0.0;
+                const unsigned m = __ballot_sync(0xffffffffu, __dadd_rn(run, inc) > target && q > 0.0);
+                if (!m) {
+                    pick = last_nz;
+                    break;
+                }
+                const int L = __ffs(m) - 1;
+                // that lane's amplitudes in order from its exclusive prefix
+                int e_pick = -1;
+                if (lane == L) {
+                    double cum = __dadd_rn(run, exc);
+                    for (int e = 0; e < kPerLane; ++e) {
+                        cum = __dadd_rn(cum, p[e]);
+                        if (cum > target && p[e] > 0.0) { e_pick = e; break; }
+                    }
+                    if (e_pick < 0) e_pick = lz;  // rounding: the lane's own last nonzero
+                }
+                e_pick = __shfl_sync(0xffffffffu, e_pick, L);
+                pick = base + r * kRowLen + kPerLane * L + e_pick;
                 break;
             }
             run = __dadd_rn(run, row);
