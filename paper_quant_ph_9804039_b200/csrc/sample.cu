@@ -24,7 +24,10 @@
 namespace sv {
 
 constexpr int kSampChunk = 4096;        // amplitudes per chunk
-constexpr int kPerLane = 4;             // consecutive amplitudes per lane per row
+#ifndef SV_SAMP_PER_LANE
+#define SV_SAMP_PER_LANE 4
+#endif
+constexpr int kPerLane = SV_SAMP_PER_LANE;  // consecutive amplitudes per lane per row
 constexpr int kRowLen = 32 * kPerLane;  // 128 amplitudes per row
 constexpr int kRows = kSampChunk / kRowLen;
 #ifndef SV_SAMP_BATCH
@@ -63,13 +66,12 @@ __device__ __forceinline__ double lane_probs(const E *a, uint64_t i0, uint64_t N
 
 // The same for a row lying entirely below N: vector loads, no guards.
 __device__ __forceinline__ double lane_probs_full(const float2 *a, uint64_t i0, double (&p)[kPerLane]) {
-    const float4 v0 = __ldcg(reinterpret_cast<const float4 *>(a + i0));
-    const float4 v1 = __ldcg(reinterpret_cast<const float4 *>(a + i0) + 1);
-    const float f[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
-    for (int e = 0; e < kPerLane; ++e) {
-        const double re = (double)f[2 * e], im = (double)f[2 * e + 1];
-        p[e] = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+    for (int h = 0; h < kPerLane / 2; ++h) {
+        const float4 v = __ldcg(reinterpret_cast<const float4 *>(a + i0) + h);
+        const double r0 = (double)v.x, i0d = (double)v.y, r1 = (double)v.z, i1 = (double)v.w;
+        p[2 * h] = __dadd_rn(__dmul_rn(r0, r0), __dmul_rn(i0d, i0d));
+        p[2 * h + 1] = __dadd_rn(__dmul_rn(r1, r1), __dmul_rn(i1, i1));
     }
     double q = p[0];
 #pragma unroll
