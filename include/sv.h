@@ -344,6 +344,14 @@ int sv_debug_tile_layout(int dtype, int phase, int tid, int reg, int *tile_elem,
 /* 1 if layout `phase` runs the butterfly stage of tile bit `bit`, else 0. */
 int sv_debug_tile_owner(int dtype, int phase, int bit);
 
+/* Shared-memory relayouts (register-layout changes between consecutive ops)
+ * the gate tile kernel performs in each step of sv_plan_gates' schedule, as
+ * rank 0 runs it (host only; 0 for swap / whole-state steps).  Writes at most
+ * cap entries, *nsteps = total.  Used by the analytical model (costmodel.py).
+ * Errors: as sv_plan_gates. */
+sv_status sv_debug_gate_relayouts(int n, int world, sv_dtype dtype, const sv_gate *gates, uint64_t count,
+                                  uint64_t *out, int cap, int *nsteps);
+
 /* Release every resource of the context (NULL-safe). */
 void sv_free(sv_ctx *ctx);
 

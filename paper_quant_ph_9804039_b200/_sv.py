@@ -84,6 +84,7 @@ _SIGS = {
     "sv_apply_gates": ([_ctxp, _vp, _u64], _i32),
     "sv_plan_gates": ([_i32, _i32, _i32, _vp, _u64, ctypes.POINTER(sv_gate_plan_step), _i32, ctypes.POINTER(_i32),
                        _vp], _i32),
+    "sv_debug_gate_relayouts": ([_i32, _i32, _i32, _vp, _u64, _vp, _i32, ctypes.POINTER(_i32)], _i32),
     "sv_profile": ([_ctxp, _i32], _i32),
     "sv_profile_read": ([_ctxp, _i32, ctypes.POINTER(_u64), _dp], _i32),
     "sv_profile_timeline": ([_ctxp, _vp, _vp, _u64, ctypes.POINTER(_u64)], _i32),
@@ -283,6 +284,17 @@ def sv_plan_gates(n: int, world: int, dtype: int, gates) -> tuple[list[dict], np
            "sv_plan_gates")
     steps = [{f: getattr(arr[i], f) for f, _ in sv_gate_plan_step._fields_} for i in range(cnt.value)]
     return steps, order[:g.size]
+
+
+def sv_debug_gate_relayouts(n: int, world: int, dtype: int, gates) -> np.ndarray:
+    g = _gates(gates)
+    ns = ctypes.c_int()
+    _check(lib.sv_debug_gate_relayouts(n, world, dtype, g.ctypes.data if len(g) else None, len(g), None, 0,
+                                       ctypes.byref(ns)), "sv_debug_gate_relayouts")
+    out = np.zeros(max(ns.value, 1), dtype=np.uint64)
+    _check(lib.sv_debug_gate_relayouts(n, world, dtype, g.ctypes.data if len(g) else None, len(g), out.ctypes.data,
+                                       ns.value, ctypes.byref(ns)), "sv_debug_gate_relayouts")
+    return out[:ns.value]
 
 
 def sv_profile(ctx: Ctx, enable: bool) -> None:

@@ -133,15 +133,16 @@ class B200Params:
     round-1 measurements, profiles/r1_costmodel_b200.json)."""
     # achieved HBM bytes/s (2 S_l per pass) per pass class; "default" covers
     # classes not calibrated
-    bw_pass: dict = dataclasses.field(default_factory=lambda: dict({'run4': 6367000000000.0, 'run13': 7010000000000.0, 'run5_far_fused': 6403000000000.0, 'run4_fused': 6336000000000.0, 'run3_far': 3020000000000.0, 'run3_fused': 5104000000000.0, 'run3_far_fused': 3015000000000.0, 'default': 4905000000000.0}))
-    bw_mean: float = 5.47e+12        # fused flip + invert-about-mean pass (2 S_l)
-    bw_reduce: float = 5.235e+12      # read-only sum pass (S_l)
-    t_gate: float = 5.748e-13          # seconds per amplitude pair per general 2x2 op (compute term)
-    t_diag: float = 1.241e-13          # ... per diagonal op (phase / controlled phase)
-    t_lin: float = 1.104e-12          # ... per merged phase-polynomial op (a run of >= 4 single-control phases)
+    bw_pass: dict = dataclasses.field(default_factory=lambda: dict({'run4': 6378000000000.0, 'run13': 7011000000000.0, 'run5_far_fused': 6409000000000.0, 'run4_fused': 6336000000000.0, 'run3_far': 3020000000000.0, 'run3_fused': 5104000000000.0, 'run3_far_fused': 3016000000000.0, 'default': 4905000000000.0}))
+    bw_mean: float = 6.178e+12        # fused flip + invert-about-mean pass (2 S_l)
+    bw_reduce: float = 6.771e+12      # read-only sum pass (S_l)
+    t_gate: float = 4.935e-13          # seconds per amplitude pair per general 2x2 op (compute term)
+    t_diag: float = 1.008e-13          # ... per diagonal op (phase / controlled phase)
+    t_lin: float = 1.116e-12          # ... per merged phase-polynomial op (a run of >= 4 single-control phases)
+    t_rel: float = 2.192e-13               # ... per amplitude per shared-memory relayout of a gate pass
     rho: float = 0                  # gate passes: fraction of min(memory, compute) hidden by overlap
     bw_nvlink: float = 900e9       # per direction, NVLink 5 (nominal)
-    bw_copy: float = 6.351e+12        # device-local copy (emulated exchange), bytes moved / s
+    bw_copy: float = 6.36e+12        # device-local copy (emulated exchange), bytes moved / s
     t_lat: float = 15e-6           # one NCCL collective
     t_launch: float = 2e-6         # per kernel launch gap
 
@@ -230,6 +231,18 @@ def _is_phase1(g) -> bool:
     return _is_diag(g) and m[0] == 1.0 and m[1] == 0.0 and bin(int(g["controls"])).count("1") <= 1
 
 
+def gate_op_mix(st: dict, order, gates) -> dict:
+    """A gate pass's ops split into merged phase runs, diagonal and general
+    ops (the diagonal share taken over the pass's gates that are not
+    single-control phases, as the host merges them)."""
+    idx = order[st["first"]:st["first"] + st["count"]]
+    rest = [gates[int(j)] for j in idx if not _is_phase1(gates[int(j)])] or [gates[int(j)] for j in idx]
+    fd = sum(1 for g in rest if _is_diag(g)) / len(rest) if rest else 0.0
+    lin = st.get("lin_ops", 0)
+    other = st["ops"] - lin
+    return {"lin": lin, "diag": other * fd, "gen": other * (1.0 - fd)}
+
+
 def gate_pass_time(t_mem: float, t_ops: float, rho: float) -> float:
     return t_mem + t_ops - rho * min(t_mem, t_ops)
 
@@ -237,29 +250,27 @@ def gate_pass_time(t_mem: float, t_ops: float, rho: float) -> float:
 def predict_gates(n: int, world: int, dtype: int, gates, prm: B200Params, emulated: bool = False) -> dict:
     """sv_apply_gates: each pass costs its HBM round trip t_mem plus its
     on-chip work t_ops = ops x pairs x t_op(kind) -- Eq. 4's l s^(n_b - 1) t_op
-    next to the memory term -- less the part the two co-resident CTAs per SM
-    overlap: t_mem + t_ops - rho min(t_mem, t_ops), rho calibrated on one
-    balanced pass; swaps as in predict_wht (unfused all-to-all)."""
+    next to the memory term -- plus its shared-memory relayouts (count from
+    sv_debug_gate_relayouts) x amplitudes x t_rel, less the part the two
+    co-resident CTAs per SM overlap: t_mem + t_ops - rho min(t_mem, t_ops)
+    (rho = 0 as calibrated); swaps as in predict_wht (unfused all-to-all)."""
     from . import _sv as sv
 
     steps, order = sv.sv_plan_gates(n, world, dtype, gates)
+    rel = sv.sv_debug_gate_relayouts(n, world, dtype, gates)
     eb = ELEM_BYTES[dtype]
     N_l = (1 << n) / (1 if emulated else world)
     S_l = N_l * eb
     t_pass = t_swap = 0.0
     npass = nswap = 0
-    for st in steps:
+    for i, st in enumerate(steps):
         if st["kind"] == 1:
             t_swap += _swap_time(S_l, world, prm, emulated)
             nswap += 1
             continue
-        idx = order[st["first"]:st["first"] + st["count"]]
-        # merged phase runs cost t_lin each; the other ops split over the
-        # diagonal / general shapes of the gates that are not single-control phases
-        rest = [gates[int(j)] for j in idx if not _is_phase1(gates[int(j)])] or [gates[int(j)] for j in idx]
-        fd = sum(1 for g in rest if _is_diag(g)) / len(rest)
-        lin = st.get("lin_ops", 0)
-        t_ops = (lin * prm.t_lin + (st["ops"] - lin) * (fd * prm.t_diag + (1.0 - fd) * prm.t_gate)) * (N_l / 2.0)
+        f = gate_op_mix(st, order, gates)
+        t_ops = (f["lin"] * prm.t_lin + f["diag"] * prm.t_diag + f["gen"] * prm.t_gate) * (N_l / 2.0)
+        t_ops += float(rel[i]) * N_l * prm.t_rel
         if st["kind"] == 0:
             t_mem = 2.0 * S_l / prm.bw(pass_class(st["tile_mask"], False))
             t_pass += gate_pass_time(t_mem, t_ops, prm.rho) + prm.t_launch

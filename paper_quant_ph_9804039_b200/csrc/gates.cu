@@ -827,6 +827,32 @@ uint64_t build_gate_ops(sv_dtype dt, const GatePassArgs &a, bool whole, std::vec
     return append_ops(ops, prog);
 }
 
+template <typename R>
+static uint64_t relayouts_of(const std::vector<GOp<R>> &ops) {
+    uint64_t r = 0;
+    unsigned int cur = 0;
+    for (size_t k = 0; k < ops.size(); ++k) {  // as the kernel's op loop walks the program
+        const unsigned int ph = ops[k].ph & 0xffu, kind = ops[k].ph >> 8;
+        if (ph != cur) {
+            ++r;
+            cur = ph;
+        }
+        if (kind == GK_LINPHASE) k += ops[k].tm;  // its entry records
+    }
+    return r;
+}
+
+uint64_t count_gate_relayouts(sv_dtype dt, const GatePassArgs &a) {
+    if (dt == SV_C64) {
+        std::vector<GOp<float>> ops;
+        build_tile_ops<Layout<float2, kGateTileBitsC64, kRegBitsC64>, float>(a, ops);
+        return relayouts_of(ops);
+    }
+    std::vector<GOp<double>> ops;
+    build_tile_ops<Layout<double2, kTileBitsC128, kRegBitsC128>, double>(a, ops);
+    return relayouts_of(ops);
+}
+
 void launch_gate_pass(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, const void *host_ops, uint64_t nops,
                       bool has_lin, cudaStream_t s) {
     if (dt == SV_C64) launch_tile_gates<float2, kGateTileBitsC64, kRegBitsC64>(a, dev_ops, host_ops, nops, has_lin, s);

@@ -1145,6 +1145,34 @@ sv_status sv_plan_gates(int n, int world, sv_dtype dtype, const sv_gate *gates, 
     });
 }
 
+sv_status sv_debug_gate_relayouts(int n, int world, sv_dtype dtype, const sv_gate *gates, uint64_t count,
+                                  uint64_t *out, int cap, int *nsteps) {
+    return guarded([&] {
+        SV_CHECK(world >= 1 && (world & (world - 1)) == 0, SV_EINVAL, "world must be a power of two");
+        int g = 0;
+        while ((1 << g) < world) ++g;
+        SV_CHECK(g <= n, SV_EINVAL, "world larger than 2^n");
+        const GatePlan gp = plan_gates(n, g, dtype, gates, count);
+        if (nsteps) *nsteps = (int)gp.steps.size();
+        for (int i = 0; i < (int)gp.steps.size() && i < cap && out; ++i) {
+            const GateStep &st = gp.steps[i];
+            out[i] = 0;
+            if (st.kind != GSTEP_PASS) continue;
+            GatePassArgs a;  // rank 0's program (controls on rank bits decided as on rank 0)
+            a.tile_mask = st.tile;
+            a.total_bits = gp.nl;
+            a.g = gp.g;
+            a.swapped = st.swapped;
+            a.n = gp.n;
+            a.nl = gp.nl;
+            a.gates = gates;
+            a.order = gp.order.data() + st.first;
+            a.count = st.count;
+            out[i] = count_gate_relayouts(dtype, a);
+        }
+    });
+}
+
 sv_status sv_profile(sv_ctx *c, int enable) {
     return guarded([&] {
         check_ctx(c);

@@ -190,6 +190,9 @@ struct GatePassArgs {
 // phase runs (launched with the kernel instantiation that handles them).
 uint64_t build_gate_ops(sv_dtype dt, const GatePassArgs &a, bool whole, std::vector<unsigned char> &prog,
                         bool *has_lin);
+// Shared-memory relayouts the tile kernel performs on one pass's program
+// (host only; layout changes between consecutive ops).
+uint64_t count_gate_relayouts(sv_dtype dt, const GatePassArgs &a);
 // dev_ops: the pass's records in device memory; host_ops: the same records on
 // the host (NULL = none) -- a program that fits the kernel-parameter space is
 // passed by value (constant bank) instead.

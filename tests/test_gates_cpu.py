@@ -111,3 +111,28 @@ def test_reserved_field_must_be_zero():
 def test_empty_circuit():
     steps, order = sv.sv_plan_gates(20, 2, sv.SV_C64, C.circuit([]))
     assert steps == [] and order.size == 0
+
+
+def test_relayout_counts_follow_the_plan():
+    """sv_debug_gate_relayouts: one count per schedule step, 0 for swaps; a
+    pass whose gates all target one register layout needs none; a pass
+    touching all 13 tile qubits of complex64 with general gates needs the
+    layouts A, B and C (>= 2 changes)."""
+    n = 20
+    one = C.circuit([C.record(12, C.H), C.record(11, C.H)])
+    steps, _ = sv.sv_plan_gates(n, 1, sv.SV_C64, one)
+    rel = sv.sv_debug_gate_relayouts(n, 1, sv.SV_C64, one)
+    assert len(rel) == len(steps) == 1 and rel[0] <= 1
+    layer = C.circuit([C.record(q, C.H) for q in range(13)] + [C.record(q, C.X) for q in range(13)])
+    rel = sv.sv_debug_gate_relayouts(n, 1, sv.SV_C64, layer)
+    assert rel[0] >= 2
+    g = C.random_circuit(n, 60, 4, max_controls=1)
+    for world in (1, 4):
+        steps, _ = sv.sv_plan_gates(n, world, sv.SV_C64, g)
+        rel = sv.sv_debug_gate_relayouts(n, world, sv.SV_C64, g)
+        assert len(rel) == len(steps)
+        for st, r in zip(steps, rel):
+            if st["kind"] != 0:
+                assert r == 0
+            else:
+                assert r <= st["ops"]

@@ -84,27 +84,34 @@ def calibrate(n=30, class_sizes=(30, 33)):
              "t_diag": C.circuit([C.record(3 + (i % 10), C.phase(0.1 * i + 0.05), [i % 3, 13 + i % 5])
                                   for i in range(300)]),
              "t_lin": C.circuit(lin_runs * 4)}
-    # overlap: one balanced pass (8 singly-controlled general 2x2 on tile
-    # qubits; compute ~ memory), solved jointly with the heavy passes
+    # a balanced pass (8 singly-controlled general 2x2; compute ~ memory) and a
+    # layout-hopping one (unitaries on the 10 tile qubits separated by
+    # controlled phases, many relayouts)
     balanced = C.circuit([C.record(3 + 2 * (i % 5), C.random_unitary(np.random.default_rng(40 + i)), [4 + 2 * (i % 4)])
                           for i in range(8)])
-    obs = {}
-    for attr, gates in list(heavy.items()) + [("rho", balanced)]:
+    rng = np.random.default_rng(77)
+    hop = []
+    for r in range(12):
+        hop += [C.record(q, C.random_unitary(rng)) for q in range(3, 13)]
+        hop += [C.record(q + 3, C.phase(0.2 + 0.1 * q + 0.01 * r), [q]) for q in range(3, 10)]
+    extra = {"balanced": balanced, "hop": C.circuit(hop)}
+    # t_pass - t_mem = pairs x (n_gen t_gate + n_diag t_diag + n_lin t_lin) + N x relayouts x t_rel,
+    # solved by non-negative least squares over the five calibration passes
+    rows, rhs = [], []
+    for name, gates in list(heavy.items()) + list(extra.items()):
         with sv.sv_init(ng, 1, sv.SV_C64, sv.SV_INIT_GAUSSIAN) as c:
             tot, _ = profiled(c, lambda: sv.sv_apply_gates(c, gates))
-        steps, _ = sv.sv_plan_gates(ng, 1, sv.SV_C64, gates)
+        steps, order = sv.sv_plan_gates(ng, 1, sv.SV_C64, gates)
         assert len(steps) == 1
-        ops = steps[0]["lin_ops"] if attr == "t_lin" else steps[0]["ops"]
-        obs[attr] = (tot / 1e3, ops)
-    pairs = 1 << (ng - 1)
+        rel = int(sv.sv_debug_gate_relayouts(ng, 1, sv.SV_C64, gates)[0])
+        f = CM.gate_op_mix(steps[0], order, gates)
+        rows.append([f["gen"] * (1 << (ng - 1)), f["diag"] * (1 << (ng - 1)), f["lin"] * (1 << (ng - 1)),
+                     rel * float(1 << ng)])
+        rhs.append(max(tot / 1e3 - t_mem, 0.0))
+    from scipy.optimize import nnls
+    sol, _ = nnls(np.array(rows), np.array(rhs))
+    prm.t_gate, prm.t_diag, prm.t_lin, prm.t_rel = (float(x) for x in sol)
     prm.rho = 0.0
-    for _ in range(20):  # heavy passes: t_ops > t_mem, so t = (1 - rho) t_mem + t_ops
-        for attr in heavy:
-            t, ops = obs[attr]
-            setattr(prm, attr, max(t - (1.0 - prm.rho) * t_mem, 0.0) / (ops * pairs))
-        t, ops = obs["rho"]
-        t_ops = ops * pairs * prm.t_gate
-        prm.rho = float(min(max((t_mem + t_ops - t) / max(min(t_mem, t_ops), 1e-12), 0.0), 1.0))
     # emulated exchange copy bandwidth (unfused mode: device-local chunk copies)
     ne = 28
     with sv.sv_init(ne, 1, sv.SV_C64, sv.SV_INIT_UNIFORM, world=2) as c:
@@ -170,7 +177,7 @@ def main():
             CM.predict_wht(30, P, 0, 4, prm, emulated=True, fused_exchange=False)["t"])
     rel = [abs(r["relative_difference"]) for r in rows]
     out = {"calibration": {"n": 30, "pass_class_sizes": [30, 33], "dtype": "c64", "bw_pass": prm.bw_pass, "bw_mean": prm.bw_mean,
-                           "bw_reduce": prm.bw_reduce, "t_gate": prm.t_gate, "t_diag": prm.t_diag, "t_lin": prm.t_lin, "rho": prm.rho, "bw_copy": prm.bw_copy,
+                           "bw_reduce": prm.bw_reduce, "t_gate": prm.t_gate, "t_diag": prm.t_diag, "t_lin": prm.t_lin, "t_rel": prm.t_rel, "rho": prm.rho, "bw_copy": prm.bw_copy,
                            "t_launch": prm.t_launch, "bw_nvlink_nominal": prm.bw_nvlink, "t_lat_assumed": prm.t_lat},
            "paper_terms": {"t_op_per_pair_per_pass_s": prm.as_machine_params(0).t_op2, "t_t": 0.0,
                            "t_b_s_per_byte": 1.0 / prm.bw_nvlink, "t_lr": 0.0},
