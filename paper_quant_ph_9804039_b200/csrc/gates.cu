@@ -269,6 +269,15 @@ __device__ __forceinline__ void apply_linphase(E (&x)[L::NR], const GOp<R> *ent,
     E F;
     F.x = (R)1;
     F.y = (R)0;
+    if constexpr (!GLB) {
+        // program in the constant bank: lane-varying entry indices would
+        // serialise the constant cache, so every lane walks the entries with
+        // uniform loads and multiplies them in entry order (identical in all lanes)
+        for (unsigned int e = RB + nthr; e < cnt; ++e) {
+            const unsigned int w = ldop<GLB>(&ent[e].ri), bit = ldop<GLB>(&ent[e].jm);
+            if (w == LP_CONST || ((base >> bit) & 1ull)) cmul_by(F, ldop<GLB>(&ent[e].m[0]), ldop<GLB>(&ent[e].m[1]));
+        }
+    } else {
     for (unsigned int e = RB + nthr + lane; e < cnt; e += 32u) {
         const unsigned int w = ldop<GLB>(&ent[e].ri), bit = ldop<GLB>(&ent[e].jm);
         if (w == LP_CONST || ((base >> bit) & 1ull)) cmul_by(F, ldop<GLB>(&ent[e].m[0]), ldop<GLB>(&ent[e].m[1]));
@@ -283,6 +292,7 @@ __device__ __forceinline__ void apply_linphase(E (&x)[L::NR], const GOp<R> *ent,
         }
         F.x = __shfl_sync(0xffffffffu, F.x, 0);
         F.y = __shfl_sync(0xffffffffu, F.y, 0);
+    }
     }
     if (tcls == LP_THR && !((et >> tbit) & 1u)) return;  // target bit 0 for all of this thread's amplitudes
     E P[RB];
