@@ -133,16 +133,16 @@ class B200Params:
     round-1 measurements, profiles/r1_costmodel_b200.json)."""
     # achieved HBM bytes/s (2 S_l per pass) per pass class; "default" covers
     # classes not calibrated
-    bw_pass: dict = dataclasses.field(default_factory=lambda: dict({'run4': 6378000000000.0, 'run13': 7011000000000.0, 'run5_far_fused': 6409000000000.0, 'run4_fused': 6336000000000.0, 'run3_far': 3020000000000.0, 'run3_fused': 5104000000000.0, 'run3_far_fused': 3016000000000.0, 'default': 4905000000000.0}))
-    bw_mean: float = 6.178e+12        # fused flip + invert-about-mean pass (2 S_l)
-    bw_reduce: float = 6.771e+12      # read-only sum pass (S_l)
-    t_gate: float = 4.935e-13          # seconds per amplitude pair per general 2x2 op (compute term)
+    bw_pass: dict = dataclasses.field(default_factory=lambda: dict({'run4': 6377000000000.0, 'run13': 7010000000000.0, 'run5_far_fused': 6405000000000.0, 'run4_fused': 6337000000000.0, 'run3_far': 3020000000000.0, 'run3_fused': 5104000000000.0, 'run3_far_fused': 3016000000000.0, 'default': 4905000000000.0}))
+    bw_mean: float = 5.823e+12        # fused flip + invert-about-mean pass (2 S_l)
+    bw_reduce: float = 4.289e+12      # read-only sum pass (S_l)
+    t_gate: float = 4.934e-13          # seconds per amplitude pair per general 2x2 op (compute term)
     t_diag: float = 1.008e-13          # ... per diagonal op (phase / controlled phase)
-    t_lin: float = 1.116e-12          # ... per merged phase-polynomial op (a run of >= 4 single-control phases)
-    t_rel: float = 2.192e-13               # ... per amplitude per shared-memory relayout of a gate pass
+    t_lin: float = 1.076e-12          # ... per merged phase-polynomial op (a run of >= 4 single-control phases)
+    t_rel: float = 2.196e-13               # ... per amplitude per shared-memory relayout of a gate pass
     rho: float = 0                  # gate passes: fraction of min(memory, compute) hidden by overlap
     bw_nvlink: float = 900e9       # per direction, NVLink 5 (nominal)
-    bw_copy: float = 6.36e+12        # device-local copy (emulated exchange), bytes moved / s
+    bw_copy: float = 6.342e+12        # device-local copy (emulated exchange), bytes moved / s
     t_lat: float = 15e-6           # one NCCL collective
     t_launch: float = 2e-6         # per kernel launch gap
 
