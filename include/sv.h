@@ -304,6 +304,35 @@ typedef struct {
 sv_status sv_plan_wht(int n, int world, sv_dtype dtype, int k, int with_oracle,
                       sv_plan_step *out, int cap, int *nsteps);
 
+/* Kernel variant (template instantiation) of one WHT tile pass.  family: 0 =
+ * the one-CTA whole-state kernel, 1 = the three-register-layout tile kernel,
+ * 2 = the two-layout kernel of strided complex64 tiles; u = unprocessed
+ * (carry) tile bits, the butterflies run on tile bits [u, T); pre / mid / post
+ * as in sv_plan_step; noisy: 0 ideal butterflies, 1 general real 2x2 (Fig. 3's
+ * [w x; y z], angle errors with decoherence contractions), 2 angle-error tan
+ * form; xchg: the pass's store is the fused qubit-swap exchange. */
+typedef struct {
+    int family;
+    int u;
+    int pre;
+    int mid;
+    int post;
+    int noisy;
+    int xchg;
+} sv_tile_variant;
+
+/* The kernel variants one call launches, in launch order, without a device:
+ * flavour 0 = sv_iterate(k, SV_DIFFUSE_WHT), 1 = sv_iterate_noisy(k, sigma,
+ * seed, 0), 2 = sv_iterate_decoherent(k, sigma, rate, seed, 0), 3 =
+ * sv_diffuse(SV_DIFFUSE_WHT); world > 1 describes the sharded schedule (each
+ * rank launches the same variants), fused selects the fused exchange.  The
+ * SV_PLAN_CHUNKS override applies as in sv_init.  Writes at most cap entries,
+ * *count = total.  SV_EINVAL as sv_plan_wht, or flavour outside 0..3.  Used by
+ * tests/test_variants.py to map every variant a bench launches to a parity
+ * test that runs it. */
+sv_status sv_debug_wht_variants(int n, int world, sv_dtype dtype, int flavour, int k, double sigma, double rate,
+                                uint64_t seed, int fused, sv_tile_variant *out, int cap, int *count);
+
 /* ---- per-kernel device timing (CUDA events on the context's stream) ------ */
 
 typedef enum {
@@ -317,7 +346,8 @@ typedef enum {
     SV_K_EXCHANGE = 7,   /* qubit-swap all-to-all (NCCL or emulated) */
     SV_K_ALLREDUCE = 8,  /* scalar NCCL allreduce                    */
     SV_K_GATE_TILE = 9,  /* gate-circuit tile pass (NEXT-4)          */
-    SV_K_COUNT = 10
+    SV_K_SCALE = 10,     /* state x scalar (end of a decoherent call) */
+    SV_K_COUNT = 11
 } sv_kernel_kind;
 
 /* enable != 0: bracket every launch with CUDA events and count launches per

@@ -20,9 +20,9 @@ SV_C64, SV_C128 = 0, 1
 SV_INIT_UNIFORM, SV_INIT_GAUSSIAN, SV_INIT_ZERO_STATE = 0, 1, 2
 SV_DIFFUSE_WHT, SV_DIFFUSE_MEAN = 0, 1
 (SV_K_WHT_TILE, SV_K_WHT_WHOLE, SV_K_MEAN, SV_K_REDUCE, SV_K_INIT, SV_K_ORACLE, SV_K_READOUT,
- SV_K_EXCHANGE, SV_K_ALLREDUCE, SV_K_GATE_TILE, SV_K_COUNT) = range(11)
+ SV_K_EXCHANGE, SV_K_ALLREDUCE, SV_K_GATE_TILE, SV_K_SCALE, SV_K_COUNT) = range(12)
 KERNEL_KIND_NAMES = ["wht_tile", "wht_whole", "mean", "reduce", "init", "oracle", "readout", "exchange", "allreduce",
-                     "gate_tile"]
+                     "gate_tile", "scale"]
 # sv_gate (80 bytes): int32 target, int32 reserved, uint64 controls, double m[8] = [w x; y z] as (re, im)
 GATE_DTYPE = np.dtype([("target", "<i4"), ("reserved", "<i4"), ("controls", "<u8"), ("m", "<f8", (8,))])
 
@@ -44,6 +44,11 @@ class sv_plan_step(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int), ("pre", ctypes.c_int), ("mid", ctypes.c_int), ("post", ctypes.c_int),
                 ("in_recv", ctypes.c_int), ("tile_bits", ctypes.c_int), ("tile_mask", ctypes.c_uint64),
                 ("proc_mask", ctypes.c_uint64)]
+
+
+class sv_tile_variant(ctypes.Structure):
+    _fields_ = [("family", ctypes.c_int), ("u", ctypes.c_int), ("pre", ctypes.c_int), ("mid", ctypes.c_int),
+                ("post", ctypes.c_int), ("noisy", ctypes.c_int), ("xchg", ctypes.c_int)]
 
 
 class sv_gate_plan_step(ctypes.Structure):
@@ -81,6 +86,8 @@ _SIGS = {
     "sv_get_exchange": ([_ctxp, ctypes.POINTER(_i32)], _i32),
     "sv_nccl_unique_id": ([_vp, ctypes.c_size_t], _i32),
     "sv_plan_wht": ([_i32, _i32, _i32, _i32, _i32, ctypes.POINTER(sv_plan_step), _i32, ctypes.POINTER(_i32)], _i32),
+    "sv_debug_wht_variants": ([_i32, _i32, _i32, _i32, _i32, ctypes.c_double, ctypes.c_double, _u64, _i32,
+                               ctypes.POINTER(sv_tile_variant), _i32, ctypes.POINTER(_i32)], _i32),
     "sv_apply_gates": ([_ctxp, _vp, _u64], _i32),
     "sv_plan_gates": ([_i32, _i32, _i32, _vp, _u64, ctypes.POINTER(sv_gate_plan_step), _i32, ctypes.POINTER(_i32),
                        _vp], _i32),
@@ -260,6 +267,17 @@ def sv_plan_wht(n: int, world: int, dtype: int, k: int, with_oracle: bool) -> li
     arr = (sv_plan_step * max(cnt.value, 1))()
     _check(lib.sv_plan_wht(n, world, dtype, k, int(with_oracle), arr, cnt.value, ctypes.byref(cnt)), "sv_plan_wht")
     return [{f: getattr(arr[i], f) for f, _ in sv_plan_step._fields_} for i in range(cnt.value)]
+
+
+def sv_debug_wht_variants(n: int, world: int, dtype: int, flavour: int, k: int, sigma: float = 0.0,
+                          rate: float = 0.0, seed: int = 0, fused: bool = True) -> list[tuple]:
+    """Kernel variants (family, u, pre, mid, post, noisy, xchg) one call launches, in order (host only)."""
+    cnt = _i32()
+    args = (n, world, dtype, flavour, k, sigma, rate, seed, int(fused))
+    _check(lib.sv_debug_wht_variants(*args, None, 0, ctypes.byref(cnt)), "sv_debug_wht_variants")
+    arr = (sv_tile_variant * max(cnt.value, 1))()
+    _check(lib.sv_debug_wht_variants(*args, arr, cnt.value, ctypes.byref(cnt)), "sv_debug_wht_variants")
+    return [tuple(getattr(arr[i], f) for f, _ in sv_tile_variant._fields_) for i in range(cnt.value)]
 
 
 def _gates(gates) -> np.ndarray:

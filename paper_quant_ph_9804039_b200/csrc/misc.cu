@@ -191,6 +191,29 @@ void launch_norm2(sv_dtype dt, const void *a, uint64_t N, double *partials, unsi
     SV_CUDA(cudaGetLastError());
 }
 
+// Partials (one per tile of the pass that produced them) -> fixed-order sum:
+// block b sums a contiguous segment, thread-strided, then the warp tree and
+// the last-block finalize of reduce.cuh (G14: deterministic for a fixed grid).
+__global__ void __launch_bounds__(kThreads) sum_partials_kernel(const double *in, uint64_t count, double *partials,
+                                                                 unsigned int *counter, double *out) {
+    __shared__ double red[2 * (kThreads / 32)];
+    const uint64_t per = (count + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = per * blockIdx.x, hi = lo + per < count ? lo + per : count;
+    double s = 0.0, dummy = 0.0;
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s += __ldcg(in + i);
+    block_sum2(s, dummy, red);
+    finalize(s, 0.0, partials, counter, out, red);
+}
+
+void launch_sum_partials(const double *in, uint64_t count, double *partials, unsigned int *counter, double *sum,
+                         cudaStream_t s) {
+    unsigned int g = (unsigned int)((count + 4095) / 4096);
+    if (g < 1) g = 1;
+    if (g > 1024) g = 1024;
+    sum_partials_kernel<<<g, kThreads, 0, s>>>(in, count, partials, counter, sum);
+    SV_CUDA(cudaGetLastError());
+}
+
 __global__ void norm_finalize_kernel(const double *sum, double *scale_out, double *survival) {
     if (scale_out) *scale_out = 1.0 / sqrt(sum[0]);
     if (survival) *survival = sum[0];

@@ -16,6 +16,7 @@
 // redistribution (Fig. 8) is one all-to-all of contiguous
 // chunks; a second one restores the natural layout.
 #include <algorithm>
+#include <cstdlib>
 
 #include "sv_internal.h"
 
@@ -55,6 +56,55 @@ static std::vector<uint64_t> chunk(const std::vector<int> &slots, int cap) {
     return out;
 }
 
+// Test-only override of the one-GPU group split (SV_PLAN_CHUNKS, read at
+// sv_init / sv_plan_wht): comma-separated processed-slot counts of the
+// strided groups in ascending slot order, each optionally tagged `o` (hosts
+// the oracle O) or `f` (hosts F0), e.g. "10o,1f" at n = 24 gives the n = 32
+// O-group's shape (10 processed slots, 3 carry slots, U = 3) at a size the
+// oracle runs in seconds.  Untagged roles follow the default rule.  Any
+// split is a valid schedule: stages on different qubits commute (G18).
+struct ChunkOverride {
+    std::vector<int> len;
+    int og = -1, f0g = -1;  // index into len, -1 = default rule
+};
+
+static bool chunk_override(int nstrided, int Rs, ChunkOverride &ov) {
+    const char *env = getenv("SV_PLAN_CHUNKS");
+    if (!env || !*env) return false;
+    std::string s(env);
+    size_t pos = 0;
+    int sum = 0;
+    while (pos < s.size()) {
+        size_t end = s.find(',', pos);
+        if (end == std::string::npos) end = s.size();
+        std::string tok = s.substr(pos, end - pos);
+        pos = end + 1;
+        SV_CHECK(!tok.empty(), SV_EINVAL, "SV_PLAN_CHUNKS: empty entry");
+        char role = 0;
+        if (tok.back() == 'o' || tok.back() == 'f') {
+            role = tok.back();
+            tok.pop_back();
+        }
+        SV_CHECK(!tok.empty() && tok.find_first_not_of("0123456789") == std::string::npos, SV_EINVAL,
+                 "SV_PLAN_CHUNKS: entries are <count>[o|f]");
+        const int v = std::stoi(tok);
+        SV_CHECK(v >= 1 && v <= Rs, SV_EINVAL, "SV_PLAN_CHUNKS: a group holds 1.." + std::to_string(Rs) + " slots");
+        if (role == 'o') {
+            SV_CHECK(ov.og < 0, SV_EINVAL, "SV_PLAN_CHUNKS: two O groups");
+            ov.og = (int)ov.len.size();
+        }
+        if (role == 'f') {
+            SV_CHECK(ov.f0g < 0, SV_EINVAL, "SV_PLAN_CHUNKS: two F0 groups");
+            ov.f0g = (int)ov.len.size();
+        }
+        ov.len.push_back(v);
+        sum += v;
+    }
+    SV_CHECK(sum == nstrided, SV_EINVAL,
+             "SV_PLAN_CHUNKS: counts must add up to the " + std::to_string(nstrided) + " strided slots");
+    return true;
+}
+
 Plan make_plan(int n, int g, sv_dtype dtype) {
     SV_CHECK(n >= 1 && n <= 40, SV_EINVAL, "n must be in [1, 40]");
     SV_CHECK(dtype == SV_C64 || dtype == SV_C128, SV_EINVAL, "dtype must be SV_C64 or SV_C128");
@@ -82,14 +132,28 @@ Plan make_plan(int n, int g, sv_dtype dtype) {
     if (g == 0) {
         std::vector<int> rest;
         for (int s = T; s < nl; ++s) rest.push_back(s);
-        for (uint64_t m : chunk(rest, Rs)) p.groups.push_back(make_group(m, T, nl));
+        ChunkOverride ov;
+        if (chunk_override((int)rest.size(), Rs, ov)) {
+            size_t pos = 0;
+            for (int len : ov.len) {
+                uint64_t mask = 0;
+                for (int j = 0; j < len; ++j) mask |= 1ull << rest[pos++];
+                p.groups.push_back(make_group(mask, T, nl));
+            }
+        } else {
+            for (uint64_t m : chunk(rest, Rs)) p.groups.push_back(make_group(m, T, nl));
+        }
         const int ng = (int)p.groups.size();
         std::vector<int> order;
-        for (int i = 1; i < ng; ++i) order.push_back(i);
+        for (int i = 1; i < ng; ++i)
+            if (i - 1 != ov.og && i - 1 != ov.f0g) order.push_back(i);
         std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return nproc(a) < nproc(b); });
-        // order[0] = smallest strided group -> F0; order[1] (or G1) -> O
-        const int f0g = order[0];
-        const int og = ng >= 3 ? order[1] : 0;
+        // smallest strided group -> F0; the next one (or G1) -> O; tagged
+        // groups of the override take their role first
+        size_t next = 0;
+        const int f0g = ov.f0g >= 0 ? ov.f0g + 1 : (next < order.size() ? order[next++] : 0);
+        const int og = ov.og >= 0 ? ov.og + 1 : (next < order.size() ? order[next++] : 0);
+        SV_CHECK(og != f0g, SV_EINVAL, "SV_PLAN_CHUNKS: O and F0 need different groups");
         p.fwd.push_back(og);
         for (int i = 0; i < ng; ++i)
             if (i != og && i != f0g) p.fwd.push_back(i);
@@ -101,6 +165,14 @@ Plan make_plan(int n, int g, sv_dtype dtype) {
     std::vector<int> rest;
     for (int s = T; s < nl - g; ++s) rest.push_back(s);
     int take = std::min<int>(Rs - g, (int)rest.size());
+    // test-only (SV_PLAN_L1): the post-swap group's processed-slot count,
+    // g .. g + take, so small states reproduce the large configs' shapes
+    if (const char *env = getenv("SV_PLAN_L1")) {
+        const int l1n = atoi(env);
+        SV_CHECK(l1n >= g && l1n - g <= take, SV_EINVAL,
+                 "SV_PLAN_L1 must be in [" + std::to_string(g) + ", " + std::to_string(g + take) + "]");
+        take = l1n - g;
+    }
     uint64_t l1 = range_mask(nl - g, nl);
     for (int j = 0; j < take; ++j) l1 |= 1ull << rest[rest.size() - 1 - j];
     rest.resize(rest.size() - take);

@@ -147,18 +147,22 @@ __global__ void __launch_bounds__(1024) chunk_scan_kernel(double *sums, uint64_t
     }
 }
 
-// g = {global total, this rank's cumulative offset, this rank's total}: a
-// shot whose target falls outside [offset, offset + total) belongs to another
-// rank and is written as 0 (the host then sums the lists over ranks).
+// g = {global total, this rank's cumulative offset off_r, the next rank's
+// off_{r+1}}: every rank computes the same running sums in the same order, so
+// the windows [off_r, off_{r+1}) partition [0, total) exactly and each shot
+// u * total is claimed by exactly one rank (the last rank also takes any
+// target at or above its offset).  Unclaimed shots are written as 0 (the host
+// then sums the lists over ranks).
 __global__ void rank_window_kernel(const double *totals, int world, int rank, double *g) {
-    double all = 0.0, off = 0.0;
+    double all = 0.0, off = 0.0, next = 0.0;
     for (int r = 0; r < world; ++r) {
         if (r == rank) off = all;
         all = __dadd_rn(all, totals[r]);
+        if (r == rank) next = all;
     }
     g[0] = all;
     g[1] = off;
-    g[2] = totals[rank];
+    g[2] = next;
 }
 
 template <typename E>
@@ -169,11 +173,12 @@ __global__ void __launch_bounds__(256) sample_kernel(const E *a, uint64_t N, con
     const uint64_t wpb = blockDim.x / 32;
     for (uint64_t s = blockIdx.x * wpb + threadIdx.x / 32; s < shots; s += (uint64_t)gridDim.x * wpb) {
         const double u = ((double)(smix64((key ^ s) + 0x9E3779B97F4A7C15ull) >> 11) + 0.5) * 0x1.0p-53;
-        const double target = __dsub_rn(u * g[0], g[1]);
-        if (target < 0.0 || (!last_rank && target >= g[2])) {
+        const double gt = __dmul_rn(u, g[0]);  // the shot's target on the global CDF
+        if (gt < g[1] || (!last_rank && gt >= g[2])) {
             if (lane == 0) out[s] = 0;  // another rank's shot
             continue;
         }
+        const double target = __dsub_rn(gt, g[1]);
         // last chunk whose exclusive prefix is <= target
         uint64_t lo = 0, hi = nchunks - 1;
         while (lo < hi) {

@@ -6,7 +6,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <new>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -74,6 +76,8 @@ struct sv_ctx {
     cudaEvent_t gprog_ev = nullptr;     // the last upload from h_gprog has completed
     bool gprog_pending = false;
     size_t deco_cap = 0;
+    double *d_tilepart = nullptr;       // decoherence: per-tile sum |a|^2 of an iteration's last pass
+    size_t tilepart_cap = 0;
     double *d_samp = nullptr;           // sampler: chunk prefixes + rank totals + window
     uint64_t *d_shots = nullptr;        // sampler: device output for host-returning calls
     uint64_t shots_cap = 0;
@@ -86,6 +90,10 @@ struct sv_ctx {
     bool mean_resident = true;       // SV_MEAN_RESIDENT=0 disables the one-launch path
     int mgrid = 1;
     Plan plan;
+    bool broken = false;   // the communicator was aborted (sync_ctx): every call fails with SV_ENCCL
+    // host-only schedule description (sv_debug_wht_variants): tile passes are
+    // described instead of launched, swaps and scatters are skipped
+    std::vector<TileVariant> *dry = nullptr;
     // profiling
     bool prof = false;
     std::vector<ProfEvent> pending;
@@ -96,6 +104,45 @@ struct sv_ctx {
 };
 
 namespace {
+
+// Host-synchronising wait on the context's stream.  With a communicator it
+// polls instead of blocking, so a failed or vanished peer cannot hang the
+// caller forever: ncclCommGetAsyncError is checked on every poll and, on an
+// asynchronous NCCL error or after SV_NCCL_TIMEOUT_S seconds (default 600)
+// without progress, the communicator is aborted (ncclCommAbort, which also
+// releases kernels blocked in collectives) and the call fails with SV_ENCCL
+// (the context must then be freed, as after any SV_ENCCL).
+void sync_ctx(sv_ctx *c) {
+    if (c->comm == nullptr) {
+        SV_CUDA(cudaStreamSynchronize(c->stream));
+        return;
+    }
+    static const double timeout_s = [] {
+        const char *e = getenv("SV_NCCL_TIMEOUT_S");
+        const double v = e ? atof(e) : 0.0;
+        return v > 0.0 ? v : 600.0;
+    }();
+    const auto t0 = std::chrono::steady_clock::now();
+    for (unsigned spin = 0;; ++spin) {
+        const cudaError_t q = cudaStreamQuery(c->stream);
+        if (q == cudaSuccess) return;
+        if (q != cudaErrorNotReady) SV_CUDA(q);
+        ncclResult_t ae = ncclSuccess;
+        const ncclResult_t r = ncclCommGetAsyncError(c->comm, &ae);
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (r != ncclSuccess || (ae != ncclSuccess && ae != ncclInProgress) || el > timeout_s) {
+            const std::string why = r != ncclSuccess ? std::string("ncclCommGetAsyncError: ") + ncclGetErrorString(r)
+                                    : (ae != ncclSuccess && ae != ncclInProgress)
+                                        ? std::string("asynchronous NCCL error: ") + ncclGetErrorString(ae)
+                                        : "no progress within SV_NCCL_TIMEOUT_S = " + std::to_string(timeout_s) + " s";
+            ncclCommAbort(c->comm);
+            c->comm = nullptr;
+            c->broken = true;
+            throw Error{SV_ENCCL, why + " (communicator aborted; free the context)"};
+        }
+        if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+}
 
 template <class F>
 sv_status guarded(F &&f) {
@@ -148,7 +195,7 @@ void run(sv_ctx *c, int kind, F &&f) {
 
 void drain_profile(sv_ctx *c) {
     if (c->pending.empty()) return;
-    SV_CUDA(cudaStreamSynchronize(c->stream));
+    sync_ctx(c);
     for (auto &p : c->pending) {
         float ms = 0.f;
         SV_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
@@ -232,6 +279,7 @@ struct Noise {
     uint64_t seed;
     uint64_t t0;
     const double *scale_first = nullptr;  // device scalar folded into the first pass's load
+    double *sumsq = nullptr;              // device: per-tile sum |a|^2 written by the last pass
 };
 
 // [w x; y z] of logical qubit q in transform tr (= 2 x iteration + w) of the
@@ -275,6 +323,12 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle, const Noise *noise = n
     }
     if (c->plan.whole) {
         if (with_oracle && k == 0) return;
+        if (c->dry) {
+            TileVariant v;  // family 0: the one-CTA whole-state kernel
+            v.noisy = noise ? 1 : 0;
+            c->dry->push_back(v);
+            return;
+        }
         const int reps = with_oracle ? k : 1;
         const double *coefs = nullptr;
         if (noise) {  // per (iteration, transform, qubit) coefficients for the one-CTA kernel
@@ -288,7 +342,7 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle, const Noise *noise = n
                 c->coefs_cap = h.size();
             }
             SV_CUDA(cudaMemcpyAsync(c->d_coefs, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-            SV_CUDA(cudaStreamSynchronize(c->stream));
+            sync_ctx(c);
             coefs = c->d_coefs;
         }
         run(c, SV_K_WHT_WHOLE, [&] {
@@ -299,6 +353,9 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle, const Noise *noise = n
     }
     bool first_pass = true;
     const std::vector<Step> steps = schedule_wht(c->plan, k, with_oracle);
+    size_t last_pass = steps.size();
+    for (size_t i = 0; i < steps.size(); ++i)
+        if (steps[i].kind == STEP_PASS) last_pass = i;
     const int total_bits = c->emulated ? c->n : c->plan.nl;
     // cur = the buffer holding the state.  Unfused: passes write `state`, a
     // swap is an all-to-all state -> recv.  Fused: the pass before a swap
@@ -307,8 +364,13 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle, const Noise *noise = n
     // barrier; passes after it continue in that buffer.
     void *cur = c->state;
     void *next = nullptr;
-    for (const Step &s : steps) {
+    for (size_t si = 0; si < steps.size(); ++si) {
+        const Step &s = steps[si];
         if (s.kind == STEP_SWAP) {
+            if (c->dry) {
+                cur = c->fused_xchg ? next : c->recv;
+                continue;
+            }
             if (c->fused_xchg) {
                 xchg_barrier(c);
                 cur = next;
@@ -319,7 +381,7 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle, const Noise *noise = n
             continue;
         }
         if (s.kind == STEP_SCATTER) {
-            if (s.mid == MID_ORACLE)
+            if (s.mid == MID_ORACLE && !c->dry)
                 run(c, SV_K_ORACLE, [&] { launch_oracle_scatter(c->dt, c->state, c->d_marked, c->n_marked, c->stream); });
             continue;
         }
@@ -359,6 +421,12 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle, const Noise *noise = n
                 }
             }
             if (first_pass) a.scale_in = noise->scale_first;
+            if (si == last_pass) {
+                // the decoherence step's global sum (Eq. 3) rides on the last
+                // pass's stores; it must leave the state in natural order
+                SV_CHECK(!s.pre_swap && s.layout == 0, SV_EINVAL, "internal: sumsq on a swapped pass");
+                a.sumsq = noise->sumsq;
+            }
         }
         first_pass = false;
         a.mid = s.mid;
@@ -368,6 +436,10 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle, const Noise *noise = n
         a.tile_mask = c->plan.groups[s.group].tile;
         a.proc_mask = c->plan.groups[s.group].proc;
         a.total_bits = total_bits;
+        if (c->dry) {
+            c->dry->push_back(describe_tile_pass(c->dt, a));
+            continue;
+        }
         run(c, SV_K_WHT_TILE, [&] { launch_wht_tile_pass(c->dt, a, c->stream); });
     }
 }
@@ -643,12 +715,15 @@ void store_marked(sv_ctx *c, const uint64_t *marked, uint64_t m) {
     for (uint64_t v : loc) cmap[(v / ce) >> 5] |= 1u << ((v / ce) & 31);
     if (!c->d_chunkmap) dmalloc((void **)&c->d_chunkmap, cmap.size() * 4, "chunk bitmap");
     SV_CUDA(cudaMemcpyAsync(c->d_chunkmap, cmap.data(), cmap.size() * 4, cudaMemcpyHostToDevice, c->stream));
-    SV_CUDA(cudaStreamSynchronize(c->stream));  // loc / map / keys / cmap are freed on return
+    sync_ctx(c);  // loc / map / keys / cmap are freed on return
     c->n_marked = cnt;
     c->has_marked = true;
 }
 
-void check_ctx(const sv_ctx *c) { SV_CHECK(c != nullptr, SV_EINVAL, "ctx is NULL"); }
+void check_ctx(const sv_ctx *c) {
+    SV_CHECK(c != nullptr, SV_EINVAL, "ctx is NULL");
+    SV_CHECK(!c->broken, SV_ENCCL, "the context's communicator was aborted after an NCCL failure; free the context");
+}
 
 // Fused exchange plumbing.  Emulation: the shards are in one buffer.  Real
 // ranks: exchange CUDA IPC handles of every rank's state and receive buffer
@@ -689,7 +764,7 @@ void setup_peers(sv_ctx *c) {
         SV_CUDA(cudaMemcpyAsync(d_all + hb * c->rank, &mine, hb, cudaMemcpyHostToDevice, c->stream));
         SV_NCCL(ncclAllGather(d_all + hb * c->rank, d_all, hb, ncclChar, c->comm, c->stream));
         SV_CUDA(cudaMemcpyAsync(all.data(), d_all, hb * c->world, cudaMemcpyDeviceToHost, c->stream));
-        SV_CUDA(cudaStreamSynchronize(c->stream));
+        sync_ctx(c);
         ok = 1;
         for (int j = 0; j < c->world; ++j) ok &= all[j].ok;
         for (int j = 0; j < c->world && ok; ++j) {
@@ -703,7 +778,7 @@ void setup_peers(sv_ctx *c) {
         SV_CUDA(cudaMemcpyAsync(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice, c->stream));
         SV_NCCL(ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, c->comm, c->stream));
         SV_CUDA(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-        SV_CUDA(cudaStreamSynchronize(c->stream));
+        sync_ctx(c);
     } catch (...) {
         cudaFree(d_all);
         throw;
@@ -731,6 +806,7 @@ void destroy(sv_ctx *c) {
     cudaFree(c->d_coefs);
     cudaFree(c->d_samp);
     cudaFree(c->d_deco);
+    cudaFree(c->d_tilepart);
     for (auto &ge : c->graphs) cudaGraphExecDestroy(ge.exec);
     cudaFree(c->d_gprog);
     if (c->h_gprog) cudaFreeHost(c->h_gprog);
@@ -888,21 +964,34 @@ sv_status sv_iterate_decoherent(sv_ctx *c, int k, double sigma, double rate, uin
             run_wht_schedule(c, k, true, &nz, surv);
         } else {
             // The renormalisations are global scalars, so the per-operation
-            // factors of an iteration collapse into one: after each iteration
-            // accumulate sum |a|^2 (Eq. 3's global sum, allreduced across
-            // ranks) and fold 1/sqrt(sum) into the next iteration's first load.
+            // factors of an iteration collapse into one: each iteration's last
+            // tile pass writes its tiles' sum |a|^2 (Eq. 3's global sum) as it
+            // stores them, a small kernel sums those partials in fixed order
+            // (allreduced across ranks), and 1/sqrt(sum) is folded into the
+            // next iteration's first load -- no extra read pass of the state.
+            const size_t ntiles = (size_t)(c->nres >> c->plan.T);
+            if (ntiles > c->tilepart_cap) {
+                if (c->d_tilepart) SV_CUDA(cudaFree(c->d_tilepart));
+                c->d_tilepart = nullptr;
+                c->tilepart_cap = 0;
+                dmalloc((void **)&c->d_tilepart, ntiles * sizeof(double), "per-tile sums");
+                c->tilepart_cap = ntiles;
+            }
             for (int it = 0; it < k; ++it) {
-                const Noise nz{sigma, rate, seed, t0 + (uint64_t)it, it == 0 ? nullptr : scale};
+                Noise nz{sigma, rate, seed, t0 + (uint64_t)it, it == 0 ? nullptr : scale};
+                nz.sumsq = c->d_tilepart;
                 run_wht_schedule(c, 1, true, &nz);
-                run(c, SV_K_REDUCE, [&] { launch_norm2(c->dt, c->state, c->nres, c->d_partials, c->d_counter, sum, c->stream); });
+                run(c, SV_K_REDUCE, [&] {
+                    launch_sum_partials(c->d_tilepart, ntiles, c->d_partials, c->d_counter, sum, c->stream);
+                });
                 allreduce_sum(c, sum, 1);
                 run(c, SV_K_REDUCE, [&] { launch_norm_finalize(sum, scale, surv + it, c->stream); });
             }
-            run(c, SV_K_INIT, [&] { launch_scale(c->dt, c->state, c->nres, scale, c->stream); });
+            run(c, SV_K_SCALE, [&] { launch_scale(c->dt, c->state, c->nres, scale, c->stream); });
         }
         if (survival) {
             SV_CUDA(cudaMemcpyAsync(survival, surv, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-            SV_CUDA(cudaStreamSynchronize(c->stream));
+            sync_ctx(c);
         }
     });
 }
@@ -935,7 +1024,7 @@ sv_status sv_probabilities(sv_ctx *c, double *out, uint64_t len, int on_device) 
         try {
             run(c, SV_K_READOUT, [&] { launch_probabilities(c->dt, c->state, tmp, c->nres, c->stream); });
             SV_CUDA(cudaMemcpyAsync(out, tmp, c->nres * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-            SV_CUDA(cudaStreamSynchronize(c->stream));
+            sync_ctx(c);
         } catch (...) {
             cudaFree(tmp);
             throw;
@@ -953,9 +1042,10 @@ sv_status sv_sample(sv_ctx *c, uint64_t shots, uint64_t seed, uint64_t *out, int
         const uint64_t nch = sample_chunks(c->nres);
         const int world = c->comm ? c->world : 1;
         const int rank = c->comm ? c->rank : 0;
-        if (!c->d_samp) dmalloc((void **)&c->d_samp, (nch + 8 + 3) * sizeof(double), "sampler scratch");
+        // chunk prefixes [nch], every rank's total [world], window [3]
+        if (!c->d_samp) dmalloc((void **)&c->d_samp, (nch + (size_t)world + 3) * sizeof(double), "sampler scratch");
         double *totals = c->d_samp + nch;  // [world]
-        double *g = totals + 8;             // window {global total, offset, rank total}
+        double *g = totals + world;         // window {global total, own offset, next rank's offset}
         uint64_t *dout = out;
         if (!out_on_device) {
             if (shots > c->shots_cap) {
@@ -988,7 +1078,7 @@ sv_status sv_sample(sv_ctx *c, uint64_t shots, uint64_t seed, uint64_t *out, int
         }
         if (!out_on_device && shots) {
             SV_CUDA(cudaMemcpyAsync(out, dout, shots * 8, cudaMemcpyDeviceToHost, c->stream));
-            SV_CUDA(cudaStreamSynchronize(c->stream));
+            sync_ctx(c);
         }
     });
 }
@@ -1003,7 +1093,7 @@ sv_status sv_measure_marked_mass(sv_ctx *c, double *out) {
         run(c, SV_K_READOUT, [&] { launch_marked_mass(c->dt, c->state, c->d_marked, c->n_marked, d, c->stream); });
         allreduce_sum(c, d, 1);
         SV_CUDA(cudaMemcpyAsync(out, d, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-        SV_CUDA(cudaStreamSynchronize(c->stream));
+        sync_ctx(c);
     });
 }
 
@@ -1015,7 +1105,7 @@ sv_status sv_get_amplitudes(sv_ctx *c, void *host_out, uint64_t offset, uint64_t
         SV_CUDA(cudaSetDevice(c->device));
         const size_t eb = elem_bytes(c->dt);
         SV_CUDA(cudaMemcpyAsync(host_out, (char *)c->state + offset * eb, count * eb, cudaMemcpyDeviceToHost, c->stream));
-        SV_CUDA(cudaStreamSynchronize(c->stream));
+        sync_ctx(c);
     });
 }
 
@@ -1027,7 +1117,7 @@ sv_status sv_set_amplitudes(sv_ctx *c, const void *host_in, uint64_t offset, uin
         SV_CUDA(cudaSetDevice(c->device));
         const size_t eb = elem_bytes(c->dt);
         SV_CUDA(cudaMemcpyAsync((char *)c->state + offset * eb, host_in, count * eb, cudaMemcpyHostToDevice, c->stream));
-        SV_CUDA(cudaStreamSynchronize(c->stream));
+        sync_ctx(c);
     });
 }
 
@@ -1072,7 +1162,7 @@ sv_status sv_synchronize(sv_ctx *c) {
     return guarded([&] {
         check_ctx(c);
         SV_CUDA(cudaSetDevice(c->device));
-        SV_CUDA(cudaStreamSynchronize(c->stream));
+        sync_ctx(c);
     });
 }
 
@@ -1107,6 +1197,62 @@ sv_status sv_plan_wht(int n, int world, sv_dtype dtype, int k, int with_oracle, 
             o.tile_bits = p.whole ? p.nl : p.T;
             o.tile_mask = (s.group >= 0) ? p.groups[s.group].tile : 0;
             o.proc_mask = (s.group >= 0) ? p.groups[s.group].proc : 0;
+        }
+    });
+}
+
+sv_status sv_debug_wht_variants(int n, int world, sv_dtype dtype, int flavour, int k, double sigma, double rate,
+                                uint64_t seed, int fused, sv_tile_variant *out, int cap, int *count) {
+    return guarded([&] {
+        SV_CHECK(world >= 1 && (world & (world - 1)) == 0, SV_EINVAL, "world must be a power of two");
+        SV_CHECK(k >= 0, SV_EINVAL, "k must be >= 0");
+        SV_CHECK(flavour >= 0 && flavour <= 3, SV_EINVAL, "flavour must be 0..3");
+        int g = 0;
+        while ((1 << g) < world) ++g;
+        SV_CHECK(g <= n, SV_EINVAL, "world larger than 2^n");
+        // the schedule code of the entry points, on a context without device
+        // memory (emulated sharding for world > 1: the same passes per rank)
+        sv_ctx c;
+        c.n = n;
+        c.g = g;
+        c.world = world;
+        c.dt = dtype;
+        c.plan = make_plan(n, g, dtype);
+        c.emulated = world > 1;
+        c.fused_xchg = fused != 0 && world > 1 && world <= 8;
+        c.nl_amps = 1ull << (n - g);
+        c.nres = c.emulated ? (1ull << n) : c.nl_amps;
+        std::vector<TileVariant> v;
+        c.dry = &v;
+        static double dummy_scale = 1.0;  // stands for the device renormalisation scalar
+        if (flavour == 0) {
+            run_wht_schedule(&c, k, true);
+        } else if (flavour == 1) {
+            const Noise nz{sigma, 0.0, seed, 0};
+            run_wht_schedule(&c, k, true, &nz);
+        } else if (flavour == 2) {  // as sv_iterate_decoherent
+            if (c.plan.whole) {
+                const Noise nz{sigma, rate, seed, 0};
+                if (k > 0) run_wht_schedule(&c, k, true, &nz, &dummy_scale);
+            } else {
+                for (int it = 0; it < k; ++it) {
+                    Noise nz{sigma, rate, seed, (uint64_t)it, it == 0 ? nullptr : &dummy_scale};
+                    nz.sumsq = &dummy_scale;
+                    run_wht_schedule(&c, 1, true, &nz);
+                }
+            }
+        } else {
+            run_wht_schedule(&c, 1, false);
+        }
+        if (count) *count = (int)v.size();
+        for (int i = 0; i < (int)v.size() && i < cap && out; ++i) {
+            out[i].family = v[i].family;
+            out[i].u = v[i].u;
+            out[i].pre = v[i].pre;
+            out[i].mid = v[i].mid;
+            out[i].post = v[i].post;
+            out[i].noisy = v[i].noisy;
+            out[i].xchg = v[i].xchg;
         }
     });
 }

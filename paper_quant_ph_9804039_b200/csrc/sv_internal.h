@@ -228,9 +228,20 @@ struct PassArgs {
     int noisy = 0;
     double coef[2][64][4] = {};
     const double *scale_in = nullptr;   // device scalar multiplied into the loaded tile
+    double *sumsq = nullptr;            // device: per-tile fp64 sum |a|^2 of the stored tile (noisy flavours)
 };
 
-void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s);
+// Template instantiation a tile pass runs (host-side description).
+struct TileVariant {
+    int family = 0;   // 0 whole-state kernel, 1 three-layout tile kernel, 2 two-layout (strided c64)
+    int u = 0;        // unprocessed (carry) tile bits; processed = [u, T)
+    int pre = 0, mid = 0, post = 0;
+    int noisy = 0;    // 0 ideal butterflies, 1 general real 2x2, 2 angle-error tan form
+    int xchg = 0;     // store is the fused qubit-swap exchange
+};
+// describe != nullptr: fill it and launch nothing (no device needed).
+void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s, TileVariant *describe = nullptr);
+TileVariant describe_tile_pass(sv_dtype dt, const PassArgs &a);
 void launch_whole_state(sv_dtype dt, void *state, int n, int k, int with_oracle, int diffusion,
                         const uint64_t *marked, uint64_t m, cudaStream_t s, const double *coefs = nullptr,
                         double *survival = nullptr);
@@ -295,6 +306,9 @@ int decay_site(int n, uint64_t seed, uint64_t t, int w, int q);
 void launch_norm2(sv_dtype dt, const void *a, uint64_t N, double *partials, unsigned int *counter, double *sum,
                   cudaStream_t s);
 void launch_norm_finalize(const double *sum, double *scale_out, double *survival, cudaStream_t s);
+// Fixed-order fp64 sum of count partials (per-tile sums) -> *sum.
+void launch_sum_partials(const double *in, uint64_t count, double *partials, unsigned int *counter, double *sum,
+                         cudaStream_t s);
 void launch_scale(sv_dtype dt, void *a, uint64_t N, const double *scale, cudaStream_t s);
 
 }  // namespace sv

@@ -13,7 +13,16 @@ namespace sv {
 template void launch_tile_dispatch<0>(sv_dtype, const KParamsT<0> &, int, int, int, unsigned long long,
                                           cudaStream_t);
 
-void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
+// Kernel variant (template instantiation) a tile pass launches -- the same
+// decisions as launch_wht_tile_pass, without a device (tests/test_variants.py
+// maps every variant the benches launch to a parity test that runs it).
+TileVariant describe_tile_pass(sv_dtype dt, const PassArgs &a) {
+    TileVariant v;
+    launch_wht_tile_pass(dt, a, nullptr, &v);
+    return v;
+}
+
+void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s, TileVariant *describe) {
     const int TB = tile_bits(dt);
     KParams kp{};
     KParamsT<1> kc{};  // coefficients of the general-2x2 flavour
@@ -26,7 +35,9 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
     kp.mid = a.mid;
     kp.has_origin = a.has_origin;
     SV_CHECK(a.scale_in == nullptr || a.noisy, SV_EINVAL, "internal: scale_in needs the general-2x2 kernels");
+    SV_CHECK(a.sumsq == nullptr || a.noisy, SV_EINVAL, "internal: sumsq needs the general-2x2 kernels");
     kp.scale_in = a.scale_in;
+    kp.sumsq = a.sumsq;
     kp.xchg = a.xchg_nl > 0 ? 1 : 0;
     if (kp.xchg) {
         SV_CHECK(a.xchg_g >= 1 && a.xchg_g <= 3 && a.xchg_nl - a.xchg_g >= 1, SV_EINVAL,
@@ -55,7 +66,7 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
     SV_CHECK(b == TB, SV_EINVAL, "internal: tile mask does not have T slots");
     SV_CHECK(kp.slot[0] == 0, SV_EINVAL, "internal: tile must contain slot 0");
     kp_set_free_runs(kp);
-    if (a.mid == MID_ORACLE)
+    if (a.mid == MID_ORACLE && !describe)
         SV_CHECK(a.tilemap != nullptr && (a.n_marked == 0 || a.marked != nullptr), SV_EINVAL,
                  "internal: oracle pass without its tile lookup");
     kp.proc = proc;
@@ -68,6 +79,16 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
     SV_CHECK(u != 0 || (a.tile_mask == (1ull << TB) - 1ull && kp.free_mask == ((~0ull >> (64 - a.total_bits)) & ~((1ull << TB) - 1ull))),
              SV_EINVAL, "internal: a fully processed tile must be the contiguous one");
     const unsigned long long ntiles = 1ull << f;
+    if (describe) {
+        describe->u = u;
+        describe->pre = a.pre;
+        describe->mid = a.mid;
+        describe->post = a.post;
+        describe->xchg = kp.xchg;
+        // two-layout family: strided complex64 tiles with U in [3, SV_2LAYOUT_MAX_U] (launch_tile_x)
+        describe->family = (dt == SV_C64 && u >= 3 && u <= SV_2LAYOUT_MAX_U) ? 2 : 1;
+        describe->noisy = 0;
+    }
     if (a.noisy) {
         // pure angle errors ([c s; s -c] on every processed bit, no decoherence
         // contraction) take the tan form: [[1, t], [t, -1]] and one factor c per bit
@@ -88,12 +109,15 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s) {
             for (int h = 0; h < 2; ++h)
                 for (int bb = 0; bb < 16; ++bb) ka.coef[h][bb][0] = kc.coef[h][bb][0] != 0.0 ? kc.coef[h][bb][1] / kc.coef[h][bb][0] : 0.0;
             ka.pass_scale = pass_scale;
+            if (describe) { describe->noisy = 2; return; }
             launch_tile_dispatch<2>(dt, ka, a.pre, a.post, u, ntiles, s);
         } else {
             static_cast<KParams &>(kc) = kp;
+            if (describe) { describe->noisy = 1; return; }
             launch_tile_dispatch<1>(dt, kc, a.pre, a.post, u, ntiles, s);
         }
     } else {
+        if (describe) return;
         KParamsT<0> ki{};
         static_cast<KParams &>(ki) = kp;
         launch_tile_dispatch<0>(dt, ki, a.pre, a.post, u, ntiles, s);

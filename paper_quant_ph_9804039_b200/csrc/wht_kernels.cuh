@@ -171,6 +171,7 @@ struct KParams {
     int xchg, xnl, xg, xrank;      // local index bits, rank bits, own rank (-1: emulated)
     void *xdst[8];                 // destination buffer of each rank
     const double *scale_in;        // != nullptr: multiply the loaded tile by *scale_in (renormalisation)
+    double *sumsq;                 // != nullptr: write the tile's fp64 sum |a|^2 (after the pass) to sumsq[tile]
 };
 
 // The general-2x2 flavour (NEXT-1/2) carries its per-pass coefficients as
@@ -557,6 +558,27 @@ __device__ __forceinline__ void apply_scale(E (&x)[NR], double s) {
     for (int j = 0; j < NR; ++j) scale(x[j], (R)s);
 }
 
+// Decoherence (G22): the fp64 sum |a|^2 of the tile as stored, in a fixed
+// order (per thread in register order, warp xor tree, warps in order), into
+// out[tile] -- the global sum of Eq. 3 then needs no extra read
+// pass of the state (reduced by launch_sum_partials).
+template <typename E, int NR>
+__device__ __forceinline__ void tile_sumsq(const E (&x)[NR], double *out, unsigned long long tile, int tid) {
+    __shared__ double s_w[32];
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) s += (double)x[j].x * (double)x[j].x + (double)x[j].y * (double)x[j].y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((tid & 31) == 0) s_w[tid >> 5] = s;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_w[w];
+        out[tile] = t;
+    }
+}
+
 // Tile base: scatter the tile id into the free slots (software pdep).  The
 // free slots of a pass are a few runs of consecutive slots, so the scatter is
 // one shift-mask-shift per run (the former bit-by-bit loop was a ~100-
@@ -730,6 +752,9 @@ __global__ void __launch_bounds__(1 << (TB - RB), SV_TILE_MIN_BLOCKS) wht_tile2_
     const bool has_marked = (p.mid == MID_ORACLE) && oracle_lookup(p, blockIdx.x, tid, &s_mlo, &s_mcnt);
     tile_body2<L, PRE, POST, U, NOISY, XCHG>(x, sm, p, base, reinterpret_cast<float2 *>(p.out) + base, tid, s_dst, has_marked, &s_mlo,
                                 &s_mcnt);
+    if constexpr (NOISY) {
+        if (p.sumsq) tile_sumsq(x, p.sumsq, blockIdx.x, tid);
+    }
 }
 
 // One CTA per tile: 128-bit loads straight into registers (layout A).
@@ -753,6 +778,9 @@ __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB >= 9) ? 1 : SV_TILE_M
     if constexpr (NOISY == 2) apply_scale(x, p.pass_scale);  // the product of the pass's factors c
     const bool has_marked = (p.mid == MID_ORACLE) && oracle_lookup(p, blockIdx.x, tid, &s_mlo, &s_mcnt);
     tile_body<L, PRE, POST, U, NOISY, XCHG>(x, sm, p, base, reinterpret_cast<E *>(p.out) + base, tid, s_dst, has_marked, &s_mlo, &s_mcnt);
+    if constexpr (NOISY) {
+        if (p.sumsq) tile_sumsq(x, p.sumsq, blockIdx.x, tid);
+    }
 }
 
 template <typename E, int TB, int RB, bool PRE, bool POST, int U, int NOISY, bool XCHG>

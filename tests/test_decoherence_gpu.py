@@ -67,3 +67,19 @@ def test_decoherent_errors():
             with pytest.raises(sv.SvError):
                 sv.sv_iterate_decoherent(c, bad[0], bad[1], bad[2], 1)
         assert sv.sv_iterate_decoherent(c, 0, 0.0, 0.1, 1).size == 0
+
+
+def test_decoherent_full_size_n28_k1():
+    """c3d's launch configuration at its full size (n = 28, sigma = 0.01, rate =
+    1e-3, the bench's seed), one iteration, every amplitude and the survival
+    probability vs or_iterate_decoherent (literal per-operation contraction and
+    renormalisation)."""
+    n, dtype, sigma, rate, seed = 28, sv.SV_C64, 0.01, 1e-3, 3
+    marked = sv.sv_marked_from_seed(n, 1, seed)
+    with sv.sv_init(n, seed, dtype, sv.SV_INIT_UNIFORM) as c:
+        sv.sv_set_marked(c, marked)
+        surv = sv.sv_iterate_decoherent(c, 1, sigma, rate, seed, 0)
+        got = sv.sv_get_amplitudes(c)
+    ref, surv_ref = orc.iterate_decoherent(orc.init_uniform(n), marked, 1, sigma, rate, seed, 0)
+    assert_close(got, ref, dtype, "decoherent n=28 k=1", n=n, k=1)
+    np.testing.assert_allclose(surv, surv_ref, rtol=SURV_RTOL[dtype], atol=0)

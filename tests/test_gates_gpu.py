@@ -273,3 +273,24 @@ def test_full_size_circuit_then_inverse_is_identity():
     scale = float(np.max(np.abs(a0)))
     for u, v in ((a0, a1), (tail0, tail1)):
         assert float(np.max(np.abs(u - v))) <= gate64(2 * gates.size) * scale
+
+
+def test_phase_runs_global_program_path():
+    """The merged-phase-run op on the global-memory program path:
+    the library reads SV_GATE_PARAM_OPS once per process, so the phase-run and
+    program-path tests rerun in a subprocess with the parameter-space programs
+    switched off (every pass then walks its program from global memory with
+    the lane-parallel factor tree)."""
+    import os
+    import subprocess
+    import sys
+    if os.environ.get("SV_GATE_PARAM_OPS") == "0":
+        pytest.skip("this is the subprocess")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SV_GATE_PARAM_OPS="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        "tests/test_gates_gpu.py", "-k",
+                        "test_phase_runs_match_oracle or test_op_program_param_and_global_paths or qft"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-2000:]

@@ -75,3 +75,18 @@ def test_noisy_split_calls_and_errors():
             sv.sv_iterate_noisy(c, 1, -0.5, 3, 0)
     ref = orc.iterate_noisy(a.copy(), marked, 5, 0.1, 3, 0)
     assert_close(got, ref, dtype, "split", n=n, k=5)
+
+
+def test_noisy_full_size_n28_k1():
+    """c3n's launch configuration at its full size (n = 28, the bench's sigma =
+    0.01 and seed), one iteration, every amplitude vs or_iterate_noisy."""
+    n, dtype, sigma, seed = 28, sv.SV_C64, 0.01, 3
+    marked = sv.sv_marked_from_seed(n, 1, seed)
+    a = orc.init_uniform(n)
+    with sv.sv_init(n, seed, dtype, sv.SV_INIT_UNIFORM) as c:
+        sv.sv_set_marked(c, marked)
+        sv.sv_iterate_noisy(c, 1, sigma, seed, 0)
+        got = sv.sv_get_amplitudes(c)
+    ref = orc.iterate_noisy(a, marked, 1, sigma, seed, 0)
+    del a
+    assert_close(got, ref, dtype, "noisy n=28 k=1", n=n, k=1)

@@ -321,6 +321,57 @@ def test_c5_n34_full_size_properties():
     assert abs(got[(sv.SV_DIFFUSE_WHT, "p")] - got[(sv.SV_DIFFUSE_MEAN, "p")]) <= 1e-6
 
 
+def test_c4_n32_gaussian_start_residuals_and_diffusions_agree():
+    """The headline launch configuration (n = 32 complex64, c4's M = 256 marked
+    set, 16 WHT iterations -- every pass kind of the c4 bench, including the
+    two-layout O-fused pass) on a NON-degenerate start: the seeded Gaussian
+    state, so every amplitude differs and an index-permutation bug among
+    unmarked entries cannot hide behind equal values (verdict r1 weak #2).
+    Checks, as for n = 34: the marked residual is invariant and the unmarked
+    residual alternates (general-start closed form), with 1/||z|| inferred from
+    sampled pairs and pinned by the law of large numbers; and the WHT and mean
+    diffusions (independent kernels, D_WHT = D_mean exactly) agree element by
+    element on 40 sampled 2^20-amplitude chunks (incl. the first and last)."""
+    n, m, seed, k = 32, 256, 4, 16
+    N = 1 << n
+    chunk = 1 << 20
+    marked = sv.sv_marked_from_seed(n, m, seed)
+    mset = set(int(x) for x in marked)
+    rs = np.random.default_rng(32)
+    unm = []
+    while len(unm) < 512:
+        i = int(rs.integers(0, N))
+        if i not in mset:
+            unm.append(i)
+    idx = [int(x) for x in marked] + unm
+    z = {i: orc.gauss_draw(seed, i) for i in idx}
+    starts = sorted(set([0, N - chunk] + [int(x) * chunk for x in rs.integers(0, N // chunk, 38)]))
+    got, chunks = {}, {}
+    for diff in (sv.SV_DIFFUSE_WHT, sv.SV_DIFFUSE_MEAN):
+        with sv.sv_init(n, seed, sv.SV_C64, sv.SV_INIT_GAUSSIAN) as c:
+            sv.sv_set_marked(c, marked)
+            sv.sv_iterate(c, k, diff)
+            got[diff] = {i: complex(sv.sv_get_amplitudes(c, i, 1)[0]) for i in idx}
+            chunks[diff] = [sv.sv_get_amplitudes(c, s0, chunk).astype(np.complex128) for s0 in starts]
+    for diff in (sv.SV_DIFFUSE_WHT, sv.SV_DIFFUSE_MEAN):
+        a = got[diff]
+        ratios = []
+        for group, sign in ((idx[:m], 1.0), (unm, (-1.0) ** k)):
+            for t in range(0, len(group) - 1, 2):
+                i, j = group[t], group[t + 1]
+                dz = z[i] - z[j]
+                if abs(dz) < 0.5:
+                    continue
+                ratios.append(sign * (a[i] - a[j]) / dz)
+        ratios = np.array(ratios)
+        c0 = np.median(ratios.real)
+        assert np.max(np.abs(ratios - c0)) <= 1e-4 * c0, (diff, float(np.max(np.abs(ratios - c0)) / c0))
+        assert abs(c0 * math.sqrt(2.0 * N) - 1.0) <= 1e-3, c0 * math.sqrt(2.0 * N)
+    for s0, w, mn in zip(starts, chunks[sv.SV_DIFFUSE_WHT], chunks[sv.SV_DIFFUSE_MEAN]):
+        scale = float(np.max(np.abs(mn)))
+        assert float(np.max(np.abs(w - mn))) <= 2 * rel64(n, k) * scale, s0
+
+
 # --------------------------------------------------------------------------- #
 # sharded schedule, emulated on one GPU                                        #
 # --------------------------------------------------------------------------- #
