@@ -17,6 +17,7 @@
 // chunks; a second one restores the natural layout.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "sv_internal.h"
 
@@ -133,7 +134,54 @@ Plan make_plan(int n, int g, sv_dtype dtype) {
         std::vector<int> rest;
         for (int s = T; s < nl; ++s) rest.push_back(s);
         ChunkOverride ov;
-        if (chunk_override((int)rest.size(), Rs, ov)) {
+        const bool overridden = chunk_override((int)rest.size(), Rs, ov);
+        // Supertile plan (complex64, one GPU): G1 hosts O (fused, visited once
+        // per iteration), all remaining R = nl - T slots form ONE group run as
+        // an L2-staged supertile pass with F0 -- 2 HBM passes per iteration,
+        // the lower bound (each transform must read and write the state once).
+        // Level A = 11 slots (tiles of 2 carry + 11 processed slots), level B =
+        // the other R - 11 (>= 1).  The supertile (2 + R slots) must leave
+        // room in the 126 MB L2 for the sub-passes in flight: 2 + R <=
+        // SV_SUPER_MAX_BITS (default 21 = 16 MiB).
+        const int R = nl - T;
+        static const int super_max = [] {
+            const char *e = getenv("SV_SUPER_MAX_BITS");
+            return e ? atoi(e) : 21;
+        }();
+        // measured slower than the plain schedule on the B200 (DESIGN.md
+        // "Supertile pass: tried"), so opt-in: SV_SUPER=1
+        const char *se = getenv("SV_SUPER");
+        const bool super_on = se && strcmp(se, "1") == 0;
+        // test-only SV_SUPER_A: level A's slot count (default 11); a small
+        // state then gets a large one's level-B tile (e.g. a = 4 at n = 25:
+        // level B of 8 slots, n = 32's shape)
+        int a = 11;
+        if (const char *e = getenv("SV_SUPER_A")) a = atoi(e);
+        const int cA = T - a, uB = T - (R - a);
+        const bool fits = a >= 1 && a <= 11 && R - a >= 1 && cA + R <= super_max && super_pair_supported(cA, uB);
+        if (getenv("SV_SUPER_A") && super_on && dtype == SV_C64 && !overridden)
+            SV_CHECK(fits, SV_EINVAL, "SV_SUPER_A: no supertile kernel for this level split");
+        if (!overridden && super_on && dtype == SV_C64 && T == 13 && R >= 12 && fits) {
+            p.super = true;
+            SuperSpec &sp = p.sup;
+            sp.procA = range_mask(T, T + a);
+            sp.tileA = range_mask(0, cA) | sp.procA;
+            sp.procB = range_mask(T + a, nl);
+            sp.uB = uB;
+            sp.st = range_mask(0, cA) | range_mask(T, nl);
+            // level B tiles: its processed slots + the lowest uB other supertile slots
+            sp.tileB = sp.procB;
+            for (int sl = 0, have = 0; sl < nl && have < uB; ++sl)
+                if (((sp.st & ~sp.procB) >> sl) & 1) { sp.tileB |= 1ull << sl; ++have; }
+            Group sg;
+            sg.proc = range_mask(T, nl);
+            sg.tile = sp.st;
+            p.groups.push_back(sg);
+            sp.group = 1;
+            p.fwd = {0, 1};  // O on G1, F0 on the supertile group
+            return p;
+        }
+        if (overridden) {
             size_t pos = 0;
             for (int len : ov.len) {
                 uint64_t mask = 0;

@@ -76,6 +76,10 @@ struct sv_ctx {
     cudaEvent_t gprog_ev = nullptr;     // the last upload from h_gprog has completed
     bool gprog_pending = false;
     size_t deco_cap = 0;
+    unsigned int *d_superctr = nullptr;   // supertile pass: ticket + per-(supertile, sub-pass) counters
+    unsigned int *d_superseg = nullptr;   // supertile pass: segment order
+    uint64_t super_nseg = 0;
+    int super_grid = 0;
     double *d_tilepart = nullptr;       // decoherence: per-tile sum |a|^2 of an iteration's last pass
     size_t tilepart_cap = 0;
     double *d_samp = nullptr;           // sampler: chunk prefixes + rank totals + window
@@ -314,6 +318,86 @@ static void transform_coefs(const Noise &nz, int tr, int n, std::vector<double> 
     }
 }
 
+// The supertile group's visit (always fused with F0, plan.cpp): level A
+// stages of the first transform, level B stages + F0 + level B stages, level A
+// stages of the second transform, as three sub-passes of one persistent launch
+// (wht_super.cu).  tcoef: per-transform coefficients of the noisy flavours.
+void run_super_step(sv_ctx *c, const Step &s, int total_bits, const std::vector<std::vector<double>> *tcoef) {
+    const SuperSpec &sp = c->plan.sup;
+    SV_CHECK(s.pre && s.post && s.mid == MID_F0 && !s.pre_swap && s.layout == 0, SV_EINVAL,
+             "internal: the supertile group is visited only fused with F0");
+    SuperArgs sa;
+    sa.st_mask = sp.st;
+    sa.ua = c->plan.T - __builtin_popcountll(sp.procA);
+    sa.ub = sp.uB;
+    sa.ctr = c->d_superctr;
+    sa.seg = c->d_superseg;
+    sa.nseg = c->super_nseg;
+    sa.grid = c->super_grid;
+    const uint64_t tiles[3] = {sp.tileA, sp.tileB, sp.tileA};
+    const uint64_t procs[3] = {sp.procA, sp.procB, sp.procA};
+    for (int j = 0; j < 3; ++j) {
+        PassArgs &a = sa.sub[j];
+        a.in = c->state;
+        a.out = c->state;
+        a.f0_scale = tcoef ? 1.0 : ldexp(1.0, -c->n);
+        a.has_origin = origin_here(c) ? 1 : 0;
+        a.pre = j < 2 ? 1 : 0;
+        a.post = j > 0 ? 1 : 0;
+        a.mid = j == 1 ? MID_F0 : MID_NONE;
+        a.tile_mask = tiles[j];
+        a.proc_mask = procs[j];
+        a.total_bits = total_bits;
+        if (tcoef) {
+            a.noisy = 1;
+            for (int sl = 0; sl < 64; ++sl) {
+                if (!((procs[j] >> sl) & 1)) continue;
+                for (int e = 0; e < 4; ++e) {  // natural layout: slot = logical qubit (g == 0)
+                    if (a.pre) a.coef[0][sl][e] = (*tcoef)[s.tr_pre][4 * sl + e];
+                    if (a.post) a.coef[1][sl][e] = (*tcoef)[s.tr_post][4 * sl + e];
+                }
+            }
+        }
+    }
+    if (c->dry) {
+        TileVariant v[3];
+        launch_wht_super_pass(c->dt, sa, nullptr, v);
+        for (int j = 0; j < 3; ++j) c->dry->push_back(v[j]);
+        return;
+    }
+    run(c, SV_K_WHT_TILE, [&] { launch_wht_super_pass(c->dt, sa, c->stream); });
+}
+
+// Work order of the supertile kernel: step w runs sub-pass 0 of supertile w,
+// sub-pass 1 of w - L and sub-pass 2 of w - 2L, so a sub-pass starts 3 L
+// segments (3 L x tiles-per-segment items) after the one it depends on --
+// more than the CTAs in flight, so CTAs rarely wait -- and about 2 L + 1
+// supertiles are live in L2.  SV_SUPER_LAG overrides L.
+void setup_super(sv_ctx *c) {
+    if (!c->plan.super) return;
+    const int stb = __builtin_popcountll(c->plan.sup.st);
+    const uint64_t nst = 1ull << (c->plan.nl - stb);
+    const uint64_t tps = 1ull << (stb - c->plan.T);
+    c->super_grid = super_grid();
+    int L = (int)((3 * (uint64_t)c->super_grid + 6 * tps - 1) / (6 * tps));  // ~1.5 x grid / (3 tps)
+    if (const char *e = getenv("SV_SUPER_LAG")) L = atoi(e);
+    if (L < 1) L = 1;
+    std::vector<unsigned int> seg;
+    seg.reserve(3 * nst);
+    for (uint64_t w = 0; w < nst + 2 * (uint64_t)L; ++w)
+        for (int j = 0; j < 3; ++j) {
+            const int64_t st = (int64_t)w - (int64_t)j * L;
+            if (st >= 0 && st < (int64_t)nst) seg.push_back((unsigned int)(st << 2) | (unsigned int)j);
+        }
+    SV_CHECK(seg.size() == 3 * nst && nst < (1ull << 30), SV_EINVAL, "internal: supertile segment table");
+    dmalloc((void **)&c->d_superseg, seg.size() * sizeof(unsigned int), "supertile segments");
+    dmalloc((void **)&c->d_superctr, (3 * nst + 1) * sizeof(unsigned int), "supertile counters");
+    SV_CUDA(cudaMemcpyAsync(c->d_superseg, seg.data(), seg.size() * sizeof(unsigned int), cudaMemcpyHostToDevice,
+                            c->stream));
+    SV_CUDA(cudaStreamSynchronize(c->stream));
+    c->super_nseg = seg.size();
+}
+
 void run_wht_schedule(sv_ctx *c, int k, bool with_oracle, const Noise *noise = nullptr, double *survival = nullptr) {
     std::vector<std::vector<double>> tcoef;  // per transform of the call
     if (noise) {
@@ -383,6 +467,11 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle, const Noise *noise = n
         if (s.kind == STEP_SCATTER) {
             if (s.mid == MID_ORACLE && !c->dry)
                 run(c, SV_K_ORACLE, [&] { launch_oracle_scatter(c->dt, c->state, c->d_marked, c->n_marked, c->stream); });
+            continue;
+        }
+        if (c->plan.super && s.group == c->plan.sup.group) {
+            run_super_step(c, s, total_bits, noise ? &tcoef : nullptr);
+            first_pass = false;
             continue;
         }
         PassArgs a;
@@ -807,6 +896,8 @@ void destroy(sv_ctx *c) {
     cudaFree(c->d_samp);
     cudaFree(c->d_deco);
     cudaFree(c->d_tilepart);
+    cudaFree(c->d_superctr);
+    cudaFree(c->d_superseg);
     for (auto &ge : c->graphs) cudaGraphExecDestroy(ge.exec);
     cudaFree(c->d_gprog);
     if (c->h_gprog) cudaFreeHost(c->h_gprog);
@@ -882,6 +973,7 @@ sv_status sv_init(sv_ctx **out, int n, uint64_t seed, sv_dtype dtype, sv_init_ki
             SV_NCCL(ncclCommInitRank(&c->comm, world, id, c->rank));
         }
         setup_peers(c);
+        setup_super(c);
         do_init(c, seed, init);
         *out = c;
     });
@@ -1194,7 +1286,8 @@ sv_status sv_plan_wht(int n, int world, sv_dtype dtype, int k, int with_oracle, 
             o.mid = s.mid;
             o.post = s.post;
             o.in_recv = s.in_recv;
-            o.tile_bits = p.whole ? p.nl : p.T;
+            o.tile_bits = p.whole ? p.nl
+                          : (p.super && s.group == p.sup.group) ? __builtin_popcountll(p.sup.st) : p.T;
             o.tile_mask = (s.group >= 0) ? p.groups[s.group].tile : 0;
             o.proc_mask = (s.group >= 0) ? p.groups[s.group].proc : 0;
         }

@@ -91,16 +91,36 @@ struct Step {
     int layout = 0;     // 0 = natural; 1 = top-g local slots hold the rank qubits
 };
 
+// L2-staged supertile pass: the F0 group's
+// processed slots plus two carry slots form a supertile of 2^|st| amplitudes
+// that stays in L2 while three dependent sub-passes of ordinary 2^T tiles run
+// over it -- level A's stages (transform 1), level B's stages + F0 + level B's
+// stages, level A's stages (transform 2) -- so the group costs ONE HBM read
+// and write of the state however many slots it has.
+struct SuperSpec {
+    int group = -1;          // index of the supertile group in Plan::groups
+    uint64_t st = 0;         // slots of one supertile (carry slots + the group's processed slots)
+    uint64_t tileA = 0, procA = 0;  // level A sub-passes: tile slots, processed slots
+    uint64_t tileB = 0, procB = 0;  // level B (F0) sub-pass
+    int uB = 0;              // unprocessed tile bits of the level B tiles
+};
+
 struct Plan {
     int nl = 0;       // local index bits (n - g)
     int g = 0;        // rank bits
     int T = 0;        // tile bits
     bool whole = false;
+    bool super = false;      // the F0 group is a supertile group (sup)
+    SuperSpec sup;
     std::vector<Group> groups;   // groups[0] = contiguous slots [0, T)
     // fwd[0] hosts the oracle O (natural layout), fwd.back() hosts F0
     std::vector<int> fwd;        // first transform: group indices, -1 = swap
 };
 
+// (level A, level B) unprocessed tile bits with a supertile kernel instantiation (wht_super.cuh).
+inline bool super_pair_supported(int ua, int ub) {
+    return (ua == 2 && ub >= 5 && ub <= 12) || (ua == 9 && ub == 5);
+}
 // Validates (n, g, dtype) and builds the group structure.  Throws Error.
 Plan make_plan(int n, int g, sv_dtype dtype);
 // Expand an op sequence to fused device steps.
@@ -233,12 +253,28 @@ struct PassArgs {
 
 // Template instantiation a tile pass runs (host-side description).
 struct TileVariant {
-    int family = 0;   // 0 whole-state kernel, 1 three-layout tile kernel, 2 two-layout (strided c64)
+    int family = 0;   // 0 whole-state kernel, 1 three-layout tile kernel, 2 two-layout (strided c64),
+                      // 3 sub-pass of the supertile kernel (three per supertile pass)
     int u = 0;        // unprocessed (carry) tile bits; processed = [u, T)
     int pre = 0, mid = 0, post = 0;
     int noisy = 0;    // 0 ideal butterflies, 1 general real 2x2, 2 angle-error tan form
     int xchg = 0;     // store is the fused qubit-swap exchange
 };
+// One supertile pass (wht_super.cu): the F0 group's three sub-passes over
+// L2-resident supertiles in one persistent launch.
+struct SuperArgs {
+    PassArgs sub[3];               // sub-pass 0: level A pre; 1: level B pre + F0 + post; 2: level A post
+    uint64_t st_mask = 0;          // slots of one supertile
+    int ua = 0, ub = 0;            // unprocessed tile bits of the level A / level B tiles
+    unsigned int *ctr = nullptr;   // device: ticket + per-(supertile, sub-pass) counters (zeroed by the launch)
+    const unsigned int *seg = nullptr;  // device: segment order, (supertile << 2) | sub-pass
+    uint64_t nseg = 0;
+    int grid = 0;                  // persistent CTAs
+};
+// describe != nullptr: fill it and launch nothing (no device needed).
+void launch_wht_super_pass(sv_dtype dt, const SuperArgs &a, cudaStream_t s, TileVariant *describe = nullptr);
+// Persistent CTAs of the supertile kernel (occupancy x SMs; host query).
+int super_grid();
 // describe != nullptr: fill it and launch nothing (no device needed).
 void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s, TileVariant *describe = nullptr);
 TileVariant describe_tile_pass(sv_dtype dt, const PassArgs &a);

@@ -22,10 +22,16 @@ TileVariant describe_tile_pass(sv_dtype dt, const PassArgs &a) {
     return v;
 }
 
-void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s, TileVariant *describe) {
+// Kernel parameters of one tile pass (shared with the supertile pass,
+// wht_super.cu): slot map, free-slot runs, op, exchange, coefficients of the
+// general 2x2 (kc) and tan (ka) flavours.  Returns the stage flavour (0 ideal,
+// 1 general 2x2, 2 tan form) and the unprocessed tile bits in *u.
+int pack_tile_params(sv_dtype dt, const PassArgs &a, bool check_lookup, KParams &kp, KParamsT<1> &kc,
+                     KParamsT<2> &ka, int *u_out, unsigned long long *ntiles) {
     const int TB = tile_bits(dt);
-    KParams kp{};
-    KParamsT<1> kc{};  // coefficients of the general-2x2 flavour
+    kp = KParams{};
+    kc = KParamsT<1>{};
+    ka = KParamsT<2>{};
     kp.in = a.in;
     kp.out = a.out;
     kp.marked = reinterpret_cast<const unsigned long long *>(a.marked);
@@ -66,7 +72,7 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s, TileVa
     SV_CHECK(b == TB, SV_EINVAL, "internal: tile mask does not have T slots");
     SV_CHECK(kp.slot[0] == 0, SV_EINVAL, "internal: tile must contain slot 0");
     kp_set_free_runs(kp);
-    if (a.mid == MID_ORACLE && !describe)
+    if (a.mid == MID_ORACLE && check_lookup)
         SV_CHECK(a.tilemap != nullptr && (a.n_marked == 0 || a.marked != nullptr), SV_EINVAL,
                  "internal: oracle pass without its tile lookup");
     kp.proc = proc;
@@ -78,7 +84,37 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s, TileVa
     // u == 0 kernels assume the contiguous tile (slots [0, T), tile t at t * 2^T)
     SV_CHECK(u != 0 || (a.tile_mask == (1ull << TB) - 1ull && kp.free_mask == ((~0ull >> (64 - a.total_bits)) & ~((1ull << TB) - 1ull))),
              SV_EINVAL, "internal: a fully processed tile must be the contiguous one");
-    const unsigned long long ntiles = 1ull << f;
+    *u_out = u;
+    *ntiles = 1ull << f;
+    if (!a.noisy) return 0;
+    // pure angle errors ([c s; s -c] on every processed bit, no decoherence
+    // contraction) take the tan form: [[1, t], [t, -1]] and one factor c per bit
+    bool tan_form = true;
+    double pass_scale = 1.0;
+    for (int bb = 0; bb < TB && tan_form; ++bb) {
+        if (!((proc >> bb) & 1u)) continue;
+        for (int h = 0; h < 2; ++h) {
+            if ((h == 0 && !a.pre) || (h == 1 && !a.post)) continue;
+            const double *m = kc.coef[h][bb];
+            if (!(m[1] == m[2] && m[3] == -m[0] && fabs(m[0]) > 0.25)) { tan_form = false; break; }
+            pass_scale *= m[0];
+        }
+    }
+    static_cast<KParams &>(kc) = kp;
+    static_cast<KParams &>(ka) = kp;
+    for (int h = 0; h < 2; ++h)
+        for (int bb = 0; bb < 16; ++bb) ka.coef[h][bb][0] = kc.coef[h][bb][0] != 0.0 ? kc.coef[h][bb][1] / kc.coef[h][bb][0] : 0.0;
+    ka.pass_scale = pass_scale;
+    return tan_form ? 2 : 1;
+}
+
+void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s, TileVariant *describe) {
+    KParams kp;
+    KParamsT<1> kc;
+    KParamsT<2> ka;
+    int u = 0;
+    unsigned long long ntiles = 0;
+    const int flavour = pack_tile_params(dt, a, describe == nullptr, kp, kc, ka, &u, &ntiles);
     if (describe) {
         describe->u = u;
         describe->pre = a.pre;
@@ -87,37 +123,14 @@ void launch_wht_tile_pass(sv_dtype dt, const PassArgs &a, cudaStream_t s, TileVa
         describe->xchg = kp.xchg;
         // two-layout family: strided complex64 tiles with U in [3, SV_2LAYOUT_MAX_U] (launch_tile_x)
         describe->family = (dt == SV_C64 && u >= 3 && u <= SV_2LAYOUT_MAX_U) ? 2 : 1;
-        describe->noisy = 0;
+        describe->noisy = flavour;
+        return;
     }
-    if (a.noisy) {
-        // pure angle errors ([c s; s -c] on every processed bit, no decoherence
-        // contraction) take the tan form: [[1, t], [t, -1]] and one factor c per bit
-        bool tan_form = true;
-        double pass_scale = 1.0;
-        for (int bb = 0; bb < TB && tan_form; ++bb) {
-            if (!((proc >> bb) & 1u)) continue;
-            for (int h = 0; h < 2; ++h) {
-                if ((h == 0 && !a.pre) || (h == 1 && !a.post)) continue;
-                const double *m = kc.coef[h][bb];
-                if (!(m[1] == m[2] && m[3] == -m[0] && fabs(m[0]) > 0.25)) { tan_form = false; break; }
-                pass_scale *= m[0];
-            }
-        }
-        if (tan_form) {
-            KParamsT<2> ka{};
-            static_cast<KParams &>(ka) = kp;
-            for (int h = 0; h < 2; ++h)
-                for (int bb = 0; bb < 16; ++bb) ka.coef[h][bb][0] = kc.coef[h][bb][0] != 0.0 ? kc.coef[h][bb][1] / kc.coef[h][bb][0] : 0.0;
-            ka.pass_scale = pass_scale;
-            if (describe) { describe->noisy = 2; return; }
-            launch_tile_dispatch<2>(dt, ka, a.pre, a.post, u, ntiles, s);
-        } else {
-            static_cast<KParams &>(kc) = kp;
-            if (describe) { describe->noisy = 1; return; }
-            launch_tile_dispatch<1>(dt, kc, a.pre, a.post, u, ntiles, s);
-        }
+    if (flavour == 2) {
+        launch_tile_dispatch<2>(dt, ka, a.pre, a.post, u, ntiles, s);
+    } else if (flavour == 1) {
+        launch_tile_dispatch<1>(dt, kc, a.pre, a.post, u, ntiles, s);
     } else {
-        if (describe) return;
         KParamsT<0> ki{};
         static_cast<KParams &>(ki) = kp;
         launch_tile_dispatch<0>(dt, ki, a.pre, a.post, u, ntiles, s);

@@ -652,39 +652,69 @@ __device__ __forceinline__ bool oracle_lookup(const KParams &p, unsigned long lo
     return has;
 }
 
+// Layout PH runs at least one processed stage (tile bits [U, TB)).
+template <class L, int U>
+__host__ __device__ constexpr bool layout_has_work(int ph) {
+    bool w = false;
+    for (int b = U; b < L::kTB; ++b) w = w || L::owns(ph, b);
+    return w;
+}
+
 // Everything after the tile is in registers (layout A): stage sets, the
-// elementwise op, relayouts through `sm`, and the coalesced global store.
+// elementwise op, relayouts through `sm`, and the global store.  Only the
+// layouts that own a processed tile bit are visited (A always does: it holds
+// the top tile bits), so a strided tile whose processed bits all live in A
+// and C skips B and needs one relayout per stage set instead of two (U = 5..8),
+// and one whose processed bits are all A register bits needs none (U >= 9).
 template <class L, bool PRE, bool POST, int U, int NOISY, bool XCHG, typename E>
 __device__ __forceinline__ void tile_body(E (&x)[L::NR], E *sm, const KParamsT<NOISY> &p, unsigned long long base, E *gout,
                                           int tid, E *const *sdst, bool has_marked, const unsigned long long *s_mlo,
                                           const unsigned long long *s_mcnt) {
+    constexpr bool wB = layout_has_work<L, U>(1), wC = layout_has_work<L, U>(2);
+    constexpr int kLast = wC ? 2 : (wB ? 1 : 0);   // last layout of a forward visit
+    constexpr int kMid = wB ? 1 : 0;               // the layout before C
     if (PRE) {
         run_stages<L, 0, U, NOISY, 0>(x, p);
-        relayout<L, 0, 1>(x, sm, tid);
-        run_stages<L, 1, U, NOISY, 0>(x, p);
-        relayout<L, 1, 2>(x, sm, tid);
-        run_stages<L, 2, U, NOISY, 0>(x, p);
-        if (p.mid == MID_F0 || has_marked) mid_op<L, 2>(x, p, base, tid, *s_mlo, *s_mcnt);
+        if constexpr (wB) {
+            relayout<L, 0, 1>(x, sm, tid);
+            run_stages<L, 1, U, NOISY, 0>(x, p);
+        }
+        if constexpr (wC) {
+            relayout<L, kMid, 2>(x, sm, tid);
+            run_stages<L, 2, U, NOISY, 0>(x, p);
+        }
+        if constexpr (kLast == 0) {
+            if (has_marked) __syncthreads();  // s_mlo / s_mcnt (no relayout barrier on this path)
+        }
+        if (p.mid == MID_F0 || has_marked) mid_op<L, kLast>(x, p, base, tid, *s_mlo, *s_mcnt);
         if (POST) {
-            run_stages<L, 2, U, NOISY, 1>(x, p);
-            relayout<L, 2, 1>(x, sm, tid);
-            run_stages<L, 1, U, NOISY, 1>(x, p);
-            relayout<L, 1, 0>(x, sm, tid);
-            run_stages<L, 0, U, NOISY, 1>(x, p);
+            run_stages<L, kLast, U, NOISY, 1>(x, p);
+            if constexpr (wC) {
+                relayout<L, 2, kMid>(x, sm, tid);
+                run_stages<L, kMid, U, NOISY, 1>(x, p);
+            }
+            if constexpr (wB) {
+                relayout<L, 1, 0>(x, sm, tid);
+                run_stages<L, 0, U, NOISY, 1>(x, p);
+            }
             pass_store<L, 0, XCHG, (U == 0)>(x, gout, base, p, tid, sdst);
         } else {
-            pass_store<L, 2, XCHG, (U == 0)>(x, gout, base, p, tid, sdst);
+            pass_store<L, kLast, XCHG, (U == 0)>(x, gout, base, p, tid, sdst);
         }
     } else {
         if (has_marked) __syncthreads();  // s_mlo / s_mcnt (uniform branch)
         if (p.mid == MID_F0 || has_marked) mid_op<L, 0>(x, p, base, tid, *s_mlo, *s_mcnt);
         if (POST) {
             run_stages<L, 0, U, NOISY, 1>(x, p);
-            relayout<L, 0, 1>(x, sm, tid);
-            run_stages<L, 1, U, NOISY, 1>(x, p);
-            relayout<L, 1, 2>(x, sm, tid);
-            run_stages<L, 2, U, NOISY, 1>(x, p);
-            pass_store<L, 2, XCHG, (U == 0)>(x, gout, base, p, tid, sdst);
+            if constexpr (wB) {
+                relayout<L, 0, 1>(x, sm, tid);
+                run_stages<L, 1, U, NOISY, 1>(x, p);
+            }
+            if constexpr (wC) {
+                relayout<L, kMid, 2>(x, sm, tid);
+                run_stages<L, 2, U, NOISY, 1>(x, p);
+            }
+            pass_store<L, kLast, XCHG, (U == 0)>(x, gout, base, p, tid, sdst);
         } else {
             pass_store<L, 0, XCHG, (U == 0)>(x, gout, base, p, tid, sdst);
         }
@@ -825,6 +855,9 @@ static void launch_tile_u(const KParamsT<NOISY> &kp, int pre, int post, int u, u
 }  // namespace sv
 
 namespace sv {
+// wht.cu: kernel parameters of one tile pass (flavour 0/1/2, unprocessed bits, tile count).
+int pack_tile_params(sv_dtype dt, const PassArgs &a, bool check_lookup, KParams &kp, KParamsT<1> &kc,
+                     KParamsT<2> &ka, int *u_out, unsigned long long *ntiles);
 // Both dtypes, one stage flavour (instantiated in wht.cu / wht_noisy.cu).
 template <int NOISY>
 void launch_tile_dispatch(sv_dtype dt, const KParamsT<NOISY> &kp, int pre, int post, int u, unsigned long long ntiles,

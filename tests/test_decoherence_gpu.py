@@ -69,6 +69,7 @@ def test_decoherent_errors():
         assert sv.sv_iterate_decoherent(c, 0, 0.0, 0.1, 1).size == 0
 
 
+
 def test_decoherent_full_size_n28_k1():
     """c3d's launch configuration at its full size (n = 28, sigma = 0.01, rate =
     1e-3, the bench's seed), one iteration, every amplitude and the survival

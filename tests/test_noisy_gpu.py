@@ -77,6 +77,7 @@ def test_noisy_split_calls_and_errors():
     assert_close(got, ref, dtype, "split", n=n, k=5)
 
 
+
 def test_noisy_full_size_n28_k1():
     """c3n's launch configuration at its full size (n = 28, the bench's sigma =
     0.01 and seed), one iteration, every amplitude vs or_iterate_noisy."""

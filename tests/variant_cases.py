@@ -26,6 +26,11 @@ for _fl, _sig, _rate in ((IDEAL, 0.0, 0.0), (NOISY, 0.05, 0.0), (DECOHERENT, 0.0
                       100 + _n, {"SV_PLAN_CHUNKS": _chunks}))
     for _l1 in (10, 2):  # sharded c4 shapes: post-swap group of 10 slots (U=3) / O group of 9 slots (U=4)
         CASES.append((f"fl{_fl}-n24-P2-L1={_l1}", 24, 2, _fl, 2, _sig, _rate, 200 + _l1, {"SV_PLAN_L1": str(_l1)}))
+    # the opt-in supertile pass (SV_SUPER=1, wht_super.cuh; measured slower than the plain
+    # schedule, kept as a correct A/B option): n = 25's plan (level A tiles U=2, level B U=12)
+    # and the test-only level split SV_SUPER_A=4 (level B U=5, n = 32's shape)
+    CASES.append((f"fl{_fl}-n25-super", 25, 1, _fl, 2, _sig, _rate, 300, {"SV_SUPER": "1"}))
+    CASES.append((f"fl{_fl}-n25-super-A4", 25, 1, _fl, 2, _sig, _rate, 301, {"SV_SUPER": "1", "SV_SUPER_A": "4"}))
 
 # the benches' WHT workloads: (config, n, world, flavour, k, sigma, rate, seed) -- bench.py CONFIGS
 BENCH = [
