@@ -58,7 +58,52 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU: start the ranks (gloo), build the sharded schedule, print the launch line")
     return ap.parse_args()
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_spawn(args) -> int:
+    """`bench.py --gpus N` without a torchrun environment: relaunch this command
+    under torch.distributed.run (one rank per GPU, rendezvous on 127.0.0.1)
+    and return its exit code (rank 0 prints the JSON line)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_dry(args):
+    """Launcher check without a GPU: every rank joins the process group (gloo),
+    rank 0's schedule for the config is described host-side, and rank 0 prints
+    which ranks joined (tests/test_bench_cpu.py runs it with --gpus 2)."""
+    import torch.distributed as dist
+
+    import paper_quant_ph_9804039_b200 as sv
+    from paper_quant_ph_9804039_b200 import dist as svd
+
+    rank, world, _ = svd.init_process_group("gloo")
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    n, dts, M, k, diff, seed, init, desc = CONFIGS[args.config]
+    dtype = sv.SV_C64 if dts == "c64" else sv.SV_C128
+    plan = sv.sv_plan_wht(n, world, dtype, k, True)
+    ranks = [None] * world
+    if world > 1:
+        dist.all_gather_object(ranks, rank)
+    else:
+        ranks = [rank]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_joined": ranks, "config": args.config,
+                          "plan_steps": len(plan), "swaps": sum(1 for st in plan if st["kind"] == 1),
+                          "tile_passes": sum(1 for st in plan if st["kind"] == 0)}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def measured_peaks():
@@ -268,6 +313,11 @@ def run_ours(args):
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = svd.sharded_init(n, seed, dtype, ikind, stream=stream.cuda_stream)
+    comm = sv.sv_comm_info(ctx)
+    print(f"[bench] rank {rank}/{world}: libsv NCCL communicator nranks={comm['nranks']} rank={comm['rank']}",
+          file=sys.stderr, flush=True)
+    if world > 1:
+        assert comm["nranks"] == world and comm["rank"] == rank, comm
     marked = sv.sv_marked_from_seed(n, M, seed)
     sv.sv_set_marked(ctx, marked)
 
@@ -409,6 +459,7 @@ def run_ours(args):
                 "clocks": clocks.summary(),
                 "phases_ms": {(nm if nm != "init" else "init_untimed"): v[1] for nm, v in prof.items() if v[0]},
                 "nvlink": nvlink,
+                "nccl": {"nranks": comm["nranks"], "rank0_comm_rank": comm["rank"]},
                 "model": model,
                 "p_success": p_success, "check": check}
         print(json.dumps(line), flush=True)
@@ -419,7 +470,11 @@ def run_ours(args):
 
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_spawn(args))
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

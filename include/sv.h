@@ -194,6 +194,12 @@ sv_status sv_marked_from_seed(int n, uint64_t m, uint64_t seed, uint64_t *out);
 sv_status sv_info(const sv_ctx *ctx, int *n, int *world, int *rank, uint64_t *local_len,
                   sv_dtype *dtype);
 
+/* The context's NCCL communicator as NCCL reports it (ncclCommCount,
+ * ncclCommUserRank): *nranks = 0 and *comm_rank = -1 when the context has
+ * none (one GPU, or single-process emulation).  Lets a launcher verify that
+ * every process joined one communicator of the expected size. */
+sv_status sv_comm_info(const sv_ctx *ctx, int *nranks, int *comm_rank);
+
 /* Qubit-swap exchange mode (P > 1).  fused = 1: the pass before each swap
  * stores every amplitude straight into its new owner's buffer -- peer memory
  * over NVLink mapped with CUDA IPC, or the emulated shard -- and the swap is

@@ -82,6 +82,7 @@ _SIGS = {
     "sv_info": ([_ctxp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                  ctypes.POINTER(_u64), ctypes.POINTER(_i32)], _i32),
     "sv_synchronize": ([_ctxp], _i32),
+    "sv_comm_info": ([_ctxp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)], _i32),
     "sv_set_exchange": ([_ctxp, _i32], _i32),
     "sv_get_exchange": ([_ctxp, ctypes.POINTER(_i32)], _i32),
     "sv_nccl_unique_id": ([_vp, ctypes.c_size_t], _i32),
@@ -249,6 +250,13 @@ def sv_get_exchange(ctx: Ctx) -> bool:
     v = _i32()
     _check(lib.sv_get_exchange(ctx.ptr, ctypes.byref(v)), "sv_get_exchange")
     return bool(v.value)
+
+
+def sv_comm_info(ctx: Ctx) -> dict:
+    """The context's NCCL communicator: {"nranks": 0, "rank": -1} without one."""
+    nr, ur = _i32(), _i32()
+    _check(lib.sv_comm_info(ctx.ptr, ctypes.byref(nr), ctypes.byref(ur)), "sv_comm_info")
+    return {"nranks": nr.value, "rank": ur.value}
 
 
 def sv_synchronize(ctx: Ctx) -> None:

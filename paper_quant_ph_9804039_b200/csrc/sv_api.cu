@@ -1234,6 +1234,19 @@ sv_status sv_info(const sv_ctx *c, int *n, int *world, int *rank, uint64_t *loca
     });
 }
 
+sv_status sv_comm_info(const sv_ctx *c, int *nranks, int *comm_rank) {
+    return guarded([&] {
+        check_ctx(c);
+        int nr = 0, ur = -1;
+        if (c->comm != nullptr) {
+            SV_NCCL(ncclCommCount(c->comm, &nr));
+            SV_NCCL(ncclCommUserRank(c->comm, &ur));
+        }
+        if (nranks) *nranks = nr;
+        if (comm_rank) *comm_rank = ur;
+    });
+}
+
 sv_status sv_set_exchange(sv_ctx *c, int fused) {
     return guarded([&] {
         check_ctx(c);
