@@ -87,3 +87,53 @@ def test_identities():
     # scaling every machine constant by c scales every time by c
     mp2 = {k: (v * 3.0 if k != "q" else v) for k, v in mp.items()}
     assert M.t_pardec(steps, 1, 2, mp2) == pytest.approx(3.0 * M.t_pardec(steps, 1, 2, mp))
+
+
+def test_f15_9bits_t3e_ladder_and_sp2_cross_check():
+    """Table 6 (T3E) f15_9bits at 32 / 64 / 128 processors (P:6269-6280:
+    Calculated 6064 / 3267 / 1893 s) with Table 3's 161 / 363 / 582
+    reorganisations, Table 2's sizes (24 QU-bits,
+    70,904 laser ops, 16 link bits, 8 state bits, so n_b = n_l + 8 in every
+    step) and Table 5's SP2 entry for 4 processors (69977 s,
+    Table 3: 8 reorganisations).
+
+    With n_b - n_l = 8 fixed, Eq. 7 summed over the steps is
+        T_par(n_p) = X (t_t + s^(8 - n_p - 1) t_op) + R(n_p) T_reorg
+    with two unknowns of the unprinted step profile: X = sum l_step s^n_l,step
+    and the mean per-reorganisation cost (Eq. 2 at the steps where they
+    happen).  Fitting both from the 32- and 64-processor rows must predict
+    the 128-processor row, and the SAME X with the SP2 constants must
+    predict the SP2 row -- a cross-machine check of Eq. 4's two terms and of
+    Fig. 9's constants.  The fitted reorganisation cost must be Eq. 2 at an
+    admissible (n_l, n_c): n_p <= n_l <= 16, 1 <= n_c <= n_p, n_b = n_l + 8.
+    Eq. 2 carries <= 3 % of any printed f15_9bits time, so the tables bound
+    it only loosely (G24)."""
+    import numpy as np
+    T3E, SP2 = M.T3E, M.SP2
+    n_s = 8
+    rows = {5: (6064.0, 161), 6: (3267.0, 363), 7: (1893.0, 582)}
+
+    def comp_coef(mp, n_p):  # Eq. 4 per unit of X = l s^n_l (n_b = n_l + n_s, at n_b - n_p): t_t + s^(n_s-n_p-1) t_op
+        return M.t_comp(1, n_s - n_p, 0, 2, mp)
+
+    A = np.array([[comp_coef(T3E, 5), rows[5][1]], [comp_coef(T3E, 6), rows[6][1]]])
+    X, b = np.linalg.solve(A, [rows[5][0], rows[6][0]])
+    assert X > 0 and b > 0
+    pred128 = X * comp_coef(T3E, 7) + rows[7][1] * b
+    assert abs(pred128 - 1893.0) / 1893.0 < 0.02, pred128
+    # reorganisation share of the printed times: small everywhere
+    for n_p, (t, R) in rows.items():
+        assert R * b / t < 0.03
+    # the same step profile on the SP2 (4 processors, 8 reorganisations of
+    # Eq. 2 evaluated at the T3E-fitted block count)
+    blocks = b / (T3E["t_lat"] + T3E["t_b"] * T3E["q"] * 2 ** n_s + T3E["t_lr"])
+    sp2_reorg = blocks * (SP2["t_lat"] + SP2["t_b"] * SP2["q"] * 2 ** n_s + SP2["t_lr"])
+    pred_sp2 = X * comp_coef(SP2, 2) + 8 * sp2_reorg
+    assert abs(pred_sp2 - 69977.0) / 69977.0 < 0.005, pred_sp2
+    # Eq. 2 at an admissible (n_l, n_c) reproduces the fitted per-reorganisation cost
+    best = min(abs(M.t_reorg(n_l, n_l + n_s, n_c, 2, T3E) - b) / b
+               for n_p in (5, 6, 7) for n_l in range(n_p, 17) for n_c in range(1, n_p + 1))
+    assert best < 0.15, best
+    # ... but not at the final structure size: every reorganisation moving
+    # half of 2^16 blocks would add ~1700 s to the 128-processor entry
+    assert X * comp_coef(T3E, 7) + 582 * M.t_reorg(16, 24, 1, 2, T3E) > 1.5 * 1893.0
