@@ -382,6 +382,21 @@ def run_ours(args):
                 "traffic": ncu_traffic(args.config, world), "kernel": f"{kname} ({kdesc})",
                 "algorithmic_bytes_per_launch": algo_bytes, "launches": launches, "avg_launch_ms": 1e3 * avg_s,
                 "share_of_step": kms / max(t_ms, 1e-9), "peak_source": peak_src}
+    if resident:
+        # all k iterations in one launch with the state in shared memory: not an
+        # HBM measurement.  Each iteration reads and writes every amplitude once
+        # in shared memory, then crosses one grid-wide barrier; the bound is the
+        # aggregate shared-memory bandwidth plus that barrier's latency.
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        smem_peak = sms * 128 * 1.965  # GB/s: 128 B/clk per SM at the 1965 MHz max SM clock
+        per_it_us = 1e6 * avg_s / k
+        roofline = {"bound": "smem+barrier", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
+                    "frac": achieved / smem_peak, "traffic": None, "kernel": f"{kname} ({kdesc})",
+                    "algorithmic_bytes_per_launch": algo_bytes, "launches": launches, "avg_launch_ms": 1e3 * avg_s,
+                    "share_of_step": kms / max(t_ms, 1e-9), "us_per_iteration": per_it_us,
+                    "peak_source": (f"aggregate shared-memory bandwidth, {sms} SMs x 128 B/clk x 1.965 GHz; "
+                                    "each iteration also waits on one grid-wide barrier (latency-bound: "
+                                    "us_per_iteration)")}
     if kname == "wht_whole":
         # one CTA on one SM, state in shared memory: the bound is that SM's
         # add rate -- k iterations x 2n stages x N/2 butterflies x 4 real adds
