@@ -189,7 +189,14 @@ Plan make_plan(int n, int g, sv_dtype dtype) {
                 p.groups.push_back(make_group(mask, T, nl));
             }
         } else {
-            for (uint64_t m : chunk(rest, Rs)) p.groups.push_back(make_group(m, T, nl));
+            // one processed slot more per strided group (2 carry slots, 32-B
+            // runs) when that saves a group -- two HBM passes per iteration --
+            // e.g. n = 34: 13 | 10 | 11 instead of 13 | 7 | 7 | 7 (SV_WIDE=1;
+            // measured in DESIGN.md "Wide strided groups")
+            const char *we = getenv("SV_WIDE");
+            const bool wide = we && strcmp(we, "1") == 0 && dtype == SV_C64 &&
+                              chunk(rest, Rs + 1).size() < chunk(rest, Rs).size();
+            for (uint64_t m : chunk(rest, wide ? Rs + 1 : Rs)) p.groups.push_back(make_group(m, T, nl));
         }
         const int ng = (int)p.groups.size();
         std::vector<int> order;
