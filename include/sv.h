@@ -200,6 +200,27 @@ sv_status sv_info(const sv_ctx *ctx, int *n, int *world, int *rank, uint64_t *lo
  * every process joined one communicator of the expected size. */
 sv_status sv_comm_info(const sv_ctx *ctx, int *nranks, int *comm_rank);
 
+/* Adopt a caller-owned device buffer as the state (SURVEY 8(b) phase-2
+ * option): dev_ptr = bytes of interleaved complex amplitudes in the natural
+ * layout (e.g. a torch.complex64 / complex128 CUDA tensor's data_ptr()), on
+ * the context's device, 16-byte aligned, bytes = resident length x element
+ * size.  The library frees its own state buffer, computes in place in
+ * dev_ptr from now on and never frees it -- the caller keeps ownership and
+ * must keep it alive until sv_free.  The buffer's current contents are the
+ * state (no initialisation).  Single-process contexts only (one GPU or
+ * emulation): SV_ESTATE with a communicator (the fused exchange's peer
+ * mappings are made at sv_init).  Errors: SV_EINVAL (NULL, size, alignment,
+ * not device memory of the context's GPU), SV_ESTATE. */
+sv_status sv_attach(sv_ctx *ctx, void *dev_ptr, uint64_t bytes);
+
+/* Debug / oracle snapshot in SPEC's text format: header line
+ * "s=2 M=<n>", then one line per nonzero resident amplitude,
+ * "<global index base-10> <re> <im>" with 17 significant digits, ascending
+ * index.  *written (may be NULL) = amplitude lines.  Synchronises.  Errors:
+ * SV_ETOOBIG above 2^26 resident amplitudes (the host-gather guard),
+ * SV_EINVAL (NULL path, file not writable). */
+sv_status sv_snapshot(sv_ctx *ctx, const char *path, uint64_t *written);
+
 /* Qubit-swap exchange mode (P > 1).  fused = 1: the pass before each swap
  * stores every amplitude straight into its new owner's buffer -- peer memory
  * over NVLink mapped with CUDA IPC, or the emulated shard -- and the swap is

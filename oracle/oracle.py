@@ -325,3 +325,33 @@ def apply_gates_sharded(a: np.ndarray, gates, g_bits: int) -> int:
     if r < 0:
         raise ValueError("invalid gate or g")
     return r
+
+
+def write_snapshot(a: np.ndarray, path: str) -> int:
+    """SPEC's debug/oracle snapshot: header "s=<s> M=<M>" (s = 2 basis
+    states per QU-bit, M = QU-bits), then "<index> <re> <im>" with 17
+    significant digits for every nonzero amplitude in index order.  Plain
+    Python (no C); returns the number of amplitude lines."""
+    n = _nbits(a)
+    lines = 0
+    with open(path, "w") as f:
+        f.write(f"s=2 M={n}\n")
+        for i, v in enumerate(a):
+            if v.real == 0.0 and v.imag == 0.0:
+                continue
+            f.write(f"{i} {float(v.real):.17g} {float(v.imag):.17g}\n")
+            lines += 1
+    return lines
+
+
+def read_snapshot(path: str) -> tuple[int, int, dict]:
+    """(s, M, {index: complex}) of a snapshot file."""
+    with open(path) as f:
+        head = f.readline().split()
+        s = int(head[0].split("=")[1])
+        m = int(head[1].split("=")[1])
+        amps = {}
+        for line in f:
+            i, re, im = line.split()
+            amps[int(i)] = complex(float(re), float(im))
+    return s, m, amps

@@ -83,6 +83,8 @@ _SIGS = {
                  ctypes.POINTER(_u64), ctypes.POINTER(_i32)], _i32),
     "sv_synchronize": ([_ctxp], _i32),
     "sv_comm_info": ([_ctxp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)], _i32),
+    "sv_attach": ([_ctxp, _vp, _u64], _i32),
+    "sv_snapshot": ([_ctxp, ctypes.c_char_p, ctypes.POINTER(_u64)], _i32),
     "sv_set_exchange": ([_ctxp, _i32], _i32),
     "sv_get_exchange": ([_ctxp, ctypes.POINTER(_i32)], _i32),
     "sv_nccl_unique_id": ([_vp, ctypes.c_size_t], _i32),
@@ -257,6 +259,18 @@ def sv_comm_info(ctx: Ctx) -> dict:
     nr, ur = _i32(), _i32()
     _check(lib.sv_comm_info(ctx.ptr, ctypes.byref(nr), ctypes.byref(ur)), "sv_comm_info")
     return {"nranks": nr.value, "rank": ur.value}
+
+
+def sv_attach(ctx: Ctx, dev_ptr: int, nbytes: int) -> None:
+    """Compute in place in a caller-owned device buffer (e.g. tensor.data_ptr()); the caller keeps ownership."""
+    _check(lib.sv_attach(ctx.ptr, dev_ptr, nbytes), "sv_attach")
+
+
+def sv_snapshot(ctx: Ctx, path: str) -> int:
+    """SPEC's text snapshot (header "s=2 M=<n>", "<index> <re> <im>" per nonzero amplitude); returns the line count."""
+    w = _u64()
+    _check(lib.sv_snapshot(ctx.ptr, os.fsencode(path), ctypes.byref(w)), "sv_snapshot")
+    return w.value
 
 
 def sv_synchronize(ctx: Ctx) -> None:

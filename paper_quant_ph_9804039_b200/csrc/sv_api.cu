@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <nccl.h>
+#include <stdio.h>
 #include <string.h>
 
 #include <algorithm>
@@ -11,6 +12,8 @@
 #include <thread>
 #include <string>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3 (CUDA toolkit): ranges for nsys / ncu --nvtx
 
 #include "sv_internal.h"
 
@@ -39,6 +42,7 @@ struct sv_ctx {
     bool own_stream = false;
     ncclComm_t comm = nullptr;
     void *state = nullptr;
+    bool owns_state = true;   // false after sv_attach: the caller owns the buffer
     void *recv = nullptr;
     uint64_t nres = 0;       // resident amplitudes (2^{n-g}; 2^n emulated)
     uint64_t nl_amps = 0;    // amplitudes per rank (2^{n-g})
@@ -175,10 +179,24 @@ void dmalloc(void **p, size_t bytes, const char *what) {
     SV_CUDA(e);
 }
 
+// NVTX range names per kernel kind (sv_kernel_kind order): every enqueued
+// device operation is bracketed by a host-side range, so an nsys timeline or
+// `ncu --nvtx --nvtx-include` can attribute launches to the schedule's phases
+// (tile passes, exchanges, allreduces -- the Fig. 12 split).
+static const char *const kKindName[SV_K_COUNT] = {"sv/wht_tile", "sv/wht_whole", "sv/mean", "sv/reduce",
+                                                  "sv/init", "sv/oracle", "sv/readout", "sv/exchange",
+                                                  "sv/allreduce", "sv/gate_tile", "sv/scale"};
+
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 // Bracket one device operation with events when profiling; count launches.
 template <class F>
 void run(sv_ctx *c, int kind, F &&f) {
     c->launches[kind] += 1;
+    NvtxRange range(kKindName[kind]);
     if (!c->prof) {
         f();
         return;
@@ -904,7 +922,7 @@ void destroy(sv_ctx *c) {
     if (c->gprog_ev) cudaEventDestroy(c->gprog_ev);
     cudaFree(c->d_shots);
     if (c->comm) ncclCommDestroy(c->comm);
-    cudaFree(c->state);
+    if (c->owns_state) cudaFree(c->state);
     cudaFree(c->recv);
     cudaFree(c->d_marked);
     cudaFree(c->d_tilemap);
@@ -1244,6 +1262,74 @@ sv_status sv_comm_info(const sv_ctx *c, int *nranks, int *comm_rank) {
         }
         if (nranks) *nranks = nr;
         if (comm_rank) *comm_rank = ur;
+    });
+}
+
+sv_status sv_attach(sv_ctx *c, void *dev_ptr, uint64_t bytes) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CHECK(dev_ptr != nullptr, SV_EINVAL, "dev_ptr is NULL");
+        SV_CHECK(bytes == c->nres * elem_bytes(c->dt), SV_EINVAL,
+                 "bytes must equal the resident state size (" + std::to_string(c->nres * elem_bytes(c->dt)) + ")");
+        SV_CHECK(((uintptr_t)dev_ptr & 15u) == 0, SV_EINVAL, "dev_ptr must be 16-byte aligned");
+        SV_CHECK(c->comm == nullptr, SV_ESTATE,
+                 "sv_attach is single-process only (peer mappings of the fused exchange are made at sv_init)");
+        SV_CUDA(cudaSetDevice(c->device));
+        cudaPointerAttributes at{};
+        SV_CUDA(cudaPointerGetAttributes(&at, dev_ptr));
+        SV_CHECK(at.type == cudaMemoryTypeDevice && at.device == c->device, SV_EINVAL,
+                 "dev_ptr is not device memory of the context's GPU");
+        sync_ctx(c);  // no pending work on the old buffer
+        if (c->owns_state) SV_CUDA(cudaFree(c->state));
+        c->state = dev_ptr;
+        c->owns_state = false;
+        for (auto &ge : c->graphs) cudaGraphExecDestroy(ge.exec);  // graphs bake the state pointer
+        c->graphs.clear();
+    });
+}
+
+sv_status sv_snapshot(sv_ctx *c, const char *path, uint64_t *written) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CHECK(path != nullptr, SV_EINVAL, "path is NULL");
+        SV_CHECK(c->nres <= (1ull << 26), SV_ETOOBIG, "snapshot above 2^26 resident amplitudes");
+        SV_CUDA(cudaSetDevice(c->device));
+        FILE *f = fopen(path, "w");
+        SV_CHECK(f != nullptr, SV_EINVAL, std::string("cannot open ") + path);
+        uint64_t count = 0;
+        try {
+            const uint64_t base = (!c->emulated && c->world > 1) ? (uint64_t)c->rank * c->nl_amps : 0;
+            fprintf(f, "s=2 M=%d\n", c->n);
+            const size_t eb = elem_bytes(c->dt);
+            constexpr uint64_t kChunk = 1ull << 20;
+            std::vector<unsigned char> buf(kChunk * eb);
+            for (uint64_t off = 0; off < c->nres; off += kChunk) {
+                const uint64_t cnt = std::min<uint64_t>(kChunk, c->nres - off);
+                SV_CUDA(cudaMemcpyAsync(buf.data(), (char *)c->state + off * eb, cnt * eb, cudaMemcpyDeviceToHost,
+                                        c->stream));
+                sync_ctx(c);
+                for (uint64_t i = 0; i < cnt; ++i) {
+                    double re, im;
+                    if (c->dt == SV_C64) {
+                        const float *v = reinterpret_cast<const float *>(buf.data()) + 2 * i;
+                        re = v[0];
+                        im = v[1];
+                    } else {
+                        const double *v = reinterpret_cast<const double *>(buf.data()) + 2 * i;
+                        re = v[0];
+                        im = v[1];
+                    }
+                    if (re == 0.0 && im == 0.0) continue;
+                    fprintf(f, "%llu %.17g %.17g\n", (unsigned long long)(base + off + i), re, im);
+                    ++count;
+                }
+            }
+        } catch (...) {
+            fclose(f);
+            throw;
+        }
+        SV_CHECK(fclose(f) == 0, SV_EINVAL, std::string("write failed: ") + path);
+        if (written) *written = count;
     });
 }
 

@@ -47,6 +47,8 @@ NULL_CTX_CALLS = {
     "sv_get_exchange": lambda: lib.sv_get_exchange(NULL, ctypes.byref(ctypes.c_int())),
     "sv_synchronize": lambda: lib.sv_synchronize(NULL),
     "sv_comm_info": lambda: lib.sv_comm_info(NULL, None, None),
+    "sv_attach": lambda: lib.sv_attach(NULL, NULL, 0),
+    "sv_snapshot": lambda: lib.sv_snapshot(NULL, b"/tmp/x", None),
     "sv_apply_gates": lambda: lib.sv_apply_gates(NULL, NULL, 0),
     "sv_profile": lambda: lib.sv_profile(NULL, 1),
     "sv_profile_read": lambda: lib.sv_profile_read(NULL, 0, None, None),

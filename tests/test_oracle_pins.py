@@ -505,3 +505,15 @@ def test_noisy_unitary_deterministic_and_noise_statistics():
     d = [np.mean([np.linalg.norm(orc.iterate_noisy(a0.copy(), marked, 6, s, sd) - ideal) for sd in range(8)])
          for s in (1e-3, 1e-2, 1e-1)]
     assert d[0] < d[1] < d[2]
+
+
+def test_snapshot_format_fig1(tmp_path):
+    """SPEC's snapshot format (S:140) written by the oracle: Fig. 1(a)'s |0>
+    and Fig. 1(b)'s uniform superposition."""
+    p = tmp_path / "s.txt"
+    assert orc.write_snapshot(orc.init_zero_state(3), str(p)) == 1
+    assert p.read_text() == "s=2 M=3\n0 1 0\n"
+    assert orc.write_snapshot(orc.init_uniform(1), str(p)) == 2
+    assert p.read_text() == "s=2 M=1\n0 0.70710678118654757 0\n1 0.70710678118654757 0\n"
+    s, m, amps = orc.read_snapshot(str(p))
+    assert (s, m) == (2, 1) and amps == {0: 2 ** -0.5, 1: 2 ** -0.5}
