@@ -183,9 +183,9 @@ void dmalloc(void **p, size_t bytes, const char *what) {
 // device operation is bracketed by a host-side range, so an nsys timeline or
 // `ncu --nvtx --nvtx-include` can attribute launches to the schedule's phases
 // (tile passes, exchanges, allreduces -- the Fig. 12 split).
-static const char *const kKindName[SV_K_COUNT] = {"sv/wht_tile", "sv/wht_whole", "sv/mean", "sv/reduce",
-                                                  "sv/init", "sv/oracle", "sv/readout", "sv/exchange",
-                                                  "sv/allreduce", "sv/gate_tile", "sv/scale"};
+static const char *const kKindName[SV_K_COUNT] = {"sv.wht_tile", "sv.wht_whole", "sv.mean", "sv.reduce",
+                                                  "sv.init", "sv.oracle", "sv.readout", "sv.exchange",
+                                                  "sv.allreduce", "sv.gate_tile", "sv.scale"};
 
 struct NvtxRange {
     explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
