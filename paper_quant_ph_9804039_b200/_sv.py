@@ -95,6 +95,7 @@ _SIGS = {
     "sv_plan_gates": ([_i32, _i32, _i32, _vp, _u64, ctypes.POINTER(sv_gate_plan_step), _i32, ctypes.POINTER(_i32),
                        _vp], _i32),
     "sv_debug_gate_relayouts": ([_i32, _i32, _i32, _vp, _u64, _vp, _i32, ctypes.POINTER(_i32)], _i32),
+    "sv_debug_gate_jit": ([_i32, _i32, _vp, _u64, _i32, ctypes.POINTER(_u64), ctypes.POINTER(_u64), _dp], _i32),
     "sv_profile": ([_ctxp, _i32], _i32),
     "sv_profile_read": ([_ctxp, _i32, ctypes.POINTER(_u64), _dp], _i32),
     "sv_profile_timeline": ([_ctxp, _vp, _vp, _u64, ctypes.POINTER(_u64)], _i32),
@@ -335,6 +336,15 @@ def sv_debug_gate_relayouts(n: int, world: int, dtype: int, gates) -> np.ndarray
     _check(lib.sv_debug_gate_relayouts(n, world, dtype, g.ctypes.data if len(g) else None, len(g), out.ctypes.data,
                                        ns.value, ctypes.byref(ns)), "sv_debug_gate_relayouts")
     return out[:ns.value]
+
+
+def sv_debug_gate_jit(n: int = 0, dtype: int = SV_C64, gates=None, compile: bool = False) -> dict:
+    """Gate-engine JIT: compile every pass kernel of a circuit (host only) and/or read the launch-side counters."""
+    g = _gates(gates if gates is not None else np.zeros(0, dtype=GATE_DTYPE))
+    p, c, t = _u64(), _u64(), ctypes.c_double()
+    _check(lib.sv_debug_gate_jit(n, dtype, g.ctypes.data if g.size else None, g.size, int(compile), ctypes.byref(p),
+                                 ctypes.byref(c), ctypes.byref(t)), "sv_debug_gate_jit")
+    return {"passes": p.value, "compiles": c.value, "compile_seconds": t.value}
 
 
 def sv_profile(ctx: Ctx, enable: bool) -> None:

@@ -71,8 +71,9 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
         objs = list(ex.map(lambda s: _compile(s, verbose, objdir, defines), srcs))
     _, libdir = _nccl_dirs()
     if force or not os.path.exists(lib) or os.path.getmtime(lib) < max(os.path.getmtime(o) for o in objs):
+        cuda_lib = os.path.join(os.path.dirname(os.path.dirname(_nvcc())), "lib64")
         cmd = [_nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-L", libdir, "-l:libnccl.so.2",
-               "-Xlinker", f"-rpath,{libdir}"]
+               "-lnvrtc", "-ldl", "-Xlinker", f"-rpath,{libdir}", "-Xlinker", f"-rpath,{cuda_lib}"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../include/sv.h"
+#include "sv_consts.h"
 
 namespace sv {
 
@@ -46,25 +47,7 @@ struct Error {
 // ------------------------------------------------------------------------- //
 // Tile geometry per dtype                       //
 // ------------------------------------------------------------------------- //
-#ifndef SV_TILE_BITS_C64
-#define SV_TILE_BITS_C64 13
-#endif
-constexpr int kTileBitsC64 = SV_TILE_BITS_C64;  // 2^13 x 8 B = 64 KiB smem tile (14: 128 KiB, A/B only)
-constexpr int kRegBitsC64 = 5;     // 32 amplitudes per thread, 256 threads
-constexpr int kTileBitsC128 = 12;  // 2^12 x 16 B = 64 KiB smem tile
-constexpr int kRegBitsC128 = 4;    // 16 amplitudes per thread, 256 threads
-// minimum unprocessed low slots kept in a strided tile: 2^c amplitudes = 64 B
-// contiguous runs (c64: 8 x 8 B, c128: 4 x 16 B)
-constexpr int kCarryC64 = 3;
-constexpr int kCarryC128 = 2;
-
 inline int tile_bits(sv_dtype d) { return d == SV_C64 ? kTileBitsC64 : kTileBitsC128; }
-// gate-circuit tiles (gates.cu) may be smaller than the WHT tiles: more
-// co-resident CTAs hide the compute of many-gate passes behind memory
-#ifndef SV_GATE_TILE_BITS_C64
-#define SV_GATE_TILE_BITS_C64 13
-#endif
-constexpr int kGateTileBitsC64 = SV_GATE_TILE_BITS_C64;
 inline int gate_tile_bits(sv_dtype d) { return d == SV_C64 ? kGateTileBitsC64 : kTileBitsC128; }
 inline int carry_bits(sv_dtype d) { return d == SV_C64 ? kCarryC64 : kCarryC128; }
 inline size_t elem_bytes(sv_dtype d) { return d == SV_C64 ? 8 : 16; }
@@ -73,7 +56,6 @@ inline size_t elem_bytes(sv_dtype d) { return d == SV_C64 ? 8 : 16; }
 // Schedule (plan.cpp)                                                        //
 // ------------------------------------------------------------------------- //
 enum StepKind { STEP_PASS = 0, STEP_SWAP = 1, STEP_WHOLE = 2, STEP_SCATTER = 3 };
-enum MidOp { MID_NONE = 0, MID_ORACLE = 1, MID_F0 = 2 };
 
 struct Group {
     uint64_t proc = 0;   // slots whose butterfly stages run in this pass

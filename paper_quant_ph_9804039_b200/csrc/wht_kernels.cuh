@@ -24,9 +24,13 @@
 //    contiguous tile).  No tensor cores: the path is add/sub only (<= 1.75
 //    FLOP/B), memory-bound.
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 
 #include "sv_internal.h"
+#else
+#include "sv_consts.h"  // runtime-compiled kernels (gate_jit.cpp): device code only
+#endif
 
 #ifndef SV_2LAYOUT_MAX_U
 #define SV_2LAYOUT_MAX_U 4  // strided c64 tiles with U in [3, this] use the two-layout family
@@ -608,6 +612,7 @@ __device__ __forceinline__ unsigned long long tile_base(unsigned long long tile,
     return base;
 }
 
+#ifndef __CUDACC_RTC__
 // Host: the runs of a free-slot mask (<= 8, else nruns = 0).
 inline void kp_set_free_runs(KParams &kp) {
     kp.nruns = 0;
@@ -625,6 +630,7 @@ inline void kp_set_free_runs(KParams &kp) {
     }
     kp.nruns = n;
 }
+#endif
 
 // Oracle tiles: one bitmap word says whether this tile holds a marked index
 // (rare); only then does thread 0 binary-search the sorted keys (tile id << 16
@@ -813,6 +819,7 @@ __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB >= 9) ? 1 : SV_TILE_M
     }
 }
 
+#ifndef __CUDACC_RTC__
 template <typename E, int TB, int RB, bool PRE, bool POST, int U, int NOISY, bool XCHG>
 static void launch_tile_x(const KParamsT<NOISY> &kp, unsigned long long ntiles, cudaStream_t s) {
     using L = Layout<E, TB, RB>;
@@ -852,8 +859,10 @@ static void launch_tile_u(const KParamsT<NOISY> &kp, int pre, int post, int u, u
     }
 }
 
+#endif  // __CUDACC_RTC__ (host launch templates)
 }  // namespace sv
 
+#ifndef __CUDACC_RTC__
 namespace sv {
 // wht.cu: kernel parameters of one tile pass (flavour 0/1/2, unprocessed bits, tile count).
 int pack_tile_params(sv_dtype dt, const PassArgs &a, bool check_lookup, KParams &kp, KParamsT<1> &kc,
@@ -872,3 +881,4 @@ extern template void launch_tile_dispatch<1>(sv_dtype, const KParamsT<1> &, int,
 extern template void launch_tile_dispatch<2>(sv_dtype, const KParamsT<2> &, int, int, int, unsigned long long,
                                               cudaStream_t);
 }  // namespace sv
+#endif  // __CUDACC_RTC__

@@ -65,7 +65,7 @@ def test_null_context_is_einval(name):
 def test_every_context_entry_point_is_covered():
     from tests.test_abi_cpu import declared_functions
     ctx_free = {"sv_init", "sv_marked_from_seed", "sv_nccl_unique_id", "sv_plan_wht", "sv_plan_gates", "sv_free",
-                "sv_debug_gate_relayouts", "sv_debug_wht_variants",
+                "sv_debug_gate_relayouts", "sv_debug_wht_variants", "sv_debug_gate_jit",
                 "sv_last_error", "sv_debug_tile_layout", "sv_debug_tile_owner"}
     assert set(declared_functions()) - ctx_free == set(NULL_CTX_CALLS)
 

@@ -136,3 +136,18 @@ def test_relayout_counts_follow_the_plan():
                 assert r == 0
             else:
                 assert r <= st["ops"]
+
+
+def test_gate_jit_sources_compile_with_nvrtc():
+    """Every pass kernel the gate JIT generates for representative circuits
+    compiles for sm_100a with NVRTC (host only, both program flavours)."""
+    import numpy as np
+    from tests import circuits as C
+    n = 16
+    for gates in (C.qft_circuit(n), C.random_circuit(n, 60, 3, max_controls=3),
+                  C.circuit([C.record(q, C.random_unitary(np.random.default_rng(q))) for q in range(n)])):
+        r = sv.sv_debug_gate_jit(n, sv.SV_C64, gates, True)
+        steps, _ = sv.sv_plan_gates(n, 1, sv.SV_C64, gates)
+        assert r["passes"] == sum(1 for s in steps if s["kind"] == 0) > 0
+    with pytest.raises(sv.SvError):
+        sv.sv_debug_gate_jit(n, sv.SV_C128, C.qft_circuit(n), True)
