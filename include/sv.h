@@ -409,12 +409,13 @@ int sv_debug_tile_owner(int dtype, int phase, int bit);
 sv_status sv_debug_gate_relayouts(int n, int world, sv_dtype dtype, const sv_gate *gates, uint64_t count,
                                   uint64_t *out, int cap, int *nsteps);
 
-/* Gate engine, pass-specialised kernels (gate_jit.cu): with compile != 0,
+/* Gate engine, pass-specialised kernels (gate_jit.cu): with compile == 1,
  * generate and NVRTC-compile (no device needed) the kernel of every tile pass
  * sv_plan_gates gives the circuit on one complex64 GPU, in both program
- * flavours; *passes = passes compiled.  Always: *compiles / *compile_seconds
- * = kernels this process has compiled and loaded for launches so far (any
- * pointer may be NULL).  Errors: SV_EINVAL (gates, dtype), SV_ECUDA (NVRTC
+ * flavours; *passes = passes compiled.  compile == 2: first wait until the
+ * background compiler has drained its queue.  Always: *compiles /
+ * *compile_seconds = specialised kernels this process has loaded for
+ * launches so far / NVRTC seconds spent (any pointer may be NULL).  Errors: SV_EINVAL (gates, dtype), SV_ECUDA (NVRTC
  * failure, with its log in sv_last_error()). */
 sv_status sv_debug_gate_jit(int n, sv_dtype dtype, const sv_gate *gates, uint64_t count, int compile,
                             uint64_t *passes, uint64_t *compiles, double *compile_seconds);

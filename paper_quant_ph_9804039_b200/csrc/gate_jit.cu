@@ -25,13 +25,17 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <chrono>
+#include <condition_variable>
+#include <deque>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gate_kernels.cuh"
@@ -137,15 +141,48 @@ std::string generate(const GOp<float> *ops, uint64_t nops, bool lin, bool glb) {
     return b;
 }
 
-struct Compiled {
+// One cache entry per distinct kernel source.  The automatic mode compiles in
+// the background (one worker thread) and keeps launching the interpreter
+// until the cubin is ready -- tiered, never blocking a call on NVRTC; the
+// library is loaded on the launching thread at first use.
+struct Entry {
+    enum State { QUEUED, READY, FAILED } state = QUEUED;
+    std::vector<char> cubin;
+    std::string err;
     cudaLibrary_t lib = nullptr;
     cudaKernel_t kern = nullptr;
 };
 
-std::mutex g_mu;
-std::map<std::string, Compiled> g_cache;
-uint64_t g_compiles = 0;
-double g_compile_s = 0.0;
+// Process-lifetime state, deliberately never destroyed: the detached worker
+// may still hold it while static destructors run at exit.
+struct JitState {
+    std::mutex mu;
+    std::condition_variable cv;        // worker wake-up / queue drained
+    std::map<std::string, Entry> cache;
+    std::deque<std::string> queue;     // sources waiting for the worker
+    bool busy = false;
+    uint64_t compiles = 0;             // kernels loaded for launches
+    double compile_s = 0.0;            // NVRTC seconds (worker + synchronous)
+};
+JitState &J() {
+    static JitState *j = new JitState;
+    return *j;
+}
+#define g_mu (J().mu)
+#define g_cv (J().cv)
+#define g_cache (J().cache)
+#define g_queue (J().queue)
+#define g_busy (J().busy)
+#define g_compiles (J().compiles)
+#define g_compile_s (J().compile_s)
+
+// At exit: drop queued work and let a running compile finish, so NVRTC is not
+// torn down under the worker.
+void drain_at_exit() {
+    std::unique_lock<std::mutex> lk(g_mu);
+    g_queue.clear();
+    g_cv.wait(lk, [] { return !g_busy; });
+}
 
 std::vector<char> compile_cubin(const std::string &src) {
     nvrtcProgram prog;
@@ -173,25 +210,86 @@ std::vector<char> compile_cubin(const std::string &src) {
     std::vector<char> cubin(cs);
     nvrtcGetCUBIN(prog, cubin.data());
     nvrtcDestroyProgram(&prog);
+    if (const char *dir = getenv("SV_JIT_DUMP")) {  // inspection: source + cubin (cuobjdump -sass)
+        const std::string stem = std::string(dir) + "/sv_gate_jit_" + std::to_string(std::hash<std::string>{}(src));
+        if (FILE *f = fopen((stem + ".cu").c_str(), "w")) {
+            fwrite(src.data(), 1, src.size(), f);
+            fclose(f);
+        }
+        if (FILE *f = fopen((stem + ".cubin").c_str(), "wb")) {
+            fwrite(cubin.data(), 1, cubin.size(), f);
+            fclose(f);
+        }
+    }
     return cubin;
 }
 
-Compiled compile(const std::string &src) {
-    const std::vector<char> cubin = compile_cubin(src);
-    Compiled c;
-    SV_CUDA(cudaLibraryLoadData(&c.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
-    SV_CUDA(cudaLibraryGetKernel(&c.kern, c.lib, "sv_gate_jit"));
-    SV_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void *>(c.kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
+std::vector<char> timed_compile(const std::string &src) {
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<char> cubin = compile_cubin(src);
+    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_compile_s += dt;
+    return cubin;
+}
+
+void worker_main() {
+    std::unique_lock<std::mutex> lk(g_mu);
+    for (;;) {
+        g_cv.wait(lk, [] { return !g_queue.empty(); });
+        const std::string src = g_queue.front();  // (moved out before the lock is released)
+        g_queue.pop_front();
+        g_busy = true;
+        lk.unlock();
+        std::vector<char> cubin;
+        std::string err;
+        try {
+            cubin = timed_compile(src);
+        } catch (const Error &e) {
+            err = e.msg;
+        }
+        lk.lock();
+        Entry &e = g_cache[src];
+        if (err.empty()) {
+            e.cubin.swap(cubin);
+            e.state = Entry::READY;
+        } else {
+            e.err = err;
+            e.state = Entry::FAILED;
+        }
+        g_busy = false;
+        g_cv.notify_all();
+    }
+}
+
+void enqueue_locked(const std::string &src) {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        std::atexit(drain_at_exit);
+        std::thread(worker_main).detach();
+    });
+    g_cache[src];  // QUEUED
+    g_queue.push_back(src);
+    g_cv.notify_all();
+}
+
+// Load a READY entry's cubin on this thread (first launch).  Caller holds g_mu.
+void load_locked(Entry &e) {
+    SV_CUDA(cudaLibraryLoadData(&e.lib, e.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+    SV_CUDA(cudaLibraryGetKernel(&e.kern, e.lib, "sv_gate_jit"));
+    SV_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void *>(e.kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (1 << kGateTileBitsC64) * (int)sizeof(float2)));
-    return c;
+    ++g_compiles;
 }
 
 }  // namespace
 
-// SV_GATE_JIT: "0" never, "1" every complex64 one-GPU pass (errors propagate),
-// unset = passes of >= 2^11 tiles (states of >= 2^24 amplitudes), where a
-// pass takes milliseconds and the one-time compile is amortised; a compile
-// failure in the automatic mode falls back to the interpreter kernel.
+// SV_GATE_JIT: "0" never, "1" every complex64 one-GPU pass, compiled before
+// its first launch (errors propagate), unset = passes of >= 2^11 tiles (states
+// of >= 2^24 amplitudes), compiled in the background on first sight while the
+// interpreter runs them (a one-shot circuit never waits for NVRTC; a repeated
+// one switches to the specialised kernel once it is ready); a compile failure
+// in the automatic mode leaves the pass on the interpreter.
 int gate_jit_mode() {
     const char *e = getenv("SV_GATE_JIT");
     if (!e) return 2;
@@ -208,26 +306,45 @@ bool launch_gate_jit(const KParams &kp, const void *dev_ops, const void *host_op
     if (mode == 0 || host_ops == nullptr) return false;
     if (mode == 2 && ntiles < (1ull << 11)) return false;
     const std::string src = generate(reinterpret_cast<const GOp<float> *>(host_ops), nops, lin, !param);
-    Compiled c;
-    try {
-        std::lock_guard<std::mutex> lk(g_mu);
+    cudaKernel_t kern = nullptr;
+    {
+        std::unique_lock<std::mutex> lk(g_mu);
         auto it = g_cache.find(src);
-        if (it == g_cache.end()) {
-            const auto t0 = std::chrono::steady_clock::now();
-            Compiled nc = compile(src);
-            g_compile_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-            ++g_compiles;
-            it = g_cache.emplace(src, nc).first;
+        if (mode == 1) {  // forced: compile now, errors propagate
+            if (it == g_cache.end() || it->second.state == Entry::FAILED) {
+                lk.unlock();
+                std::vector<char> cubin = timed_compile(src);
+                lk.lock();
+                Entry &e = g_cache[src];
+                if (e.state != Entry::READY) {
+                    e.cubin.swap(cubin);
+                    e.state = Entry::READY;
+                }
+                it = g_cache.find(src);
+            } else if (it->second.state == Entry::QUEUED) {
+                g_cv.wait(lk, [&] { return it->second.state != Entry::QUEUED; });
+                if (it->second.state == Entry::FAILED) throw Error{SV_ECUDA, it->second.err};
+            }
+        } else {  // automatic: queue it and run the interpreter until it is ready
+            if (it == g_cache.end()) {
+                enqueue_locked(src);
+                return false;
+            }
+            if (it->second.state != Entry::READY) {
+                if (it->second.state == Entry::FAILED) {
+                    static bool warned = false;
+                    if (!warned) {
+                        fprintf(stderr, "libsv: gate JIT unavailable, using the interpreter kernel: %s\n",
+                                it->second.err.c_str());
+                        warned = true;
+                    }
+                }
+                return false;
+            }
         }
-        c = it->second;
-    } catch (const Error &e) {
-        if (mode == 1) throw;
-        static bool warned = false;
-        if (!warned) {
-            fprintf(stderr, "libsv: gate JIT unavailable, using the interpreter kernel: %s\n", e.msg.c_str());
-            warned = true;
-        }
-        return false;
+        Entry &e = it->second;
+        if (e.kern == nullptr) load_locked(e);
+        kern = e.kern;
     }
     KParams p = kp;
     int n = (int)nops;
@@ -236,12 +353,12 @@ bool launch_gate_jit(const KParams &kp, const void *dev_ops, const void *host_op
         auto prog = std::make_unique<GProg<float>>();
         memcpy(prog->op, host_ops, nops * sizeof(GOp<float>));
         void *args[] = {&p, prog.get(), &n};
-        SV_CUDA(cudaLaunchKernel(reinterpret_cast<const void *>(c.kern), dim3((unsigned int)ntiles), dim3(256), args,
+        SV_CUDA(cudaLaunchKernel(reinterpret_cast<const void *>(kern), dim3((unsigned int)ntiles), dim3(256), args,
                                  smem, s));
     } else {
         const void *ops = dev_ops;
         void *args[] = {&p, &ops, &n};
-        SV_CUDA(cudaLaunchKernel(reinterpret_cast<const void *>(c.kern), dim3((unsigned int)ntiles), dim3(256), args,
+        SV_CUDA(cudaLaunchKernel(reinterpret_cast<const void *>(kern), dim3((unsigned int)ntiles), dim3(256), args,
                                  smem, s));
     }
     return true;
@@ -252,8 +369,9 @@ size_t gate_jit_compile_only(const void *host_ops, uint64_t nops, bool lin, bool
     return compile_cubin(generate(reinterpret_cast<const GOp<float> *>(host_ops), nops, lin, glb)).size();
 }
 
-void gate_jit_stats(uint64_t *compiles, double *seconds) {
-    std::lock_guard<std::mutex> lk(g_mu);
+void gate_jit_stats(uint64_t *compiles, double *seconds, bool wait) {
+    std::unique_lock<std::mutex> lk(g_mu);
+    if (wait) g_cv.wait(lk, [] { return g_queue.empty() && !g_busy; });
     if (compiles) *compiles = g_compiles;
     if (seconds) *seconds = g_compile_s;
 }

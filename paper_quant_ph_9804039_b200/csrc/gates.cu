@@ -36,7 +36,7 @@ namespace sv {
 bool launch_gate_jit(const KParams &kp, const void *dev_ops, const void *host_ops, uint64_t nops, bool lin,
                      bool param, unsigned long long ntiles, cudaStream_t s);
 size_t gate_jit_compile_only(const void *host_ops, uint64_t nops, bool lin, bool glb);
-void gate_jit_stats(uint64_t *compiles, double *seconds);
+void gate_jit_stats(uint64_t *compiles, double *seconds, bool wait);
 
 // ------------------------------------------------------------------------- //
 // Host: op programs                                                          //
@@ -475,7 +475,7 @@ extern "C" sv_status sv_debug_gate_jit(int n, sv_dtype dtype, const sv_gate *gat
                                        uint64_t *passes, uint64_t *compiles, double *compile_seconds) {
     using namespace sv;
     try {
-        if (compile) {
+        if (compile == 1) {
             SV_CHECK(dtype == SV_C64, SV_EINVAL, "the gate JIT is complex64 only");
             const GatePlan gp = plan_gates(n, 0, dtype, gates, count);
             uint64_t np = 0;
@@ -497,7 +497,7 @@ extern "C" sv_status sv_debug_gate_jit(int n, sv_dtype dtype, const sv_gate *gat
             }
             if (passes) *passes = np;
         }
-        gate_jit_stats(compiles, compile_seconds);
+        gate_jit_stats(compiles, compile_seconds, compile == 2);
         set_error("");
         return SV_OK;
     } catch (const Error &e) {

@@ -46,8 +46,9 @@ def main():
     with sv.sv_init(n, 1, sv.SV_C64, sv.SV_INIT_GAUSSIAN) as c:
         for name, gates in work.items():
             steps, _ = sv.sv_plan_gates(n, 1, sv.SV_C64, gates)
-            sv.sv_apply_gates(c, gates)  # warm-up
+            sv.sv_apply_gates(c, gates)  # warm-up (queues the passes' specialised kernels, gate_jit.cu)
             sv.sv_synchronize(c)
+            sv.sv_debug_gate_jit(compile=2)  # steady state: wait for the background compiler
             best = None
             for _ in range(args.reps):
                 sv.sv_profile(c, True)
@@ -72,6 +73,7 @@ def main():
                 "avg_pass_frac": 2 * S * len(best) / t / 1e9 / peak,
                 "per_pass": passes}
             print(name, json.dumps({k: v for k, v in res["workloads"][name].items() if k != "per_pass"}), flush=True)
+    res["gate_jit"] = {"mode": os.environ.get("SV_GATE_JIT", "auto"), **sv.sv_debug_gate_jit()}
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     json.dump(res, open(args.out, "w"), indent=1)
 
