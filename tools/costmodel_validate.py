@@ -34,6 +34,7 @@ def profiled(ctx, fn):
     """Run fn() once for warm-up, then once profiled; return (total device ms, timeline)."""
     fn()
     sv.sv_synchronize(ctx)
+    sv.sv_debug_gate_jit(compile=2)  # gate passes: the specialised kernels are ready (gate_jit.cu)
     sv.sv_profile(ctx, True)
     fn()
     tl = sv.sv_profile_timeline(ctx)
