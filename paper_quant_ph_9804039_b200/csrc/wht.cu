@@ -263,9 +263,206 @@ __global__ void __launch_bounds__(512) whole_state_kernel(E *a, int n, int k, in
     for (unsigned int i = tid; i < N; i += nt) a[i] = s[i];
 }
 
+// ------------------------------------------------------------------------- //
+// Whole state in the REGISTERS of 4 warps (n = LOGR + 7, round 2): 2^LOGR    //
+// amplitudes per thread.  Index bits [0, LOGR) are register bits (stages in  //
+// registers), [LOGR, LOGR + 5) lane bits (stages by warp shuffles: lane with //
+// the bit clear forms x + y, its partner y' - x' = a_i - a_j, the same two   //
+// sums as the pair butterfly), the top 2 warp bits go through ONE shared-    //
+// memory relayout per transform (layout B makes them register bits).  The    //
+// CTA barriers per iteration drop from ~22 (two stages per shared-memory     //
+// round trip, whole_state_kernel) to 4.                                       //
+// ------------------------------------------------------------------------- //
+template <typename E, typename R>
+__device__ __forceinline__ void shfl_stage(E &x, int d, bool hi, const double *c) {
+    E y;
+    y.x = __shfl_xor_sync(0xffffffffu, x.x, d);
+    y.y = __shfl_xor_sync(0xffffffffu, x.y, d);
+    if (c == nullptr) {  // ideal butterfly: (a_i, a_j) -> (a_i + a_j, a_i - a_j)
+        if (!hi) { x.x = x.x + y.x; x.y = x.y + y.y; }
+        else { x.x = y.x - x.x; x.y = y.y - x.y; }
+    } else {  // Fig. 3's [w x; y z]: a_i' = w a_i + x a_j, a_j' = y a_i + z a_j
+        const R w = (R)c[0], xx = (R)c[1], yy = (R)c[2], z = (R)c[3];
+        if (!hi) { x.x = w * x.x + xx * y.x; x.y = w * x.y + xx * y.y; }
+        else { x.x = yy * y.x + z * x.x; x.y = yy * y.y + z * x.y; }
+    }
+}
+
+template <int LOGR>
+__device__ __forceinline__ unsigned int wr_pad(unsigned int i) { return i + (i >> LOGR); }  // conflict-free rows
+// layout A: index = tid * 2^LOGR + r; layout B: register bits 0-1 = the two
+// warp (top) bits, register bits 2.. = index bits 0 .., thread bits = index
+// bits LOGR - 2 .. LOGR + 4
+template <int LOGR>
+__device__ __forceinline__ unsigned int wr_idxA(int tid, int r) { return ((unsigned int)tid << LOGR) | (unsigned int)r; }
+template <int LOGR>
+__device__ __forceinline__ unsigned int wr_idxB(int tid, int r) {
+    return ((unsigned int)(r & 3) << (LOGR + 5)) | ((unsigned int)r >> 2) | ((unsigned int)tid << (LOGR - 2));
+}
+
+template <typename E, int LOGR>
+__device__ __forceinline__ void wr_transform(E (&x)[1 << LOGR], E *s, int tid, const double *cbase) {
+    using R = typename RealOf<E>::T;
+    constexpr int NR = 1 << LOGR;
+    const int lane = tid & 31;
+#pragma unroll
+    for (int q = 0; q < LOGR; ++q) {
+        const double *c = cbase ? cbase + 4 * q : nullptr;
+#pragma unroll
+        for (int j = 0; j < NR; ++j)
+            if (!(j & (1 << q))) {
+                if (c) bfly_gen(x[j], x[j | (1 << q)], c);
+                else bfly(x[j], x[j | (1 << q)]);
+            }
+    }
+#pragma unroll
+    for (int b = 0; b < 5; ++b) {
+        const double *c = cbase ? cbase + 4 * (LOGR + b) : nullptr;
+        const bool hi = (lane >> b) & 1;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) shfl_stage<E, R>(x[j], 1 << b, hi, c);
+    }
+    // warp bits: relayout A -> B (each thread then rewrites only what it read: one barrier each way)
+#pragma unroll
+    for (int r = 0; r < NR; ++r) s[wr_pad<LOGR>(wr_idxA<LOGR>(tid, r))] = x[r];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < NR; ++r) x[r] = s[wr_pad<LOGR>(wr_idxB<LOGR>(tid, r))];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const double *c = cbase ? cbase + 4 * (LOGR + 5 + q) : nullptr;
+#pragma unroll
+        for (int j = 0; j < NR; ++j)
+            if (!(j & (1 << q))) {
+                if (c) bfly_gen(x[j], x[j | (1 << q)], c);
+                else bfly(x[j], x[j | (1 << q)]);
+            }
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) s[wr_pad<LOGR>(wr_idxB<LOGR>(tid, r))] = x[r];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < NR; ++r) x[r] = s[wr_pad<LOGR>(wr_idxA<LOGR>(tid, r))];
+}
+
+// fixed-order CTA sums: the thread's values in register order, a warp xor
+// butterfly (every lane ends with bitwise the same value), the 4 warps in order
+__device__ __forceinline__ void wr_cta_sum2(double re, double im, double &tre, double &tim, double *red, int tid) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, o);
+        im += __shfl_xor_sync(0xffffffffu, im, o);
+    }
+    if ((tid & 31) == 0) { red[2 * (tid >> 5)] = re; red[2 * (tid >> 5) + 1] = im; }
+    __syncthreads();
+    tre = red[0] + red[2] + red[4] + red[6];
+    tim = red[1] + red[3] + red[5] + red[7];
+    __syncthreads();  // red reused
+}
+
+template <typename E, int LOGR>
+__global__ void __launch_bounds__(128) whole_reg_kernel(E *a, int k, int with_oracle, int diffusion,
+                                                        const unsigned long long *marked, unsigned long long m,
+                                                        double f0_scale, const double *coefs, double *survival) {
+    using R = typename RealOf<E>::T;
+    constexpr int NR = 1 << LOGR, n = LOGR + 7;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    E *s = reinterpret_cast<E *>(smem_raw);
+    __shared__ double red[2 * 4];
+    const int tid = threadIdx.x;
+    __shared__ unsigned long long s_mk[64];  // the marked set, when it is small, read once
+    E x[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) x[r] = a[wr_idxA<LOGR>(tid, r)];
+    const bool mk_smem = with_oracle && m <= 64;
+    if (mk_smem && tid < (int)m) s_mk[tid] = marked[tid];
+    __syncthreads();
+    for (int it = 0; it < k; ++it) {
+        if (with_oracle) {
+            for (unsigned long long j = 0; j < m; ++j) {
+                const unsigned long long mk = mk_smem ? s_mk[j] : marked[j];
+                if ((int)(mk >> LOGR) == tid) {
+                    const int rr = (int)(mk & (NR - 1));
+#pragma unroll
+                    for (int r = 0; r < NR; ++r)
+                        if (r == rr) { x[r].x = -x[r].x; x[r].y = -x[r].y; }
+                }
+            }
+        }
+        if (diffusion == SV_DIFFUSE_WHT) {
+            wr_transform<E, LOGR>(x, s, tid, coefs ? coefs + (size_t)(2 * it) * n * 4 : nullptr);
+            // F0 = 2|0><0| - I with the 2^-n of the unnormalised transforms (G2, G5)
+#pragma unroll
+            for (int r = 0; r < NR; ++r) scale(x[r], (R)(-f0_scale));
+            if (tid == 0) { x[0].x = -x[0].x; x[0].y = -x[0].y; }
+            wr_transform<E, LOGR>(x, s, tid, coefs ? coefs + (size_t)(2 * it + 1) * n * 4 : nullptr);
+            if (survival) {  // renormalise (G22): sum |a|^2 in fixed order, record it, scale to norm 1
+                double sq = 0.0;
+#pragma unroll
+                for (int r = 0; r < NR; ++r) sq += (double)x[r].x * (double)x[r].x + (double)x[r].y * (double)x[r].y;
+                double tot, dummy;
+                wr_cta_sum2(sq, 0.0, tot, dummy, red, tid);
+                if (tid == 0) survival[it] = tot;
+                const R inv = (R)(1.0 / sqrt(tot));
+#pragma unroll
+                for (int r = 0; r < NR; ++r) { x[r].x *= inv; x[r].y *= inv; }
+            }
+        } else {  // inversion about the mean
+            double re = 0.0, im = 0.0;
+#pragma unroll
+            for (int r = 0; r < NR; ++r) { re += (double)x[r].x; im += (double)x[r].y; }
+            double mr, mi;
+            wr_cta_sum2(re, im, mr, mi, red, tid);
+            const R two_mr = (R)(2.0 * mr * f0_scale), two_mi = (R)(2.0 * mi * f0_scale);
+#pragma unroll
+            for (int r = 0; r < NR; ++r) { x[r].x = two_mr - x[r].x; x[r].y = two_mi - x[r].y; }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) a[wr_idxA<LOGR>(tid, r)] = x[r];
+}
+
+template <typename E, int LOGR>
+static void launch_whole_reg(E *state, int k, int with_oracle, int diffusion, const unsigned long long *mk,
+                             uint64_t m, double f0, const double *coefs, double *survival, cudaStream_t s) {
+    const unsigned int N = 1u << (LOGR + 7);
+    const int smem = (int)((N + (N >> LOGR)) * sizeof(E));
+    SV_CUDA(cudaFuncSetAttribute(whole_reg_kernel<E, LOGR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    whole_reg_kernel<E, LOGR><<<1, 128, smem, s>>>(state, k, with_oracle, diffusion, mk, m, f0, coefs, survival);
+    SV_CUDA(cudaGetLastError());
+}
+
+#ifndef SV_WHOLE_REG
+#define SV_WHOLE_REG 1  // 0: every whole-state run on whole_state_kernel (A/B)
+#endif
+
 void launch_whole_state(sv_dtype dt, void *state, int n, int k, int with_oracle, int diffusion,
                         const uint64_t *marked, uint64_t m, cudaStream_t s, const double *coefs, double *survival) {
     const unsigned int N = 1u << n;
+    if (SV_WHOLE_REG && n >= 9) {  // the register-resident kernel (n = 9 .. T)
+        const double f0r = coefs ? 1.0 : ldexp(1.0, -n);
+        SV_CHECK(!coefs || diffusion == SV_DIFFUSE_WHT, SV_EINVAL, "internal: angle errors need the WHT diffusion");
+        const auto mkr = reinterpret_cast<const unsigned long long *>(marked);
+        if (dt == SV_C64) {
+            float2 *st = reinterpret_cast<float2 *>(state);
+            switch (n) {
+                case 9: return launch_whole_reg<float2, 2>(st, k, with_oracle, diffusion, mkr, m, f0r, coefs, survival, s);
+                case 10: return launch_whole_reg<float2, 3>(st, k, with_oracle, diffusion, mkr, m, f0r, coefs, survival, s);
+                case 11: return launch_whole_reg<float2, 4>(st, k, with_oracle, diffusion, mkr, m, f0r, coefs, survival, s);
+                case 12: return launch_whole_reg<float2, 5>(st, k, with_oracle, diffusion, mkr, m, f0r, coefs, survival, s);
+                case 13: return launch_whole_reg<float2, 6>(st, k, with_oracle, diffusion, mkr, m, f0r, coefs, survival, s);
+                default: break;
+            }
+        } else {
+            double2 *st = reinterpret_cast<double2 *>(state);
+            switch (n) {  // (n = 12: 32 amplitudes per thread measured 2x slower than whole_state_kernel)
+                case 9: return launch_whole_reg<double2, 2>(st, k, with_oracle, diffusion, mkr, m, f0r, coefs, survival, s);
+                case 10: return launch_whole_reg<double2, 3>(st, k, with_oracle, diffusion, mkr, m, f0r, coefs, survival, s);
+                case 11: return launch_whole_reg<double2, 4>(st, k, with_oracle, diffusion, mkr, m, f0r, coefs, survival, s);
+                default: break;
+            }
+        }
+    }
     const int threads = N >= 1024 ? 512 : (N / 2 >= 32 ? (int)(N / 2) : 32);
     const double f0 = coefs ? 1.0 : ldexp(1.0, -n);
     SV_CHECK(!coefs || diffusion == SV_DIFFUSE_WHT, SV_EINVAL, "internal: angle errors need the WHT diffusion");
