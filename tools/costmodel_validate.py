@@ -159,11 +159,15 @@ def observe_mean(n, k):
     return tot / 1e3
 
 
+LAST_TIMELINE = []
+
+
 def observe_gates(n, gates, world=1):
     with sv.sv_init(n, 1, sv.SV_C64, sv.SV_INIT_GAUSSIAN, world=world) as c:
         if world > 1:
             sv.sv_set_exchange(c, False)
-        tot, _ = profiled(c, lambda: sv.sv_apply_gates(c, gates))
+        tot, tl = profiled(c, lambda: sv.sv_apply_gates(c, gates))
+    LAST_TIMELINE[:] = [round(ms, 3) for _, ms in tl]
     return tot / 1e3
 
 
@@ -194,6 +198,7 @@ def main():
         before = sv.sv_debug_gate_jit()["compiles"]
         row(f"gates {name} n={n} (c64)", 1, observe_gates(n, g), CM.predict_gates(n, 1, 0, g, prm)["t"])
         rows[-1]["jit_kernels_loaded"] = sv.sv_debug_gate_jit()["compiles"] - before
+        rows[-1]["pass_ms"] = list(LAST_TIMELINE)
     for P in (2, 4):
         row(f"WHT n=30 k=4 emulated P={P} (a2a copies)", P, observe_wht(30, 4, world=P, fused=False),
             CM.predict_wht(30, P, 0, 4, prm, emulated=True, fused_exchange=False)["t"])
