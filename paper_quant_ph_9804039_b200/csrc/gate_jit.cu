@@ -147,6 +147,7 @@ std::string generate(const GOp<float> *ops, uint64_t nops, bool lin, bool glb) {
 // library is loaded on the launching thread at first use.
 struct Entry {
     enum State { QUEUED, READY, FAILED } state = QUEUED;
+    int device = 0;              // the device of the first request (the worker loads the module there)
     std::vector<char> cubin;
     std::string err;
     cudaLibrary_t lib = nullptr;
@@ -233,6 +234,15 @@ std::vector<char> timed_compile(const std::string &src) {
     return cubin;
 }
 
+void load_kernel(const std::vector<char> &cubin, cudaLibrary_t *lib, cudaKernel_t *kern) {
+    SV_CUDA(cudaLibraryLoadData(lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+    SV_CUDA(cudaLibraryGetKernel(kern, *lib, "sv_gate_jit"));
+    SV_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void *>(*kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (1 << kGateTileBitsC64) * (int)sizeof(float2)));
+    cudaFuncAttributes fa{};  // forces the module into the current context now
+    SV_CUDA(cudaFuncGetAttributes(&fa, reinterpret_cast<const void *>(*kern)));
+}
+
 void worker_main() {
     std::unique_lock<std::mutex> lk(g_mu);
     for (;;) {
@@ -240,11 +250,18 @@ void worker_main() {
         const std::string src = g_queue.front();  // (moved out before the lock is released)
         g_queue.pop_front();
         g_busy = true;
+        const int device = g_cache[src].device;
         lk.unlock();
         std::vector<char> cubin;
         std::string err;
+        cudaLibrary_t lib = nullptr;
+        cudaKernel_t kern = nullptr;
         try {
             cubin = timed_compile(src);
+            // load here, off the launch path: with CUDA's lazy module loading the
+            // first launch would otherwise pay the module load inside the pass
+            SV_CUDA(cudaSetDevice(device));
+            load_kernel(cubin, &lib, &kern);
         } catch (const Error &e) {
             err = e.msg;
         }
@@ -252,6 +269,9 @@ void worker_main() {
         Entry &e = g_cache[src];
         if (err.empty()) {
             e.cubin.swap(cubin);
+            e.lib = lib;
+            e.kern = kern;
+            ++g_compiles;
             e.state = Entry::READY;
         } else {
             e.err = err;
@@ -262,23 +282,21 @@ void worker_main() {
     }
 }
 
-void enqueue_locked(const std::string &src) {
+
+void enqueue_locked(const std::string &src, int device) {
     static std::once_flag once;
     std::call_once(once, [] {
         std::atexit(drain_at_exit);
         std::thread(worker_main).detach();
     });
-    g_cache[src];  // QUEUED
+    g_cache[src].device = device;  // QUEUED
     g_queue.push_back(src);
     g_cv.notify_all();
 }
 
-// Load a READY entry's cubin on this thread (first launch).  Caller holds g_mu.
+// Load a READY entry's cubin on this thread (forced mode).  Caller holds g_mu.
 void load_locked(Entry &e) {
-    SV_CUDA(cudaLibraryLoadData(&e.lib, e.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
-    SV_CUDA(cudaLibraryGetKernel(&e.kern, e.lib, "sv_gate_jit"));
-    SV_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void *>(e.kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (1 << kGateTileBitsC64) * (int)sizeof(float2)));
+    load_kernel(e.cubin, &e.lib, &e.kern);
     ++g_compiles;
 }
 
@@ -327,7 +345,9 @@ bool launch_gate_jit(const KParams &kp, const void *dev_ops, const void *host_op
             }
         } else {  // automatic: queue it and run the interpreter until it is ready
             if (it == g_cache.end()) {
-                enqueue_locked(src);
+                int dev = 0;
+                SV_CUDA(cudaGetDevice(&dev));
+                enqueue_locked(src, dev);
                 return false;
             }
             if (it->second.state != Entry::READY) {

@@ -98,7 +98,14 @@ def calibrate(n=30, class_sizes=(30, 33)):
     # memory-side passes: a few uncontrolled unitaries (memory ~ compute) -- they pin the overlap rho
     light = {f"light{m}": C.circuit([C.record(3 + q, C.random_unitary(np.random.default_rng(90 + m * 10 + q)))
                                      for q in range(m)]) for m in (3, 6)}
-    extra = {"balanced": balanced, "hop": C.circuit(hop), **light}
+    # separate the op cost from the relayout cost: controlled unitaries cycling over tile bits 9-12
+    # (all register bits of layout A: no relayout, nothing fuses), and cheap NOT gates alternating
+    # (CNOTs, alternately controlled: nothing commutes) between a layout-A and a layout-B target
+    cyc = [C.record(9 + (i % 4), C.random_unitary(np.random.default_rng(200 + i)), [9 + ((i + 1) % 4)])
+           for i in range(240)]
+    flip = [C.record(10, C.X, [4]) if i % 2 else C.record(4, C.X, [10]) for i in range(120)]
+    extra = {"balanced": balanced, "hop": C.circuit(hop), **light, "ops_no_relayout": C.circuit(cyc),
+             "relayouts": C.circuit(flip)}
     # t_pass = t_mem + t_ops - rho min(t_mem, t_ops), t_ops = pairs x (n_gen t_gate + n_diag t_diag +
     # n_lin t_lin) + N x relayouts x t_rel.  For each rho on a grid the op costs come from non-negative
     # least squares over the compute-dominated passes (t_ops >= t_mem: rhs = t_pass - (1 - rho) t_mem);
