@@ -73,6 +73,8 @@ typedef struct sv_ctx sv_ctx; /* opaque; one per process (= per GPU rank) */
  *  - nccl_id != NULL: real rank `rank` of a P-rank job; nccl_id points to the
  *    128-byte ncclUniqueId produced by sv_nccl_unique_id() on rank 0 and
  *    broadcast by the caller (e.g. torch.distributed).  One GPU per rank.
+ *    world = 1 with an id makes a one-rank communicator (the collectives of
+ *    the schedule then run through NCCL on one GPU).
  *  - nccl_id == NULL and world > 1: single-process emulation of all P ranks on
  *    one device (the state is held as P shards in rank order; qubit swaps are
  *    device-local copies).  For tests of the sharded schedule on one GPU.

@@ -150,7 +150,7 @@ def sv_init(n: int, seed: int = 0, dtype: int = SV_C64, init: int = SV_INIT_UNIF
     out = ctypes.c_void_p()
     dist = None
     idbuf = None
-    if world > 1 or stream is not None or device != 0:
+    if world > 1 or stream is not None or device != 0 or nccl_id is not None:
         idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         dist = sv_dist(rank, world, ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None, device,
                        stream if stream else None)

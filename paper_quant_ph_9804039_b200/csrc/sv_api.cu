@@ -985,7 +985,10 @@ sv_status sv_init(sv_ctx **out, int n, uint64_t seed, sv_dtype dtype, sv_init_ki
         SV_CUDA(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned int), c->stream));
         SV_CUDA(cudaMemsetAsync(c->d_sums, 0, 8 * sizeof(double), c->stream));
         c->mgrid = std::min(mean_grid(c->nres, dtype), kMaxGrid);
-        if (dist && world > 1 && !c->emulated) {
+        // world = 1 with an id: a one-rank communicator -- every collective of
+        // the schedule (scalar allreduces, the polling waits) runs through NCCL
+        // on one GPU (tests/test_nccl_one_rank_gpu.py)
+        if (dist && !c->emulated && dist->nccl_id != nullptr) {
             ncclUniqueId id;
             memcpy(&id, dist->nccl_id, sizeof(id));
             SV_NCCL(ncclCommInitRank(&c->comm, world, id, c->rank));
