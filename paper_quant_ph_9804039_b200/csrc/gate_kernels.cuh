@@ -285,28 +285,6 @@ __device__ __forceinline__ void apply_linphase(E (&x)[L::NR], const GOp<R> *ent,
     hi[0] = F;
 #pragma unroll
     for (int j = 1; j < (1 << HI); ++j) hi[j] = cprod(hi[j & (j - 1)], (j & 1) ? P[LO < RB ? LO : 0] : P[LO + 1 < RB ? LO + 1 : 0]);
-#if SV_GATE_PACKED
-    if constexpr (sizeof(R) == 4) {
-        // complex64: x (lo) (hi) with the packed operand pairs (re, re) / (-im, im) of the
-        // 8 + 4 table entries built once -- per amplitude 4 packed FMUL2/FFMA2 and no
-        // pair re-assembly (the lane swap folds into the operand); round 2, QFT passes
-        // ~20 % fewer instructions than x (lo hi)
-        float2 lre[1 << LO], lim[1 << LO], hre[1 << HI], him[1 << HI];
-#pragma unroll
-        for (int j = 0; j < (1 << LO); ++j) { lre[j] = make_float2(lo[j].x, lo[j].x); lim[j] = make_float2(-lo[j].y, lo[j].y); }
-#pragma unroll
-        for (int j = 0; j < (1 << HI); ++j) { hre[j] = make_float2(hi[j].x, hi[j].x); him[j] = make_float2(-hi[j].y, hi[j].y); }
-#pragma unroll
-        for (int j = 0; j < L::NR; ++j)
-            if (tcls != LP_REG || ((j >> tbit) & 1)) {
-                const int l = j & ((1 << LO) - 1), h = j >> LO;
-                float2 t = x[j];
-                t = __ffma2_rn(lim[l], make_float2(t.y, t.x), __fmul2_rn(lre[l], t));
-                x[j] = __ffma2_rn(him[h], make_float2(t.y, t.x), __fmul2_rn(hre[h], t));
-            }
-        return;
-    }
-#endif
 #pragma unroll
     for (int j = 0; j < L::NR; ++j)
         if (tcls != LP_REG || ((j >> tbit) & 1)) {
