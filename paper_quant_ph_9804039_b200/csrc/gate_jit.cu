@@ -75,7 +75,13 @@ std::string u32(unsigned int v) { return std::to_string(v) + "u"; }
 std::string generate(const GOp<float> *ops, uint64_t nops, bool lin, bool glb) {
     std::string b;
     b += "#include \"gate_kernels.cuh\"\nusing namespace sv;\n";
-    b += "extern \"C\" __global__ void __launch_bounds__(256, 2) sv_gate_jit(const KParams p, ";
+    // co-resident CTAs per SM the kernel is compiled for (SV_GATE_JIT_MINB, A/B; default 2 -- the
+    // interpreter's; 3 caps registers at 85)
+    static const int minb = [] {
+        const char *e = getenv("SV_GATE_JIT_MINB");
+        return e ? atoi(e) : 2;
+    }();
+    b += "extern \"C\" __global__ void __launch_bounds__(256, " + std::to_string(minb) + ") sv_gate_jit(const KParams p, ";
     if (lin && !glb) b += "const __grid_constant__ GProg<float> prog, int nops) {\n    const GOp<float> *ops = prog.op;\n";
     else b += "const GOp<float> *__restrict__ ops, int nops) {\n";
     b += "    (void)ops; (void)nops;\n"
