@@ -437,6 +437,16 @@ def run_ours(args):
         cf = math.sin((2 * k + 1) * math.asin(math.sqrt(M / N_amp))) ** 2
         check = {"p_success": p_success, "closed_form": cf, "abs_err": abs(p_success - cf),
                  "what": "marked mass after k iterations from the uniform start vs sin^2((2k+1) theta)"}
+    else:
+        # no closed form (angle errors, decoherence, Gaussian start): the timed run's state must
+        # still have norm 1 -- the iteration is unitary (angle errors, ideal) or renormalised
+        # every iteration (decoherence, G22); sum |a|^2 in fp64 (sv_norm2)
+        try:
+            nrm = sv.sv_norm2(ctx)
+            check = {"norm": nrm, "abs_err": abs(nrm - 1.0),
+                     "what": "sum |a|^2 of the timed run's final state vs 1 (unitary / renormalised iteration)"}
+        except Exception as e:  # reporting only
+            check = {"error": repr(e)[:200]}
 
     # the B200 refit of the paper's analytical model (costmodel.py) for this
     # step, next to the measurement: its prediction error is the Table 5/6 analog

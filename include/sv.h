@@ -178,6 +178,13 @@ sv_status sv_sample(sv_ctx *ctx, uint64_t shots, uint64_t seed, uint64_t *out, i
  * ranks (identical on every rank).  SV_ESTATE if no marked set. */
 sv_status sv_measure_marked_mass(sv_ctx *ctx, double *out);
 
+/* Squared norm sum_i |a_i|^2 of the whole register (all ranks; fp64,
+ * deterministic fixed-order reduction, allreduced): the norm-drift readout of
+ * S:134 / S:125 -- 1 up to rounding after any unitary iteration (ideal or
+ * with angle errors) and after every renormalised decoherent iteration.
+ * Synchronises.  Errors: SV_EINVAL (NULL out). */
+sv_status sv_norm2(sv_ctx *ctx, double *out);
+
 /* Copy `count` resident amplitudes starting at resident offset `offset` to
  * host memory, dtype-native (8 or 16 bytes each).  SV_EINVAL if out of range. */
 sv_status sv_get_amplitudes(sv_ctx *ctx, void *host_out, uint64_t offset, uint64_t count);

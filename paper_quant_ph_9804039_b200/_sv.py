@@ -75,6 +75,7 @@ _SIGS = {
     "sv_iterate_decoherent": ([_ctxp, _i32, ctypes.c_double, ctypes.c_double, _u64, _u64, _vp], _i32),
     "sv_probabilities": ([_ctxp, _vp, _u64, _i32], _i32),
     "sv_measure_marked_mass": ([_ctxp, _dp], _i32),
+    "sv_norm2": ([_ctxp, _dp], _i32),
     "sv_sample": ([_ctxp, _u64, _u64, _vp, _i32], _i32),
     "sv_get_amplitudes": ([_ctxp, _vp, _u64, _u64], _i32),
     "sv_set_amplitudes": ([_ctxp, _vp, _u64, _u64], _i32),
@@ -223,6 +224,13 @@ def sv_sample(ctx: Ctx, shots: int, seed: int, out_device_ptr: int | None = None
 def sv_measure_marked_mass(ctx: Ctx) -> float:
     v = ctypes.c_double()
     _check(lib.sv_measure_marked_mass(ctx.ptr, ctypes.byref(v)), "sv_measure_marked_mass")
+    return v.value
+
+
+def sv_norm2(ctx: Ctx) -> float:
+    """sum |a|^2 over the whole register (fp64, all ranks)."""
+    v = ctypes.c_double()
+    _check(lib.sv_norm2(ctx.ptr, ctypes.byref(v)), "sv_norm2")
     return v.value
 
 

@@ -1210,6 +1210,19 @@ sv_status sv_measure_marked_mass(sv_ctx *c, double *out) {
     });
 }
 
+sv_status sv_norm2(sv_ctx *c, double *out) {
+    return guarded([&] {
+        check_ctx(c);
+        SV_CHECK(out != nullptr, SV_EINVAL, "out is NULL");
+        SV_CUDA(cudaSetDevice(c->device));
+        double *d = c->d_sums + 7;
+        run(c, SV_K_READOUT, [&] { launch_norm2(c->dt, c->state, c->nres, c->d_partials, c->d_counter, d, c->stream); });
+        allreduce_sum(c, d, 1);
+        SV_CUDA(cudaMemcpyAsync(out, d, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        sync_ctx(c);
+    });
+}
+
 sv_status sv_get_amplitudes(sv_ctx *c, void *host_out, uint64_t offset, uint64_t count) {
     return guarded([&] {
         check_ctx(c);

@@ -47,6 +47,7 @@ NULL_CTX_CALLS = {
     "sv_get_exchange": lambda: lib.sv_get_exchange(NULL, ctypes.byref(ctypes.c_int())),
     "sv_synchronize": lambda: lib.sv_synchronize(NULL),
     "sv_comm_info": lambda: lib.sv_comm_info(NULL, None, None),
+    "sv_norm2": lambda: lib.sv_norm2(NULL, ctypes.byref(ctypes.c_double())),
     "sv_attach": lambda: lib.sv_attach(NULL, NULL, 0),
     "sv_snapshot": lambda: lib.sv_snapshot(NULL, b"/tmp/x", None),
     "sv_apply_gates": lambda: lib.sv_apply_gates(NULL, NULL, 0),

@@ -37,7 +37,7 @@ def test_one_rank_communicator_runs_the_collectives(dtype, monkeypatch):
             mass = sv.sv_measure_marked_mass(c)
             surv = sv.sv_iterate_decoherent(c, 2, 0.02, 0.01, 9, 0)
             shots = sv.sv_sample(c, 1000, 11)
-            out[tag] = (a0, sv.sv_get_amplitudes(c), mass, surv, shots)
+            out[tag] = (a0, sv.sv_get_amplitudes(c), mass, surv, shots, sv.sv_norm2(c))
     for x, y in zip(out["nccl"], out["plain"]):
         np.testing.assert_array_equal(x, y)
     a0 = out["plain"][0]
@@ -45,3 +45,4 @@ def test_one_rank_communicator_runs_the_collectives(dtype, monkeypatch):
     assert abs(out["nccl"][2] - orc.marked_mass(ref, marked)) <= 1e-5
     ref, _ = orc.iterate_decoherent(ref, marked, 2, 0.02, 0.01, 9, 0)
     assert_close(out["nccl"][1], ref, dtype, "one-rank NCCL", n=n, k=k + 4)
+    assert abs(out["nccl"][5] - orc.norm_sq(ref)) <= (1e-12 if dtype == sv.SV_C128 else 1e-5)

@@ -26,8 +26,10 @@ def test_noisy_iterate_matches_oracle(dtype, n, m, k, sigma):
         sv.sv_set_marked(c, marked)
         sv.sv_iterate_noisy(c, k, sigma, seed, t0)
         got = sv.sv_get_amplitudes(c)
+        nrm = sv.sv_norm2(c)
     ref = orc.iterate_noisy(a.copy(), marked, k, sigma, seed, t0)
     assert_close(got, ref, dtype, f"noisy n={n}", n=n, k=k)
+    assert abs(nrm - orc.norm_sq(ref)) < (1e-12 if dtype == sv.SV_C128 else 1e-5)  # sv_norm2
     assert abs(float(np.sum(np.abs(got.astype(np.complex128)) ** 2)) - 1.0) < (1e-12 if dtype == sv.SV_C128 else 1e-5)
 
 
