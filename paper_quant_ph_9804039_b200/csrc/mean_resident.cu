@@ -64,16 +64,39 @@ __device__ __forceinline__ void block_sum_bcast(double &re, double &im, double *
     im = red[65];
 }
 
+// One published block total: the fp64 (re, im) partial and the epoch it
+// belongs to (launch-unique: the host advances the base by k + 1 per launch,
+// so a slot left over from an earlier call never matches).
+struct alignas(32) ResSlot {
+    double re, im;
+    unsigned long long epoch;
+    unsigned long long pad;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+#ifndef SV_RES_SLOTS
+#define SV_RES_SLOTS 0  // 1: all-gather slots (measured slower: 7.7 vs 5.1 us per iteration at c2), A/B
+#endif
+
 template <typename E>
 __global__ void __launch_bounds__(kResThreads, 1)
     mean_resident_kernel(E *a, unsigned long long N, unsigned long long C, double inv_N,
                          const unsigned long long *marked, unsigned long long n_marked, int k, double *partials,
-                         unsigned int *bar) {
+                         unsigned int *bar, ResSlot *slots, unsigned long long epoch0) {
     using R = decltype(E{}.x);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     E *s = reinterpret_cast<E *>(smem_raw);
     __shared__ double red[66];
     __shared__ unsigned long long s_mlo, s_mcnt;
+    __shared__ unsigned long long s_mk[256];  // this block's marked entries, when few (read every iteration)
     const unsigned long long lo = (unsigned long long)blockIdx.x * C;
     const unsigned long long hi = lo + C < N ? lo + C : N;
     const unsigned int len = (unsigned int)(hi > lo ? hi - lo : 0);
@@ -90,30 +113,61 @@ __global__ void __launch_bounds__(kResThreads, 1)
     for (unsigned int i = threadIdx.x; i < len; i += blockDim.x) s[i] = __ldcg(a + lo + i);
     __syncthreads();
     const unsigned long long mlo = s_mlo, mcnt = s_mcnt;
+    const bool mk_smem = mcnt <= 256;
+    if (mk_smem && threadIdx.x < mcnt) s_mk[threadIdx.x] = marked[mlo + threadIdx.x];
+    __syncthreads();
     // Negate this block's marked entries (O); returns the thread's share of
     // sum over them of the values BEFORE negation.
     auto negate_marked = [&](double &cr, double &ci) {
         cr = 0.0;
         ci = 0.0;
         for (unsigned long long j = threadIdx.x; j < mcnt; j += blockDim.x) {
-            E &v = s[marked[mlo + j] - lo];
+            E &v = s[(mk_smem ? s_mk[j] : marked[mlo + j]) - lo];
             cr += (double)v.x;
             ci += (double)v.y;
             v.x = -v.x;
             v.y = -v.y;
         }
     };
+    unsigned int parity_round = 0;  // rounds gathered so far (epoch offset)
+    (void)parity_round;
     // Grid total of the per-block values (r, m): one partial per block, grid
     // barrier, then warp 0 sums the partials in a fixed order (lane-strided,
     // then a fixed shuffle tree) -- the same total in every block.
     auto grid_total = [&](double r, double m, int parity, double &tr, double &ti) {
         block_sum_bcast(r, m, red);
+#if SV_RES_SLOTS
+        // all-gather instead of a counter barrier: every block publishes its
+        // total with a release store of the round's epoch, and warp 0 of every
+        // block waits (acquire) on each slot's epoch before reading it -- no
+        // single atomic that all blocks serialise on, no second wait for a
+        // generation flip; the slots alternate by parity, so a slot is never
+        // rewritten before every block has read it (the next write to it comes
+        // after its owner has gathered the round in between, which needs every
+        // block's publication of that round, i.e. after every block's read)
+        const unsigned long long want = epoch0 + (unsigned long long)(parity_round++);
+        ResSlot *sl = slots + (size_t)parity * nb;
+        if (threadIdx.x == 0) {
+            sl[blockIdx.x].re = r;
+            sl[blockIdx.x].im = m;
+            st_release_u64(&sl[blockIdx.x].epoch, want);
+        }
+        if (threadIdx.x < 32) {
+            double R0 = 0.0, M0 = 0.0;
+            for (unsigned int b = threadIdx.x; b < nb; b += 32) {
+                while (ld_acquire_u64(&sl[b].epoch) != want) {
+                }
+                R0 += __ldcg(&sl[b].re);
+                M0 += __ldcg(&sl[b].im);
+            }
+#else
         double *part = partials + (size_t)parity * 2 * nb;
         if (threadIdx.x == 0) { part[2 * blockIdx.x] = r; part[2 * blockIdx.x + 1] = m; }
         grid_barrier(bar, bar + 1, nb);
         if (threadIdx.x < 32) {
             double R0 = 0.0, M0 = 0.0;
             for (unsigned int b = threadIdx.x; b < nb; b += 32) { R0 += __ldcg(&part[2 * b]); M0 += __ldcg(&part[2 * b + 1]); }
+#endif
             for (int o = 16; o > 0; o >>= 1) {
                 R0 += __shfl_xor_sync(0xffffffffu, R0, o);
                 M0 += __shfl_xor_sync(0xffffffffu, M0, o);
@@ -184,8 +238,16 @@ bool mean_resident_fits(sv_dtype dt, uint64_t N, size_t partials_cap) {
     return grid > 0 && (size_t)4 * grid <= partials_cap;
 }
 
+size_t mean_resident_slot_bytes(sv_dtype dt, uint64_t N) {
+    int grid, smem;
+    uint64_t C;
+    void *fn;
+    resident_geometry(dt, N, grid, C, smem, fn);
+    return (size_t)2 * (size_t)(grid > 0 ? grid : 0) * sizeof(ResSlot);
+}
+
 void launch_mean_resident(sv_dtype dt, void *a, uint64_t N, double inv_N, const uint64_t *marked, uint64_t m, int k,
-                          double *partials, unsigned int *bar, cudaStream_t s) {
+                          double *partials, unsigned int *bar, void *slots, unsigned long long epoch0, cudaStream_t s) {
     int grid, smem;
     uint64_t C;
     void *fn;
@@ -193,7 +255,8 @@ void launch_mean_resident(sv_dtype dt, void *a, uint64_t N, double inv_N, const 
     SV_CHECK(grid > 0 && k >= 1, SV_EINVAL, "internal: resident mean launch without a fitting geometry");
     unsigned long long Nl = N, Cl = C, ml = m;
     const unsigned long long *mk = reinterpret_cast<const unsigned long long *>(marked);
-    void *args[] = {&a, &Nl, &Cl, &inv_N, &mk, &ml, &k, &partials, &bar};
+    ResSlot *sl = reinterpret_cast<ResSlot *>(slots);
+    void *args[] = {&a, &Nl, &Cl, &inv_N, &mk, &ml, &k, &partials, &bar, &sl, &epoch0};
     SV_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kResThreads), args, (size_t)smem, s));
 }
 

@@ -95,6 +95,8 @@ struct sv_ctx {
     double *d_sums = nullptr;      // [0..1], [2..3] ping-pong; [4] norm; [6] scalar out
     unsigned int *d_counter = nullptr;
     unsigned int *d_gbar = nullptr;  // grid barrier of the persistent mean kernel {count, generation}
+    void *d_res_slots = nullptr;     // resident mean kernel: per-block published totals (two rounds)
+    unsigned long long res_epoch = 0;  // last epoch handed to the resident mean kernel
     bool mean_resident = true;       // SV_MEAN_RESIDENT=0 disables the one-launch path
     int mgrid = 1;
     Plan plan;
@@ -733,9 +735,17 @@ void run_mean(sv_ctx *c, int k, bool with_oracle) {
     // single GPU, state within the aggregate shared memory: all iterations in
     // one persistent launch (mean_resident.cu)
     if (c->comm == nullptr && c->mean_resident && mean_resident_fits(c->dt, c->nres, 2 * kMaxGrid)) {
+        if (c->d_res_slots == nullptr) {  // zeroed once: epochs start at 1
+            const size_t b = mean_resident_slot_bytes(c->dt, c->nres);
+            dmalloc(&c->d_res_slots, b, "resident mean slots");
+            SV_CUDA(cudaMemsetAsync(c->d_res_slots, 0, b, c->stream));
+        }
+        const unsigned long long epoch0 = c->res_epoch + 1;
+        c->res_epoch += (unsigned long long)reps + 1;  // rounds of this launch: reps (+1 spare)
         run(c, SV_K_MEAN, [&] {
             launch_mean_resident(c->dt, c->state, c->nres, ldexp(1.0, -c->n), with_oracle ? c->d_marked : nullptr,
-                                 with_oracle ? c->n_marked : 0, reps, c->d_partials, c->d_gbar, c->stream);
+                                 with_oracle ? c->n_marked : 0, reps, c->d_partials, c->d_gbar, c->d_res_slots,
+                                 epoch0, c->stream);
         });
         return;
     }
@@ -932,6 +942,7 @@ void destroy(sv_ctx *c) {
     cudaFree(c->d_sums);
     cudaFree(c->d_counter);
     cudaFree(c->d_gbar);
+    cudaFree(c->d_res_slots);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
