@@ -168,6 +168,8 @@ struct JitState {
     std::map<std::string, Entry> cache;
     std::deque<std::string> queue;     // sources waiting for the worker
     bool busy = false;
+    bool stop = false;                 // exit: the worker finishes its current job and returns
+    std::thread worker;                // joined at exit (no thread left running during teardown)
     uint64_t compiles = 0;             // kernels loaded for launches
     double compile_s = 0.0;            // NVRTC seconds (worker + synchronous)
 };
@@ -183,12 +185,17 @@ JitState &J() {
 #define g_compiles (J().compiles)
 #define g_compile_s (J().compile_s)
 
-// At exit: drop queued work and let a running compile finish, so NVRTC is not
-// torn down under the worker.
+// At exit: drop queued work, let a running compile finish and JOIN the
+// worker, so no thread of ours is alive while the CUDA runtime and NVRTC are
+// torn down (a parked detached worker crashed the process at exit).
 void drain_at_exit() {
-    std::unique_lock<std::mutex> lk(g_mu);
-    g_queue.clear();
-    g_cv.wait(lk, [] { return !g_busy; });
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_queue.clear();
+        J().stop = true;
+    }
+    g_cv.notify_all();
+    if (J().worker.joinable()) J().worker.join();
 }
 
 std::vector<char> compile_cubin(const std::string &src) {
@@ -252,7 +259,8 @@ void load_kernel(const std::vector<char> &cubin, cudaLibrary_t *lib, cudaKernel_
 void worker_main() {
     std::unique_lock<std::mutex> lk(g_mu);
     for (;;) {
-        g_cv.wait(lk, [] { return !g_queue.empty(); });
+        g_cv.wait(lk, [] { return !g_queue.empty() || J().stop; });
+        if (J().stop) return;
         const std::string src = g_queue.front();  // (moved out before the lock is released)
         g_queue.pop_front();
         g_busy = true;
@@ -293,7 +301,7 @@ void enqueue_locked(const std::string &src, int device) {
     static std::once_flag once;
     std::call_once(once, [] {
         std::atexit(drain_at_exit);
-        std::thread(worker_main).detach();
+        J().worker = std::thread(worker_main);
     });
     g_cache[src].device = device;  // QUEUED
     g_queue.push_back(src);
