@@ -268,14 +268,9 @@ void worker_main() {
         lk.unlock();
         std::vector<char> cubin;
         std::string err;
-        cudaLibrary_t lib = nullptr;
-        cudaKernel_t kern = nullptr;
+        (void)device;
         try {
-            cubin = timed_compile(src);
-            // load here, off the launch path: with CUDA's lazy module loading the
-            // first launch would otherwise pay the module load inside the pass
-            SV_CUDA(cudaSetDevice(device));
-            load_kernel(cubin, &lib, &kern);
+            cubin = timed_compile(src);  // NVRTC only: the worker makes no CUDA calls
         } catch (const Error &e) {
             err = e.msg;
         }
@@ -283,9 +278,6 @@ void worker_main() {
         Entry &e = g_cache[src];
         if (err.empty()) {
             e.cubin.swap(cubin);
-            e.lib = lib;
-            e.kern = kern;
-            ++g_compiles;
             e.state = Entry::READY;
         } else {
             e.err = err;
@@ -396,6 +388,19 @@ bool launch_gate_jit(const KParams &kp, const void *dev_ops, const void *host_op
                                  smem, s));
     }
     return true;
+}
+
+// Load every compiled-but-unloaded kernel on the calling thread (run_gates
+// calls this before its first launch, outside the launches' profiling events:
+// with CUDA's lazy module loading a first launch would otherwise pay the
+// module load inside the pass it times).  The background worker itself makes
+// no CUDA calls (a worker thread with CUDA state crashed the process at exit).
+void gate_jit_load_ready() {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto &kv : g_cache) {
+        Entry &e = kv.second;
+        if (e.state == Entry::READY && e.kern == nullptr) load_locked(e);
+    }
 }
 
 // NVRTC only (no device): the cubin size of the pass kernel, for host tests.

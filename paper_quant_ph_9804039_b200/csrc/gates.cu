@@ -37,6 +37,7 @@ bool launch_gate_jit(const KParams &kp, const void *dev_ops, const void *host_op
                      bool param, unsigned long long ntiles, cudaStream_t s);
 size_t gate_jit_compile_only(const void *host_ops, uint64_t nops, bool lin, bool glb);
 void gate_jit_stats(uint64_t *compiles, double *seconds, bool wait);
+void gate_jit_load_ready();
 
 // ------------------------------------------------------------------------- //
 // Host: op programs                                                          //

@@ -562,6 +562,7 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle, const Noise *noise = n
 void run_gates(sv_ctx *c, const sv_gate *gates, uint64_t count) {
     const GatePlan gp = plan_gates(c->n, c->g, c->dt, gates, count);
     if (gp.steps.empty()) return;
+    gate_jit_load_ready();  // kernels compiled in the background since the last call
     const int total_bits = c->emulated ? c->n : gp.nl;
     auto args = [&](const GateStep &st) {
         GatePassArgs a;

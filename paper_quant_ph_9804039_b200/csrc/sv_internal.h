@@ -201,6 +201,8 @@ uint64_t count_gate_relayouts(sv_dtype dt, const GatePassArgs &a);
 void launch_gate_pass(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, const void *host_ops, uint64_t nops,
                       bool has_lin, cudaStream_t s);
 void launch_gate_whole(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, uint64_t nops, cudaStream_t s);
+// gate_jit.cu: load the background-compiled pass kernels on this thread (host work, no launch).
+void gate_jit_load_ready();
 
 // ------------------------------------------------------------------------- //
 // Kernel launchers (wht.cu, mean.cu, misc.cu)                                //
