@@ -421,8 +421,8 @@ sv_status sv_debug_gate_relayouts(int n, int world, sv_dtype dtype, const sv_gat
 /* Gate engine, pass-specialised kernels (gate_jit.cu): with compile == 1,
  * generate and NVRTC-compile (no device needed) the kernel of every tile pass
  * sv_plan_gates gives the circuit on one complex64 GPU, in both program
- * flavours; *passes = passes compiled.  compile == 2: first wait until the
- * background compiler has drained its queue.  Always: *compiles /
+ * flavours; *passes = passes compiled.  (compile == 2 is accepted and, the
+ * automatic mode compiling synchronously, has nothing to wait for.)  Always: *compiles /
  * *compile_seconds = specialised kernels this process has loaded for
  * launches so far / NVRTC seconds spent (any pointer may be NULL).  Errors: SV_EINVAL (gates, dtype), SV_ECUDA (NVRTC
  * failure, with its log in sv_last_error()). */

@@ -347,8 +347,8 @@ def sv_debug_gate_relayouts(n: int, world: int, dtype: int, gates) -> np.ndarray
 
 
 def sv_debug_gate_jit(n: int = 0, dtype: int = SV_C64, gates=None, compile: int = 0) -> dict:
-    """Gate-engine JIT: compile=1 compiles every pass kernel of a circuit (host only); 2 waits for the
-    background compiler; always returns the launch-side counters."""
+    """Gate-engine JIT: compile=1 compiles every pass kernel of a circuit (host only); always returns
+    the launch-side counters (kernels compiled and loaded, NVRTC seconds)."""
     g = _gates(gates if gates is not None else np.zeros(0, dtype=GATE_DTYPE))
     p, c, t = _u64(), _u64(), ctypes.c_double()
     _check(lib.sv_debug_gate_jit(n, dtype, g.ctypes.data if g.size else None, g.size, int(compile), ctypes.byref(p),

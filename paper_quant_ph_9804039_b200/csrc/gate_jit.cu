@@ -29,13 +29,10 @@
 #include <string.h>
 
 #include <chrono>
-#include <condition_variable>
-#include <deque>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <string>
-#include <thread>
 #include <vector>
 
 #include "gate_kernels.cuh"
@@ -147,55 +144,32 @@ std::string generate(const GOp<float> *ops, uint64_t nops, bool lin, bool glb) {
     return b;
 }
 
-// One cache entry per distinct kernel source.  The automatic mode compiles in
-// the background (one worker thread) and keeps launching the interpreter
-// until the cubin is ready -- tiered, never blocking a call on NVRTC; the
-// library is loaded on the launching thread at first use.
+// One cache entry per distinct kernel source.  Tiering without a thread: the
+// automatic mode leaves a program's first call on the interpreter (a one-shot
+// circuit never waits for NVRTC) and compiles it, synchronously, when a
+// later call meets it again.  (A background compiler thread was tried: NVRTC's
+// lazily-constructed statics are destroyed by exit() while a compile can still
+// be running on it, which crashed processes at exit.)
 struct Entry {
-    enum State { QUEUED, READY, FAILED } state = QUEUED;
-    int device = 0;              // the device of the first request (the worker loads the module there)
-    std::vector<char> cubin;
+    enum State { SEEN, READY, FAILED } state = SEEN;
+    uint64_t call = 0;           // the run_gates call that first saw it (SEEN)
+    std::vector<char> cubin;     // kept alive for the library's lifetime
     std::string err;
     cudaLibrary_t lib = nullptr;
     cudaKernel_t kern = nullptr;
 };
 
-// Process-lifetime state, deliberately never destroyed: the detached worker
-// may still hold it while static destructors run at exit.
+// Process-lifetime state, deliberately never destroyed (no teardown order
+// against the CUDA runtime at exit).
 struct JitState {
     std::mutex mu;
-    std::condition_variable cv;        // worker wake-up / queue drained
     std::map<std::string, Entry> cache;
-    std::deque<std::string> queue;     // sources waiting for the worker
-    bool busy = false;
-    bool stop = false;                 // exit: the worker finishes its current job and returns
-    std::thread worker;                // joined at exit (no thread left running during teardown)
-    uint64_t compiles = 0;             // kernels loaded for launches
-    double compile_s = 0.0;            // NVRTC seconds (worker + synchronous)
+    uint64_t compiles = 0;             // kernels compiled and loaded for launches
+    double compile_s = 0.0;            // NVRTC seconds
 };
 JitState &J() {
     static JitState *j = new JitState;
     return *j;
-}
-#define g_mu (J().mu)
-#define g_cv (J().cv)
-#define g_cache (J().cache)
-#define g_queue (J().queue)
-#define g_busy (J().busy)
-#define g_compiles (J().compiles)
-#define g_compile_s (J().compile_s)
-
-// At exit: drop queued work, let a running compile finish and JOIN the
-// worker, so no thread of ours is alive while the CUDA runtime and NVRTC are
-// torn down (a parked detached worker crashed the process at exit).
-void drain_at_exit() {
-    {
-        std::lock_guard<std::mutex> lk(g_mu);
-        g_queue.clear();
-        J().stop = true;
-    }
-    g_cv.notify_all();
-    if (J().worker.joinable()) J().worker.join();
 }
 
 std::vector<char> compile_cubin(const std::string &src) {
@@ -238,82 +212,29 @@ std::vector<char> compile_cubin(const std::string &src) {
     return cubin;
 }
 
-std::vector<char> timed_compile(const std::string &src) {
+// Compile and load one entry on the calling thread.  Caller holds J().mu.
+void compile_load_locked(const std::string &src, Entry &e) {
     const auto t0 = std::chrono::steady_clock::now();
     std::vector<char> cubin = compile_cubin(src);
-    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    std::lock_guard<std::mutex> lk(g_mu);
-    g_compile_s += dt;
-    return cubin;
-}
-
-void load_kernel(const std::vector<char> &cubin, cudaLibrary_t *lib, cudaKernel_t *kern) {
-    SV_CUDA(cudaLibraryLoadData(lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
-    SV_CUDA(cudaLibraryGetKernel(kern, *lib, "sv_gate_jit"));
-    SV_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void *>(*kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
+    J().compile_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    e.cubin.swap(cubin);
+    SV_CUDA(cudaLibraryLoadData(&e.lib, e.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+    SV_CUDA(cudaLibraryGetKernel(&e.kern, e.lib, "sv_gate_jit"));
+    SV_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void *>(e.kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (1 << kGateTileBitsC64) * (int)sizeof(float2)));
-    cudaFuncAttributes fa{};  // forces the module into the current context now
-    SV_CUDA(cudaFuncGetAttributes(&fa, reinterpret_cast<const void *>(*kern)));
-}
-
-void worker_main() {
-    std::unique_lock<std::mutex> lk(g_mu);
-    for (;;) {
-        g_cv.wait(lk, [] { return !g_queue.empty() || J().stop; });
-        if (J().stop) return;
-        const std::string src = g_queue.front();  // (moved out before the lock is released)
-        g_queue.pop_front();
-        g_busy = true;
-        const int device = g_cache[src].device;
-        lk.unlock();
-        std::vector<char> cubin;
-        std::string err;
-        (void)device;
-        try {
-            cubin = timed_compile(src);  // NVRTC only: the worker makes no CUDA calls
-        } catch (const Error &e) {
-            err = e.msg;
-        }
-        lk.lock();
-        Entry &e = g_cache[src];
-        if (err.empty()) {
-            e.cubin.swap(cubin);
-            e.state = Entry::READY;
-        } else {
-            e.err = err;
-            e.state = Entry::FAILED;
-        }
-        g_busy = false;
-        g_cv.notify_all();
-    }
-}
-
-
-void enqueue_locked(const std::string &src, int device) {
-    static std::once_flag once;
-    std::call_once(once, [] {
-        std::atexit(drain_at_exit);
-        J().worker = std::thread(worker_main);
-    });
-    g_cache[src].device = device;  // QUEUED
-    g_queue.push_back(src);
-    g_cv.notify_all();
-}
-
-// Load a READY entry's cubin on this thread (forced mode).  Caller holds g_mu.
-void load_locked(Entry &e) {
-    load_kernel(e.cubin, &e.lib, &e.kern);
-    ++g_compiles;
+    cudaFuncAttributes fa{};  // forces the module into the current context now, not at the first launch
+    SV_CUDA(cudaFuncGetAttributes(&fa, reinterpret_cast<const void *>(e.kern)));
+    e.state = Entry::READY;
+    ++J().compiles;
 }
 
 }  // namespace
 
 // SV_GATE_JIT: "0" never, "1" every complex64 one-GPU pass, compiled before
 // its first launch (errors propagate), unset = passes of >= 2^11 tiles (states
-// of >= 2^24 amplitudes), compiled in the background on first sight while the
-// interpreter runs them (a one-shot circuit never waits for NVRTC; a repeated
-// one switches to the specialised kernel once it is ready); a compile failure
-// in the automatic mode leaves the pass on the interpreter.
+// of >= 2^24 amplitudes) from the second call that runs the same program on
+// (the first runs the interpreter); a compile failure in the automatic mode
+// leaves the pass on the interpreter.
 int gate_jit_mode() {
     const char *e = getenv("SV_GATE_JIT");
     if (!e) return 2;
@@ -324,54 +245,46 @@ std::string gate_jit_source(const void *host_ops, uint64_t nops, bool lin, bool 
     return generate(reinterpret_cast<const GOp<float> *>(host_ops), nops, lin, glb);
 }
 
-bool launch_gate_jit(const KParams &kp, const void *dev_ops, const void *host_ops, uint64_t nops, bool lin,
-                     bool param, unsigned long long ntiles, cudaStream_t s) {
+// Before a run_gates call launches anything (host work only; module loads
+// stay out of the passes' profiling events): decide and, where due, compile
+// this pass's kernel.  Returns the kernel to launch, or nullptr for the
+// interpreter.  `call` numbers the run_gates calls (>= 1).
+void *gate_jit_prepare(const void *host_ops, uint64_t nops, bool lin, bool param, unsigned long long ntiles,
+                       uint64_t call) {
     const int mode = gate_jit_mode();
-    if (mode == 0 || host_ops == nullptr) return false;
-    if (mode == 2 && ntiles < (1ull << 11)) return false;
+    if (mode == 0 || host_ops == nullptr) return nullptr;
+    if (mode == 2 && ntiles < (1ull << 11)) return nullptr;
     const std::string src = generate(reinterpret_cast<const GOp<float> *>(host_ops), nops, lin, !param);
-    cudaKernel_t kern = nullptr;
-    {
-        std::unique_lock<std::mutex> lk(g_mu);
-        auto it = g_cache.find(src);
-        if (mode == 1) {  // forced: compile now, errors propagate
-            if (it == g_cache.end() || it->second.state == Entry::FAILED) {
-                lk.unlock();
-                std::vector<char> cubin = timed_compile(src);
-                lk.lock();
-                Entry &e = g_cache[src];
-                if (e.state != Entry::READY) {
-                    e.cubin.swap(cubin);
-                    e.state = Entry::READY;
-                }
-                it = g_cache.find(src);
-            } else if (it->second.state == Entry::QUEUED) {
-                g_cv.wait(lk, [&] { return it->second.state != Entry::QUEUED; });
-                if (it->second.state == Entry::FAILED) throw Error{SV_ECUDA, it->second.err};
-            }
-        } else {  // automatic: queue it and run the interpreter until it is ready
-            if (it == g_cache.end()) {
-                int dev = 0;
-                SV_CUDA(cudaGetDevice(&dev));
-                enqueue_locked(src, dev);
-                return false;
-            }
-            if (it->second.state != Entry::READY) {
-                if (it->second.state == Entry::FAILED) {
-                    static bool warned = false;
-                    if (!warned) {
-                        fprintf(stderr, "libsv: gate JIT unavailable, using the interpreter kernel: %s\n",
-                                it->second.err.c_str());
-                        warned = true;
-                    }
-                }
-                return false;
-            }
-        }
-        Entry &e = it->second;
-        if (e.kern == nullptr) load_locked(e);
-        kern = e.kern;
+    std::lock_guard<std::mutex> lk(J().mu);
+    auto it = J().cache.find(src);
+    if (it == J().cache.end()) {
+        Entry &e = J().cache[src];
+        e.call = call;
+        if (mode == 2) return nullptr;  // first sight: the interpreter
+        compile_load_locked(src, e);    // forced: errors propagate
+        return e.kern;
     }
+    Entry &e = it->second;
+    if (e.state == Entry::READY) return e.kern;
+    if (e.state == Entry::SEEN && mode == 2 && e.call == call) return nullptr;  // again within the first call
+    if (e.state == Entry::FAILED && mode == 2) return nullptr;
+    if (mode == 1) {
+        compile_load_locked(src, e);
+        return e.kern;
+    }
+    try {  // automatic, second call: compile now; a failure keeps the interpreter
+        compile_load_locked(src, e);
+        return e.kern;
+    } catch (const Error &err) {
+        e.state = Entry::FAILED;
+        e.err = err.msg;
+        fprintf(stderr, "libsv: gate JIT unavailable, using the interpreter kernel: %s\n", e.err.c_str());
+        return nullptr;
+    }
+}
+
+void launch_gate_jit(void *kern, const KParams &kp, const void *dev_ops, const void *host_ops, uint64_t nops,
+                     bool lin, bool param, unsigned long long ntiles, cudaStream_t s) {
     KParams p = kp;
     int n = (int)nops;
     const int smem = (1 << kGateTileBitsC64) * (int)sizeof(float2);
@@ -379,27 +292,11 @@ bool launch_gate_jit(const KParams &kp, const void *dev_ops, const void *host_op
         auto prog = std::make_unique<GProg<float>>();
         memcpy(prog->op, host_ops, nops * sizeof(GOp<float>));
         void *args[] = {&p, prog.get(), &n};
-        SV_CUDA(cudaLaunchKernel(reinterpret_cast<const void *>(kern), dim3((unsigned int)ntiles), dim3(256), args,
-                                 smem, s));
+        SV_CUDA(cudaLaunchKernel(kern, dim3((unsigned int)ntiles), dim3(256), args, smem, s));
     } else {
         const void *ops = dev_ops;
         void *args[] = {&p, &ops, &n};
-        SV_CUDA(cudaLaunchKernel(reinterpret_cast<const void *>(kern), dim3((unsigned int)ntiles), dim3(256), args,
-                                 smem, s));
-    }
-    return true;
-}
-
-// Load every compiled-but-unloaded kernel on the calling thread (run_gates
-// calls this before its first launch, outside the launches' profiling events:
-// with CUDA's lazy module loading a first launch would otherwise pay the
-// module load inside the pass it times).  The background worker itself makes
-// no CUDA calls (a worker thread with CUDA state crashed the process at exit).
-void gate_jit_load_ready() {
-    std::lock_guard<std::mutex> lk(g_mu);
-    for (auto &kv : g_cache) {
-        Entry &e = kv.second;
-        if (e.state == Entry::READY && e.kern == nullptr) load_locked(e);
+        SV_CUDA(cudaLaunchKernel(kern, dim3((unsigned int)ntiles), dim3(256), args, smem, s));
     }
 }
 
@@ -408,11 +305,10 @@ size_t gate_jit_compile_only(const void *host_ops, uint64_t nops, bool lin, bool
     return compile_cubin(generate(reinterpret_cast<const GOp<float> *>(host_ops), nops, lin, glb)).size();
 }
 
-void gate_jit_stats(uint64_t *compiles, double *seconds, bool wait) {
-    std::unique_lock<std::mutex> lk(g_mu);
-    if (wait) g_cv.wait(lk, [] { return g_queue.empty() && !g_busy; });
-    if (compiles) *compiles = g_compiles;
-    if (seconds) *seconds = g_compile_s;
+void gate_jit_stats(uint64_t *compiles, double *seconds) {
+    std::lock_guard<std::mutex> lk(J().mu);
+    if (compiles) *compiles = J().compiles;
+    if (seconds) *seconds = J().compile_s;
 }
 
 }  // namespace sv

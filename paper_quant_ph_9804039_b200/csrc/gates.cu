@@ -33,11 +33,12 @@
 namespace sv {
 
 // gate_jit.cu: pass-specialised kernels compiled at run time (complex64, no exchange store)
-bool launch_gate_jit(const KParams &kp, const void *dev_ops, const void *host_ops, uint64_t nops, bool lin,
-                     bool param, unsigned long long ntiles, cudaStream_t s);
+void *gate_jit_prepare(const void *host_ops, uint64_t nops, bool lin, bool param, unsigned long long ntiles,
+                       uint64_t call);
+void launch_gate_jit(void *kern, const KParams &kp, const void *dev_ops, const void *host_ops, uint64_t nops,
+                     bool lin, bool param, unsigned long long ntiles, cudaStream_t s);
 size_t gate_jit_compile_only(const void *host_ops, uint64_t nops, bool lin, bool glb);
-void gate_jit_stats(uint64_t *compiles, double *seconds, bool wait);
-void gate_jit_load_ready();
+void gate_jit_stats(uint64_t *compiles, double *seconds);
 
 // ------------------------------------------------------------------------- //
 // Host: op programs                                                          //
@@ -366,8 +367,16 @@ void launch_tile_gates(const GatePassArgs &a, const void *dev_ops, const void *h
         // complex64, no exchange store: the pass-specialised kernel (bitwise the
         // interpreter's result; same program flavour for merged phase runs)
         const bool param = host_ops != nullptr && nops <= cap && gate_param_ops();
-        if (!kp.xchg && launch_gate_jit(kp, dev_ops, host_ops, nops, lin, param, ntiles, s)) return;
+        if (a.jit_prepare) {
+            if (!kp.xchg && a.jit_kern) *a.jit_kern = gate_jit_prepare(host_ops, nops, lin, param, ntiles, a.jit_prepare);
+            return;
+        }
+        if (!kp.xchg && a.jit_kern && *a.jit_kern) {
+            launch_gate_jit(*a.jit_kern, kp, dev_ops, host_ops, nops, lin, param, ntiles, s);
+            return;
+        }
     }
+    if (a.jit_prepare) return;
     if (host_ops != nullptr && nops <= cap && gate_param_ops()) {
         auto prog = std::make_unique<GProg<R>>();
         memcpy(prog->op, host_ops, nops * sizeof(GOp<R>));
@@ -498,7 +507,7 @@ extern "C" sv_status sv_debug_gate_jit(int n, sv_dtype dtype, const sv_gate *gat
             }
             if (passes) *passes = np;
         }
-        gate_jit_stats(compiles, compile_seconds, compile == 2);
+        gate_jit_stats(compiles, compile_seconds);
         set_error("");
         return SV_OK;
     } catch (const Error &e) {

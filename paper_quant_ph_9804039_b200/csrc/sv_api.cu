@@ -1,5 +1,6 @@
 // sv_api.cu -- the C ABI of include/sv.h: context, validation, dispatch of
 // the device schedule, NCCL plumbing, profiling.
+#include <atomic>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <nccl.h>
@@ -562,7 +563,6 @@ void run_wht_schedule(sv_ctx *c, int k, bool with_oracle, const Noise *noise = n
 void run_gates(sv_ctx *c, const sv_gate *gates, uint64_t count) {
     const GatePlan gp = plan_gates(c->n, c->g, c->dt, gates, count);
     if (gp.steps.empty()) return;
-    gate_jit_load_ready();  // kernels compiled in the background since the last call
     const int total_bits = c->emulated ? c->n : gp.nl;
     auto args = [&](const GateStep &st) {
         GatePassArgs a;
@@ -614,6 +614,21 @@ void run_gates(sv_ctx *c, const sv_gate *gates, uint64_t count) {
         SV_CUDA(cudaEventRecord(c->gprog_ev, c->stream));
         c->gprog_pending = true;
     }
+    // gate JIT: decide (and compile where due) every pass's specialised kernel
+    // before the first launch -- host work outside the passes' events
+    static std::atomic<uint64_t> calls{0};
+    const uint64_t call = ++calls;
+    std::vector<void *> jit(gp.steps.size(), nullptr);
+    for (size_t i = 0; i < gp.steps.size(); ++i) {
+        const GateStep &st = gp.steps[i];
+        if (st.kind != GSTEP_PASS) continue;
+        GatePassArgs a = args(st);
+        const bool pre_swap = i + 1 < gp.steps.size() && gp.steps[i + 1].kind == GSTEP_SWAP;
+        if (c->fused_xchg && pre_swap) continue;  // exchange-store passes keep the interpreter
+        a.jit_prepare = call;
+        a.jit_kern = &jit[i];
+        launch_gate_pass(c->dt, a, nullptr, prog.data() + where[i].first, where[i].second, lin[i] != 0, c->stream);
+    }
     void *cur = c->state, *next = nullptr;
     for (size_t i = 0; i < gp.steps.size(); ++i) {
         const GateStep &st = gp.steps[i];
@@ -654,6 +669,7 @@ void run_gates(sv_ctx *c, const sv_gate *gates, uint64_t count) {
                     a.xchg_dst[j] = to_recv ? c->peer_recv[j] : c->peer_state[j];
             }
         }
+        a.jit_kern = &jit[i];
         run(c, SV_K_GATE_TILE, [&] {
             launch_gate_pass(c->dt, a, ops, prog.data() + where[i].first, where[i].second, lin[i] != 0, c->stream);
         });

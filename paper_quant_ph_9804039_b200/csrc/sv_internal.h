@@ -185,6 +185,11 @@ struct GatePassArgs {
     // fused qubit-swap exchange as in PassArgs
     int xchg_nl = 0, xchg_g = 0, xchg_rank = -1;
     void *xchg_dst[8] = {};
+    // gate JIT (complex64, gate_jit.cu): jit_prepare = the run_gates call
+    // number -> decide / compile only, store the kernel (or nullptr) in
+    // *jit_kern, launch nothing; 0 -> launch *jit_kern if set, else the interpreter
+    uint64_t jit_prepare = 0;
+    void **jit_kern = nullptr;
 };
 // Append the op program of one pass (whole: the one-CTA kernel) to `prog`
 // (16-byte aligned records); returns the op count.  Ops whose rank-bit
@@ -201,8 +206,6 @@ uint64_t count_gate_relayouts(sv_dtype dt, const GatePassArgs &a);
 void launch_gate_pass(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, const void *host_ops, uint64_t nops,
                       bool has_lin, cudaStream_t s);
 void launch_gate_whole(sv_dtype dt, const GatePassArgs &a, const void *dev_ops, uint64_t nops, cudaStream_t s);
-// gate_jit.cu: load the background-compiled pass kernels on this thread (host work, no launch).
-void gate_jit_load_ready();
 
 // ------------------------------------------------------------------------- //
 // Kernel launchers (wht.cu, mean.cu, misc.cu)                                //

@@ -61,19 +61,19 @@ def test_jit_global_program_flavour(monkeypatch):
 
 def test_jit_automatic_at_large_states(monkeypatch):
     """Unset SV_GATE_JIT: passes of >= 2^11 tiles (n >= 24) run on the
-    interpreter while their specialised kernels compile in the background,
-    then switch; both runs agree bitwise and with the oracle."""
+    interpreter at a program's first call and on the specialised kernel, compiled
+    then, from the second; both runs agree bitwise and with the oracle."""
     monkeypatch.delenv("SV_GATE_JIT", raising=False)
     n = 24
     gates = C.random_circuit(n, 40, 8, max_controls=2)
     before = sv.sv_debug_gate_jit()["compiles"]
     with sv.sv_init(n, 3, sv.SV_C64, sv.SV_INIT_GAUSSIAN) as c:
         a0 = sv.sv_get_amplitudes(c).astype(np.complex128)
-        sv.sv_apply_gates(c, gates)  # first sight: interpreter, compiles queued
+        sv.sv_apply_gates(c, gates)  # first sight: interpreter, nothing compiled
         first = sv.sv_get_amplitudes(c)
-        sv.sv_debug_gate_jit(compile=2)  # wait for the background compiler
+        assert sv.sv_debug_gate_jit()["compiles"] == before
         sv.sv_set_amplitudes(c, a0)
-        sv.sv_apply_gates(c, gates)  # specialised kernels
+        sv.sv_apply_gates(c, gates)  # second call: compiled, specialised kernels
         second = sv.sv_get_amplitudes(c)
     assert sv.sv_debug_gate_jit()["compiles"] > before
     np.testing.assert_array_equal(first, second)

@@ -46,9 +46,9 @@ def main():
     with sv.sv_init(n, 1, sv.SV_C64, sv.SV_INIT_GAUSSIAN) as c:
         for name, gates in work.items():
             steps, _ = sv.sv_plan_gates(n, 1, sv.SV_C64, gates)
-            sv.sv_apply_gates(c, gates)  # warm-up (queues the passes' specialised kernels, gate_jit.cu)
+            for _ in range(2):  # warm-up: first call on the interpreter, the second compiles (gate_jit.cu)
+                sv.sv_apply_gates(c, gates)
             sv.sv_synchronize(c)
-            sv.sv_debug_gate_jit(compile=2)  # steady state: wait for the background compiler
             best = None
             for _ in range(args.reps):
                 sv.sv_profile(c, True)
