@@ -5,13 +5,14 @@
 // and returns the smallest index whose inclusive cumulative probability
 // exceeds u_s times the total.
 //
-// Device plan (three launches, fp64, fixed order => deterministic):
+// Device plan (five launches, fp64, fixed order => deterministic):
 //   1. chunk_sum_kernel: one warp per 4096-amplitude chunk, 32 rows of 128
 //      amplitudes; lane l of a row owns its 4 consecutive amplitudes 4l..4l+3
 //      and sums them in order, the row sum is a fixed xor-butterfly over the
 //      lanes, rows are accumulated in row order (HBM-bound read of the state,
 //      32-64 contiguous bytes per lane);
-//   2. chunk_scan_kernel: one block, exclusive prefix of the chunk sums;
+//   2. scan_partial / scan_offsets / scan_apply: exclusive prefix of the
+//      chunk sums in a fixed order (segments of 8192 sums per block);
 //   3. sample_kernel: one warp per shot, binary search over the chunk
 //      prefixes, then the chunk's rows in the SAME order as kernel 1 until the
 //      running sum passes the target; the crossing lane comes from an
@@ -30,6 +31,7 @@ constexpr int kSampChunk = 4096;        // amplitudes per chunk
 constexpr int kPerLane = SV_SAMP_PER_LANE;  // consecutive amplitudes per lane per row
 constexpr int kRowLen = 32 * kPerLane;  // 128 amplitudes per row
 constexpr int kRows = kSampChunk / kRowLen;
+inline uint64_t sample_chunks_impl(uint64_t N) { return (N + kSampChunk - 1) / kSampChunk; }
 #ifndef SV_SAMP_BATCH
 #define SV_SAMP_BATCH 8  // rows per batch of loads in the chunk-sum sweep
 #endif
@@ -118,28 +120,84 @@ __global__ void __launch_bounds__(256) chunk_sum_kernel(const E *a, uint64_t N, 
     }
 }
 
-// In place: sums -> exclusive prefix; total -> *total.  1024 threads, each a
-// contiguous segment (sequential), then a sequential scan of the 1024
-// segment totals by thread 0.
-__global__ void __launch_bounds__(1024) chunk_scan_kernel(double *sums, uint64_t nchunks, double *total) {
-    __shared__ double seg[1024];
-    const uint64_t per = (nchunks + blockDim.x - 1) / blockDim.x;
-    const uint64_t lo = threadIdx.x * per, hi = lo + per < nchunks ? lo + per : nchunks;
+// In place: sums -> exclusive prefix; total -> *total (fixed order, three
+// launches; round 1's single-block sequential scan of the 2^20 chunk sums of
+// an n = 32 state took ~1.8 ms, a quarter of the prefix phase).  Segments of
+// kScanSeg consecutive chunk sums, one 256-thread block each: thread t sums
+// its kScanPer consecutive values in order; the thread totals are scanned in
+// a fixed order (warp Hillis-Steele by shuffles, warp totals in order); the
+// segment totals are scanned sequentially by one thread; the apply pass
+// recomputes the same thread sums and writes every exclusive prefix.
+constexpr int kScanPer = 32;
+constexpr int kScanThreads = 256;
+constexpr uint64_t kScanSeg = (uint64_t)kScanPer * kScanThreads;  // 8192 chunk sums per segment
+
+uint64_t sample_scan_blocks(uint64_t N) { return (sample_chunks_impl(N) + kScanSeg - 1) / kScanSeg; }
+
+// The thread's kScanPer values in order (0 beyond n).
+__device__ __forceinline__ double scan_thread_sum(const double *sums, uint64_t lo, uint64_t n) {
     double s = 0.0;
-    for (uint64_t i = lo; i < hi; ++i) s = __dadd_rn(s, sums[i]);
-    seg[threadIdx.x] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double run = 0.0;
-        for (unsigned t = 0; t < blockDim.x; ++t) {
-            const double v = seg[t];
-            seg[t] = run;
-            run = __dadd_rn(run, v);
+    if (lo + kScanPer <= n) {
+#pragma unroll
+        for (int h = 0; h < kScanPer / 2; ++h) {
+            const double2 v = __ldcg(reinterpret_cast<const double2 *>(sums + lo) + h);
+            s = __dadd_rn(s, v.x);
+            s = __dadd_rn(s, v.y);
         }
-        *total = run;
+    } else {
+        for (uint64_t i = lo; i < n; ++i) s = __dadd_rn(s, sums[i]);
     }
+    return s;
+}
+
+// Exclusive prefix of v over the block's threads (fixed order) and the block total.
+__device__ __forceinline__ double scan_block_exclusive(double v, double &total) {
+    __shared__ double s_w[kScanThreads / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc = __dadd_rn(inc, u);
+    }
+    if (lane == 31) s_w[w] = inc;
     __syncthreads();
-    double run = seg[threadIdx.x];
+    double woff = 0.0, tot = 0.0;
+#pragma unroll
+    for (int i = 0; i < kScanThreads / 32; ++i) {
+        if (i == w) woff = tot;
+        tot = __dadd_rn(tot, s_w[i]);
+    }
+    total = tot;
+    double exc = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) exc = 0.0;
+    return __dadd_rn(woff, exc);
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_partial_kernel(const double *sums, uint64_t n, double *bsum) {
+    const uint64_t lo = blockIdx.x * kScanSeg + (uint64_t)threadIdx.x * kScanPer;
+    double total;
+    (void)scan_block_exclusive(scan_thread_sum(sums, lo, n), total);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+}
+
+// One thread: the segment totals -> exclusive offsets (in order), total.
+__global__ void scan_offsets_kernel(double *bsum, uint64_t nb, double *total) {
+    double run = 0.0;
+    for (uint64_t b = 0; b < nb; ++b) {
+        const double v = bsum[b];
+        bsum[b] = run;
+        run = __dadd_rn(run, v);
+    }
+    *total = run;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(double *sums, uint64_t n, const double *boff) {
+    const uint64_t lo = blockIdx.x * kScanSeg + (uint64_t)threadIdx.x * kScanPer;
+    double total;
+    const double exc = scan_block_exclusive(scan_thread_sum(sums, lo, n), total);
+    double run = __dadd_rn(boff[blockIdx.x], exc);  // (each thread rewrites only the values it read)
+    const uint64_t hi = lo + kScanPer < n ? lo + kScanPer : n;
     for (uint64_t i = lo; i < hi; ++i) {
         const double v = sums[i];
         sums[i] = run;
@@ -239,16 +297,22 @@ __global__ void __launch_bounds__(256) sample_kernel(const E *a, uint64_t N, con
     }
 }
 
-uint64_t sample_chunks(uint64_t N) { return (N + kSampChunk - 1) / kSampChunk; }
+uint64_t sample_chunks(uint64_t N) { return sample_chunks_impl(N); }
 
 void launch_sample_prefix(sv_dtype dt, const void *a, uint64_t N, double *scratch, double *rank_total,
-                          cudaStream_t s) {
+                          double *bscratch, cudaStream_t s) {
     const uint64_t nch = sample_chunks(N);
     const unsigned g1 = (unsigned)((nch + 7) / 8 < 148 * 64 ? (nch + 7) / 8 : 148 * 64);
     if (dt == SV_C64) chunk_sum_kernel<float2><<<g1, 256, 0, s>>>((const float2 *)a, N, scratch, nch);
     else chunk_sum_kernel<double2><<<g1, 256, 0, s>>>((const double2 *)a, N, scratch, nch);
     SV_CUDA(cudaGetLastError());
-    chunk_scan_kernel<<<1, 1024, 0, s>>>(scratch, nch, rank_total);
+    const uint64_t nb = (nch + kScanSeg - 1) / kScanSeg;
+    SV_CHECK(nb <= 0x7fffffffull, SV_EINVAL, "internal: too many scan segments");
+    scan_partial_kernel<<<(unsigned)nb, kScanThreads, 0, s>>>(scratch, nch, bscratch);
+    SV_CUDA(cudaGetLastError());
+    scan_offsets_kernel<<<1, 1, 0, s>>>(bscratch, nb, rank_total);
+    SV_CUDA(cudaGetLastError());
+    scan_apply_kernel<<<(unsigned)nb, kScanThreads, 0, s>>>(scratch, nch, bscratch);
     SV_CUDA(cudaGetLastError());
 }
 

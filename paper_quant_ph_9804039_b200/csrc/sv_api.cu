@@ -1183,10 +1183,13 @@ sv_status sv_sample(sv_ctx *c, uint64_t shots, uint64_t seed, uint64_t *out, int
         const uint64_t nch = sample_chunks(c->nres);
         const int world = c->comm ? c->world : 1;
         const int rank = c->comm ? c->rank : 0;
-        // chunk prefixes [nch], every rank's total [world], window [3]
-        if (!c->d_samp) dmalloc((void **)&c->d_samp, (nch + (size_t)world + 3) * sizeof(double), "sampler scratch");
+        // chunk prefixes [nch], every rank's total [world], window [3], scan segments [nb]
+        const uint64_t nb = sample_scan_blocks(c->nres);
+        if (!c->d_samp)
+            dmalloc((void **)&c->d_samp, (nch + (size_t)world + 3 + nb) * sizeof(double), "sampler scratch");
         double *totals = c->d_samp + nch;  // [world]
         double *g = totals + world;         // window {global total, own offset, next rank's offset}
+        double *bscr = g + 3;               // [nb]
         uint64_t *dout = out;
         if (!out_on_device) {
             if (shots > c->shots_cap) {
@@ -1200,7 +1203,7 @@ sv_status sv_sample(sv_ctx *c, uint64_t shots, uint64_t seed, uint64_t *out, int
         }
         const uint64_t key = hash64(seed ^ 0x53414D5000000000ull);  // "SAMP" (G21)
         run(c, SV_K_READOUT, [&] {
-            launch_sample_prefix(c->dt, c->state, c->nres, c->d_samp, totals + rank, c->stream);
+            launch_sample_prefix(c->dt, c->state, c->nres, c->d_samp, totals + rank, bscr, c->stream);
         });
         if (c->comm) {  // every rank's total, in rank order
             run(c, SV_K_ALLREDUCE, [&] {
