@@ -377,7 +377,8 @@ def run_ours(args):
     kdesc = {"wht_tile": "wht_tile_kernel / wht_tile2_kernel",
              "mean": ("mean_resident_kernel (state held in shared memory for all k iterations; "
                       "bytes = 2 S per iteration, served on-chip)") if resident else "mean_kernel",
-             "wht_whole": "whole_state_kernel (one CTA on one SM, state in shared memory)"}[kname]
+             "wht_whole": "whole_reg_kernel (one CTA on one SM, state in the registers of 8 warps; "
+                          "whole_state_kernel in shared memory below n = 9)"}[kname]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": ncu_traffic(args.config, world), "kernel": f"{kname} ({kdesc})",
                 "algorithmic_bytes_per_launch": algo_bytes, "launches": launches, "avg_launch_ms": 1e3 * avg_s,
@@ -398,8 +399,8 @@ def run_ours(args):
                                     "each iteration also waits on one grid-wide barrier (latency-bound: "
                                     "us_per_iteration)")}
     if kname == "wht_whole":
-        # one CTA on one SM, state in shared memory: the bound is that SM's
-        # add rate -- k iterations x 2n stages x N/2 butterflies x 4 real adds
+        # one CTA on one SM (state in registers / shared memory): the bound is
+        # that SM's add rate -- k iterations x 2n stages x N/2 butterflies x 4 real adds
         flops = k * 2 * n * (N_amp // 2) * 4
         lanes = 64 if dtype == sv.SV_C128 else 128  # FP64 / FP32 lanes per SM (B200: 37 / 74 TFLOP/s over 148 SMs)
         peak_g = lanes * 1.965  # GFLOP/s of adds at the 1965 MHz max SM clock

@@ -264,21 +264,24 @@ __global__ void __launch_bounds__(512) whole_state_kernel(E *a, int n, int k, in
 }
 
 // ------------------------------------------------------------------------- //
-// Whole state in the REGISTERS of 4 warps (n = LOGR + 7, round 2): 2^LOGR    //
-// amplitudes per thread.  Index bits [0, LOGR) are register bits (stages in  //
-// registers), [LOGR, LOGR + 5) lane bits (stages by warp shuffles: lane with //
-// the bit clear forms x + y, its partner y' - x' = a_i - a_j, the same two   //
-// sums as the pair butterfly), the top 2 warp bits go through ONE shared-    //
-// memory relayout per transform (layout B makes them register bits).  The    //
-// CTA barriers per iteration drop from ~22 (two stages per shared-memory     //
-// round trip, whole_state_kernel) to 4.                                       //
+// Whole state in the REGISTERS of 2^LOGW warps (n = LOGR + 5 + LOGW): 2^LOGR //
+// amplitudes per thread.  Layout A: index = tid * 2^LOGR + r -- the register //
+// bits [0, LOGR) and the lane bits [LOGR, LOGR + 5) run in registers and by  //
+// warp shuffles (the lane with the bit clear forms x + y, its partner        //
+// y' - x' = a_i - a_j: the pair butterfly's two sums).  Layout B (one        //
+// shared-memory relayout away): r = the top LOGR index bits, lane = the 5    //
+// below, warp = the lowest LOGW -- the warp bits of A, [LOGR + 5, n), are    //
+// register or lane bits there.  A transform visits A then B, the next one B  //
+// then A (stages on different bits commute, G18), so each transform costs    //
+// ONE relayout and barrier; F0 runs in B, O in A.  Round 2 widened it from 4 //
+// warps (1 warp per SMSP: issue stalled on every dependency) to 8-16.        //
 // ------------------------------------------------------------------------- //
-template <typename E, typename R>
+template <typename E, typename R, bool GEN>
 __device__ __forceinline__ void shfl_stage(E &x, int d, bool hi, const double *c) {
     E y;
     y.x = __shfl_xor_sync(0xffffffffu, x.x, d);
     y.y = __shfl_xor_sync(0xffffffffu, x.y, d);
-    if (c == nullptr) {  // ideal butterfly: (a_i, a_j) -> (a_i + a_j, a_i - a_j)
+    if constexpr (!GEN) {  // ideal butterfly: (a_i, a_j) -> (a_i + a_j, a_i - a_j)
         if (!hi) { x.x = x.x + y.x; x.y = x.y + y.y; }
         else { x.x = y.x - x.x; x.y = y.y - x.y; }
     } else {  // Fig. 3's [w x; y z]: a_i' = w a_i + x a_j, a_j' = y a_i + z a_j
@@ -288,65 +291,86 @@ __device__ __forceinline__ void shfl_stage(E &x, int d, bool hi, const double *c
     }
 }
 
-template <int LOGR>
-__device__ __forceinline__ unsigned int wr_pad(unsigned int i) { return i + (i >> LOGR); }  // conflict-free rows
-// layout A: index = tid * 2^LOGR + r; layout B: register bits 0-1 = the two
-// warp (top) bits, register bits 2.. = index bits 0 .., thread bits = index
-// bits LOGR - 2 .. LOGR + 4
-template <int LOGR>
-__device__ __forceinline__ unsigned int wr_idxA(int tid, int r) { return ((unsigned int)tid << LOGR) | (unsigned int)r; }
-template <int LOGR>
-__device__ __forceinline__ unsigned int wr_idxB(int tid, int r) {
-    return ((unsigned int)(r & 3) << (LOGR + 5)) | ((unsigned int)r >> 2) | ((unsigned int)tid << (LOGR - 2));
-}
+template <typename E, int LOGR, int LOGW>
+struct WR {
+    static constexpr int NR = 1 << LOGR, NT = 32 << LOGW, n = LOGR + 5 + LOGW;
+    static_assert(LOGW >= 2 && LOGW <= LOGR + 5, "layout B must hold A's warp bits in registers and lanes");
+    // XOR swizzle of the shared-memory index: every quarter-warp (16-B
+    // elements) / half-warp (8-B) access of both layouts is bank-conflict free
+    // (brute-force checked for every instantiated (LOGR, LOGW))
+    static constexpr uint32_t M = sizeof(E) == 16 ? 7u : 15u;
+    static constexpr int S1 = (sizeof(E) == 8 && LOGR == 6 && LOGW == 2) ? 2 : 1;
+    static constexpr int S2 = LOGR > LOGW ? LOGR : LOGW;
+    __device__ static __forceinline__ uint32_t swz(uint32_t i) { return i ^ ((i >> S1) & M) ^ ((i >> S2) & M); }
+    __device__ static __forceinline__ uint32_t idxA(int tid, int r) { return ((uint32_t)tid << LOGR) | (uint32_t)r; }
+    __device__ static __forceinline__ uint32_t idxB(int tid, int r) {
+        return ((uint32_t)r << (n - LOGR)) | ((uint32_t)(tid & 31) << (n - LOGR - 5)) | ((uint32_t)tid >> 5);
+    }
+};
 
-template <typename E, int LOGR>
-__device__ __forceinline__ void wr_transform(E (&x)[1 << LOGR], E *s, int tid, const double *cbase) {
+// Stages of layout A: index bits [0, LOGR + 5).
+template <typename E, int LOGR, int LOGW, bool GEN>
+__device__ __forceinline__ void wr_stages_a(E (&x)[1 << LOGR], int lane, const double *cbase) {
     using R = typename RealOf<E>::T;
     constexpr int NR = 1 << LOGR;
-    const int lane = tid & 31;
 #pragma unroll
     for (int q = 0; q < LOGR; ++q) {
-        const double *c = cbase ? cbase + 4 * q : nullptr;
 #pragma unroll
         for (int j = 0; j < NR; ++j)
             if (!(j & (1 << q))) {
-                if (c) bfly_gen(x[j], x[j | (1 << q)], c);
+                if constexpr (GEN) bfly_gen(x[j], x[j | (1 << q)], cbase + 4 * q);
                 else bfly(x[j], x[j | (1 << q)]);
             }
     }
 #pragma unroll
     for (int b = 0; b < 5; ++b) {
-        const double *c = cbase ? cbase + 4 * (LOGR + b) : nullptr;
         const bool hi = (lane >> b) & 1;
 #pragma unroll
-        for (int j = 0; j < NR; ++j) shfl_stage<E, R>(x[j], 1 << b, hi, c);
+        for (int j = 0; j < NR; ++j) shfl_stage<E, R, GEN>(x[j], 1 << b, hi, GEN ? cbase + 4 * (LOGR + b) : nullptr);
     }
-    // warp bits: relayout A -> B (each thread then rewrites only what it read: one barrier each way)
+}
+
+// Stages of layout B: index bits [LOGR + 5, n) -- register bits at the top,
+// lane bits below them.
+template <typename E, int LOGR, int LOGW, bool GEN>
+__device__ __forceinline__ void wr_stages_b(E (&x)[1 << LOGR], int lane, const double *cbase) {
+    using R = typename RealOf<E>::T;
+    constexpr int NR = 1 << LOGR, n = LOGR + 5 + LOGW;
 #pragma unroll
-    for (int r = 0; r < NR; ++r) s[wr_pad<LOGR>(wr_idxA<LOGR>(tid, r))] = x[r];
+    for (int t = LOGR + 5; t < n; ++t) {
+        if (t >= n - LOGR) {
+            const int q = t - (n - LOGR);
+#pragma unroll
+            for (int j = 0; j < NR; ++j)
+                if (!(j & (1 << q))) {
+                    if constexpr (GEN) bfly_gen(x[j], x[j | (1 << q)], cbase + 4 * t);
+                    else bfly(x[j], x[j | (1 << q)]);
+                }
+        } else {
+            const int b = t - (n - LOGR - 5);
+            const bool hi = (lane >> b) & 1;
+#pragma unroll
+            for (int j = 0; j < NR; ++j) shfl_stage<E, R, GEN>(x[j], 1 << b, hi, GEN ? cbase + 4 * t : nullptr);
+        }
+    }
+}
+
+// Relayout A -> B (TO_B) or B -> A through the swizzled tile: each thread
+// rewrites only the positions it read in the previous relayout, so one
+// barrier per change suffices.
+template <typename E, int LOGR, int LOGW, bool TO_B>
+__device__ __forceinline__ void wr_relayout(E (&x)[1 << LOGR], E *s, int tid) {
+    using W = WR<E, LOGR, LOGW>;
+#pragma unroll
+    for (int r = 0; r < W::NR; ++r) s[W::swz(TO_B ? W::idxA(tid, r) : W::idxB(tid, r))] = x[r];
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < NR; ++r) x[r] = s[wr_pad<LOGR>(wr_idxB<LOGR>(tid, r))];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        const double *c = cbase ? cbase + 4 * (LOGR + 5 + q) : nullptr;
-#pragma unroll
-        for (int j = 0; j < NR; ++j)
-            if (!(j & (1 << q))) {
-                if (c) bfly_gen(x[j], x[j | (1 << q)], c);
-                else bfly(x[j], x[j | (1 << q)]);
-            }
-    }
-#pragma unroll
-    for (int r = 0; r < NR; ++r) s[wr_pad<LOGR>(wr_idxB<LOGR>(tid, r))] = x[r];
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < NR; ++r) x[r] = s[wr_pad<LOGR>(wr_idxA<LOGR>(tid, r))];
+    for (int r = 0; r < W::NR; ++r) x[r] = s[W::swz(TO_B ? W::idxB(tid, r) : W::idxA(tid, r))];
 }
 
 // fixed-order CTA sums: the thread's values in register order, a warp xor
-// butterfly (every lane ends with bitwise the same value), the 4 warps in order
+// butterfly (every lane ends with bitwise the same value), the warps in order
+template <int NW>
 __device__ __forceinline__ void wr_cta_sum2(double re, double im, double &tre, double &tim, double *red, int tid) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -355,30 +379,33 @@ __device__ __forceinline__ void wr_cta_sum2(double re, double im, double &tre, d
     }
     if ((tid & 31) == 0) { red[2 * (tid >> 5)] = re; red[2 * (tid >> 5) + 1] = im; }
     __syncthreads();
-    tre = red[0] + red[2] + red[4] + red[6];
-    tim = red[1] + red[3] + red[5] + red[7];
+    tre = 0.0;
+    tim = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) { tre += red[2 * w]; tim += red[2 * w + 1]; }
     __syncthreads();  // red reused
 }
 
-template <typename E, int LOGR>
-__global__ void __launch_bounds__(128) whole_reg_kernel(E *a, int k, int with_oracle, int diffusion,
-                                                        const unsigned long long *marked, unsigned long long m,
-                                                        double f0_scale, const double *coefs, double *survival) {
+template <typename E, int LOGR, int LOGW, bool GEN>
+__global__ void __launch_bounds__(32 << LOGW) whole_reg_kernel(E *a, int k, int with_oracle, int diffusion,
+                                                               const unsigned long long *marked, unsigned long long m,
+                                                               double f0_scale, const double *coefs, double *survival) {
     using R = typename RealOf<E>::T;
-    constexpr int NR = 1 << LOGR, n = LOGR + 7;
+    using W = WR<E, LOGR, LOGW>;
+    constexpr int NR = W::NR, n = W::n;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     E *s = reinterpret_cast<E *>(smem_raw);
-    __shared__ double red[2 * 4];
-    const int tid = threadIdx.x;
+    __shared__ double red[2 * (1 << LOGW)];
+    const int tid = threadIdx.x, lane = tid & 31;
     __shared__ unsigned long long s_mk[64];  // the marked set, when it is small, read once
     E x[NR];
 #pragma unroll
-    for (int r = 0; r < NR; ++r) x[r] = a[wr_idxA<LOGR>(tid, r)];
+    for (int r = 0; r < NR; ++r) x[r] = a[W::idxA(tid, r)];
     const bool mk_smem = with_oracle && m <= 64;
     if (mk_smem && tid < (int)m) s_mk[tid] = marked[tid];
     __syncthreads();
     for (int it = 0; it < k; ++it) {
-        if (with_oracle) {
+        if (with_oracle) {  // layout A
             for (unsigned long long j = 0; j < m; ++j) {
                 const unsigned long long mk = mk_smem ? s_mk[j] : marked[j];
                 if ((int)(mk >> LOGR) == tid) {
@@ -390,18 +417,25 @@ __global__ void __launch_bounds__(128) whole_reg_kernel(E *a, int k, int with_or
             }
         }
         if (diffusion == SV_DIFFUSE_WHT) {
-            wr_transform<E, LOGR>(x, s, tid, coefs ? coefs + (size_t)(2 * it) * n * 4 : nullptr);
-            // F0 = 2|0><0| - I with the 2^-n of the unnormalised transforms (G2, G5)
+            const double *c1 = GEN ? coefs + (size_t)(2 * it) * n * 4 : nullptr;
+            const double *c2 = GEN ? coefs + (size_t)(2 * it + 1) * n * 4 : nullptr;
+            wr_stages_a<E, LOGR, LOGW, GEN>(x, lane, c1);
+            wr_relayout<E, LOGR, LOGW, true>(x, s, tid);
+            wr_stages_b<E, LOGR, LOGW, GEN>(x, lane, c1);
+            // F0 = 2|0><0| - I with the 2^-n of the unnormalised transforms (G2, G5);
+            // index 0 is thread 0's register 0 in both layouts
 #pragma unroll
             for (int r = 0; r < NR; ++r) scale(x[r], (R)(-f0_scale));
             if (tid == 0) { x[0].x = -x[0].x; x[0].y = -x[0].y; }
-            wr_transform<E, LOGR>(x, s, tid, coefs ? coefs + (size_t)(2 * it + 1) * n * 4 : nullptr);
+            wr_stages_b<E, LOGR, LOGW, GEN>(x, lane, c2);
+            wr_relayout<E, LOGR, LOGW, false>(x, s, tid);
+            wr_stages_a<E, LOGR, LOGW, GEN>(x, lane, c2);
             if (survival) {  // renormalise (G22): sum |a|^2 in fixed order, record it, scale to norm 1
                 double sq = 0.0;
 #pragma unroll
                 for (int r = 0; r < NR; ++r) sq += (double)x[r].x * (double)x[r].x + (double)x[r].y * (double)x[r].y;
                 double tot, dummy;
-                wr_cta_sum2(sq, 0.0, tot, dummy, red, tid);
+                wr_cta_sum2<1 << LOGW>(sq, 0.0, tot, dummy, red, tid);
                 if (tid == 0) survival[it] = tot;
                 const R inv = (R)(1.0 / sqrt(tot));
 #pragma unroll
@@ -412,24 +446,38 @@ __global__ void __launch_bounds__(128) whole_reg_kernel(E *a, int k, int with_or
 #pragma unroll
             for (int r = 0; r < NR; ++r) { re += (double)x[r].x; im += (double)x[r].y; }
             double mr, mi;
-            wr_cta_sum2(re, im, mr, mi, red, tid);
+            wr_cta_sum2<1 << LOGW>(re, im, mr, mi, red, tid);
             const R two_mr = (R)(2.0 * mr * f0_scale), two_mi = (R)(2.0 * mi * f0_scale);
 #pragma unroll
             for (int r = 0; r < NR; ++r) { x[r].x = two_mr - x[r].x; x[r].y = two_mi - x[r].y; }
         }
     }
 #pragma unroll
-    for (int r = 0; r < NR; ++r) a[wr_idxA<LOGR>(tid, r)] = x[r];
+    for (int r = 0; r < NR; ++r) a[W::idxA(tid, r)] = x[r];
 }
 
-template <typename E, int LOGR>
+template <typename E, int LOGR, int LOGW>
 static void launch_whole_reg(E *state, int k, int with_oracle, int diffusion, const unsigned long long *mk,
                              uint64_t m, double f0, const double *coefs, double *survival, cudaStream_t s) {
-    const unsigned int N = 1u << (LOGR + 7);
-    const int smem = (int)((N + (N >> LOGR)) * sizeof(E));
-    SV_CUDA(cudaFuncSetAttribute(whole_reg_kernel<E, LOGR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    whole_reg_kernel<E, LOGR><<<1, 128, smem, s>>>(state, k, with_oracle, diffusion, mk, m, f0, coefs, survival);
+    const int smem = (int)((1u << (LOGR + 5 + LOGW)) * sizeof(E));
+    auto kern = coefs ? whole_reg_kernel<E, LOGR, LOGW, true> : whole_reg_kernel<E, LOGR, LOGW, false>;
+    SV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<1, 32 << LOGW, smem, s>>>(state, k, with_oracle, diffusion, mk, m, f0, coefs, survival);
     SV_CUDA(cudaGetLastError());
+}
+
+// Warp bits of the register kernel per (dtype, n): SV_WHOLE_W=<LOGW> picks
+// another instantiated split (tools/whole_state_bench.py).
+static int whole_reg_logw(bool c64, int n) {
+    static const int forced = [] {
+        const char *e = getenv("SV_WHOLE_W");
+        return e ? atoi(e) : 0;
+    }();
+    if (forced) return forced;
+    // measured (profiles/r2_whole_state_bench.txt): 4 warps at n = 9, 8 up to
+    // n = 12, 16 for complex64 n = 13
+    (void)c64;
+    return n <= 9 ? 2 : n <= 12 ? 3 : 4;
 }
 
 #ifndef SV_WHOLE_REG
@@ -439,29 +487,23 @@ static void launch_whole_reg(E *state, int k, int with_oracle, int diffusion, co
 void launch_whole_state(sv_dtype dt, void *state, int n, int k, int with_oracle, int diffusion,
                         const uint64_t *marked, uint64_t m, cudaStream_t s, const double *coefs, double *survival) {
     const unsigned int N = 1u << n;
-    if (SV_WHOLE_REG && n >= 9) {  // the register-resident kernel (n = 9 .. T)
+    if (SV_WHOLE_REG && n >= 9 && (dt == SV_C64 ? n <= 13 : n <= 12)) {  // the register-resident kernel
         const double f0r = coefs ? 1.0 : ldexp(1.0, -n);
         SV_CHECK(!coefs || diffusion == SV_DIFFUSE_WHT, SV_EINVAL, "internal: angle errors need the WHT diffusion");
         const auto mkr = reinterpret_cast<const unsigned long long *>(marked);
+        const int w = whole_reg_logw(dt == SV_C64, n);
+#define SV_WR(E, LR, LW) \
+    if (n == LR + 5 + LW && w == LW) \
+        return launch_whole_reg<E, LR, LW>(reinterpret_cast<E *>(state), k, with_oracle, diffusion, mkr, m, f0r, coefs, survival, s)
         if (dt == SV_C64) {
-            float2 *st = reinterpret_cast<float2 *>(state);
-            switch (n) {
-                case 9: return launch_whole_reg<float2, 2>(st, k, with_oracle, diffusion, mkr, m, f0r, coefs, survival, s);
-                case 10: return launch_whole_reg<float2, 3>(st, k, with_oracle, diffusion, mkr, m, f0r, coefs, survival, s);
-                case 11: return launch_whole_reg<float2, 4>(st, k, with_oracle, diffusion, mkr, m, f0r, coefs, survival, s);
-                case 12: return launch_whole_reg<float2, 5>(st, k, with_oracle, diffusion, mkr, m, f0r, coefs, survival, s);
-                case 13: return launch_whole_reg<float2, 6>(st, k, with_oracle, diffusion, mkr, m, f0r, coefs, survival, s);
-                default: break;
-            }
+            SV_WR(float2, 2, 2); SV_WR(float2, 3, 2); SV_WR(float2, 2, 3); SV_WR(float2, 4, 2); SV_WR(float2, 3, 3);
+            SV_WR(float2, 2, 4); SV_WR(float2, 5, 2); SV_WR(float2, 4, 3); SV_WR(float2, 3, 4); SV_WR(float2, 6, 2);
+            SV_WR(float2, 5, 3); SV_WR(float2, 4, 4);
         } else {
-            double2 *st = reinterpret_cast<double2 *>(state);
-            switch (n) {  // (n = 12: 32 amplitudes per thread measured 2x slower than whole_state_kernel)
-                case 9: return launch_whole_reg<double2, 2>(st, k, with_oracle, diffusion, mkr, m, f0r, coefs, survival, s);
-                case 10: return launch_whole_reg<double2, 3>(st, k, with_oracle, diffusion, mkr, m, f0r, coefs, survival, s);
-                case 11: return launch_whole_reg<double2, 4>(st, k, with_oracle, diffusion, mkr, m, f0r, coefs, survival, s);
-                default: break;
-            }
+            SV_WR(double2, 2, 2); SV_WR(double2, 3, 2); SV_WR(double2, 2, 3); SV_WR(double2, 4, 2); SV_WR(double2, 3, 3);
+            SV_WR(double2, 2, 4); SV_WR(double2, 4, 3); SV_WR(double2, 3, 4);
         }
+#undef SV_WR
     }
     const int threads = N >= 1024 ? 512 : (N / 2 >= 32 ? (int)(N / 2) : 32);
     const double f0 = coefs ? 1.0 : ldexp(1.0, -n);
