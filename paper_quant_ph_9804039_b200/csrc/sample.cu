@@ -10,14 +10,16 @@
 //      amplitudes; lane l of a row owns its 4 consecutive amplitudes 4l..4l+3
 //      and sums them in order, the row sum is a fixed xor-butterfly over the
 //      lanes, rows are accumulated in row order (HBM-bound read of the state,
-//      32-64 contiguous bytes per lane);
+//      32-64 contiguous bytes per lane); it also stores each row's
+//      chunk-local exclusive running sum (32 doubles per chunk);
 //   2. scan_partial / scan_offsets / scan_apply: exclusive prefix of the
 //      chunk sums in a fixed order (segments of 8192 sums per block);
 //   3. sample_kernel: one warp per shot, binary search over the chunk
-//      prefixes, then the chunk's rows in the SAME order as kernel 1 until the
-//      running sum passes the target; the crossing lane comes from an
-//      inclusive warp scan of the lane sums, the amplitude from that lane's
-//      4 in order.
+//      prefixes, the row from the chunk's 32 row starts (prefix + row
+//      running sum, one ballot), then rows from there in kernel 1's order
+//      until the running sum passes the target; the crossing lane comes from
+//      an inclusive warp scan of the lane sums, the amplitude from that
+//      lane's 4 in order.
 #include <cuda_runtime.h>
 
 #include "sv_internal.h"
@@ -93,11 +95,13 @@ __device__ __forceinline__ double lane_probs_full(const double2 *a, uint64_t i0,
 }
 
 template <typename E>
-__global__ void __launch_bounds__(256) chunk_sum_kernel(const E *a, uint64_t N, double *sums, uint64_t nchunks) {
+__global__ void __launch_bounds__(256) chunk_sum_kernel(const E *a, uint64_t N, double *sums, double *rowp,
+                                                        uint64_t nchunks) {
     const int lane = threadIdx.x & 31;
     const uint64_t wpb = blockDim.x / 32;
+    static_assert(kRows == 32, "one row prefix per lane");
     for (uint64_t c = blockIdx.x * wpb + threadIdx.x / 32; c < nchunks; c += (uint64_t)gridDim.x * wpb) {
-        double acc = 0.0;
+        double acc = 0.0, mine = 0.0;  // lane r: the chunk-local running sum before row r
         const uint64_t base = c * kSampChunk;
         if (base + kSampChunk <= N) {  // warp-uniform: the whole chunk is below N
             for (int r0 = 0; r0 < kRows; r0 += SV_SAMP_BATCH) {
@@ -108,15 +112,20 @@ __global__ void __launch_bounds__(256) chunk_sum_kernel(const E *a, uint64_t N, 
                     q[r] = lane_probs_full(a, base + (r0 + r) * kRowLen + kPerLane * lane, p);
                 }
 #pragma unroll
-                for (int r = 0; r < SV_SAMP_BATCH; ++r) acc = __dadd_rn(acc, warp_xor_sum(q[r]));
+                for (int r = 0; r < SV_SAMP_BATCH; ++r) {
+                    if (lane == r0 + r) mine = acc;
+                    acc = __dadd_rn(acc, warp_xor_sum(q[r]));
+                }
             }
         } else {
             for (int r = 0; r < kRows; ++r) {
                 double p[kPerLane];
+                if (lane == r) mine = acc;
                 acc = __dadd_rn(acc, warp_xor_sum(lane_probs(a, base + r * kRowLen + kPerLane * lane, N, p)));
             }
         }
         if (lane == 0) sums[c] = acc;
+        rowp[c * kRows + lane] = mine;
     }
 }
 
@@ -224,7 +233,8 @@ __global__ void rank_window_kernel(const double *totals, int world, int rank, do
 }
 
 template <typename E>
-__global__ void __launch_bounds__(256) sample_kernel(const E *a, uint64_t N, const double *prefix, uint64_t nchunks,
+__global__ void __launch_bounds__(256) sample_kernel(const E *a, uint64_t N, const double *prefix, const double *rowp,
+                                                     uint64_t nchunks,
                                                      const double *g, uint64_t key, uint64_t shots,
                                                      uint64_t index_base, int last_rank, uint64_t *out) {
     const int lane = threadIdx.x & 31;
@@ -244,10 +254,16 @@ __global__ void __launch_bounds__(256) sample_kernel(const E *a, uint64_t N, con
             if (prefix[md] <= target) lo = md; else hi = md - 1;
         }
         const uint64_t base = lo * kSampChunk;
-        double run = prefix[lo];
+        // the row: the last whose start prefix[lo] + rowp[row] is <= target
+        // (starts are nondecreasing; one 256-B load per shot instead of
+        // walking the chunk's rows from the first)
+        const double start = __dadd_rn(prefix[lo], __ldcg(rowp + lo * kRows + lane));
+        const unsigned le = __ballot_sync(0xffffffffu, start <= target);
+        const int r_first = le ? 31 - __clz(le) : 0;
+        double run = __shfl_sync(0xffffffffu, start, r_first);
         uint64_t pick = (base + kSampChunk <= N ? base + kSampChunk : N) - 1;
-        uint64_t last_nz = base;
-        for (int r = 0; r < kRows; ++r) {
+        uint64_t last_nz = base + (uint64_t)r_first * kRowLen;
+        for (int r = r_first; r < kRows; ++r) {
             const uint64_t i0 = base + r * kRowLen + kPerLane * lane;
             double p[kPerLane];
             const double q = base + kSampChunk <= N ? lane_probs_full(a, i0, p) : lane_probs(a, i0, N, p);
@@ -300,11 +316,11 @@ __global__ void __launch_bounds__(256) sample_kernel(const E *a, uint64_t N, con
 uint64_t sample_chunks(uint64_t N) { return sample_chunks_impl(N); }
 
 void launch_sample_prefix(sv_dtype dt, const void *a, uint64_t N, double *scratch, double *rank_total,
-                          double *bscratch, cudaStream_t s) {
+                          double *bscratch, double *rowp, cudaStream_t s) {
     const uint64_t nch = sample_chunks(N);
     const unsigned g1 = (unsigned)((nch + 7) / 8 < 148 * 64 ? (nch + 7) / 8 : 148 * 64);
-    if (dt == SV_C64) chunk_sum_kernel<float2><<<g1, 256, 0, s>>>((const float2 *)a, N, scratch, nch);
-    else chunk_sum_kernel<double2><<<g1, 256, 0, s>>>((const double2 *)a, N, scratch, nch);
+    if (dt == SV_C64) chunk_sum_kernel<float2><<<g1, 256, 0, s>>>((const float2 *)a, N, scratch, rowp, nch);
+    else chunk_sum_kernel<double2><<<g1, 256, 0, s>>>((const double2 *)a, N, scratch, rowp, nch);
     SV_CUDA(cudaGetLastError());
     const uint64_t nb = (nch + kScanSeg - 1) / kScanSeg;
     SV_CHECK(nb <= 0x7fffffffull, SV_EINVAL, "internal: too many scan segments");
@@ -316,7 +332,8 @@ void launch_sample_prefix(sv_dtype dt, const void *a, uint64_t N, double *scratc
     SV_CUDA(cudaGetLastError());
 }
 
-void launch_sample_draw(sv_dtype dt, const void *a, uint64_t N, const double *scratch, const double *totals,
+void launch_sample_draw(sv_dtype dt, const void *a, uint64_t N, const double *scratch, const double *rowp,
+                        const double *totals,
                         int world, int rank, double *g, uint64_t key, uint64_t shots, uint64_t index_base,
                         uint64_t *out, cudaStream_t s) {
     rank_window_kernel<<<1, 1, 0, s>>>(totals, world, rank, g);
@@ -326,10 +343,10 @@ void launch_sample_draw(sv_dtype dt, const void *a, uint64_t N, const double *sc
     const unsigned g3 = (unsigned)((shots + 7) / 8 < 148 * 64 ? (shots + 7) / 8 : 148 * 64);
     const int last = rank == world - 1 ? 1 : 0;
     if (dt == SV_C64)
-        sample_kernel<float2><<<g3, 256, 0, s>>>((const float2 *)a, N, scratch, nch, g, key, shots, index_base, last,
+        sample_kernel<float2><<<g3, 256, 0, s>>>((const float2 *)a, N, scratch, rowp, nch, g, key, shots, index_base, last,
                                                  out);
     else
-        sample_kernel<double2><<<g3, 256, 0, s>>>((const double2 *)a, N, scratch, nch, g, key, shots, index_base,
+        sample_kernel<double2><<<g3, 256, 0, s>>>((const double2 *)a, N, scratch, rowp, nch, g, key, shots, index_base,
                                                   last, out);
     SV_CUDA(cudaGetLastError());
 }

@@ -1183,13 +1183,15 @@ sv_status sv_sample(sv_ctx *c, uint64_t shots, uint64_t seed, uint64_t *out, int
         const uint64_t nch = sample_chunks(c->nres);
         const int world = c->comm ? c->world : 1;
         const int rank = c->comm ? c->rank : 0;
-        // chunk prefixes [nch], every rank's total [world], window [3], scan segments [nb]
+        // chunk prefixes [nch], every rank's total [world], window [3], scan
+        // segments [nb], chunk-local row prefixes [32 nch] (1/128 of the amplitudes)
         const uint64_t nb = sample_scan_blocks(c->nres);
         if (!c->d_samp)
-            dmalloc((void **)&c->d_samp, (nch + (size_t)world + 3 + nb) * sizeof(double), "sampler scratch");
+            dmalloc((void **)&c->d_samp, (nch + (size_t)world + 3 + nb + 32 * nch) * sizeof(double), "sampler scratch");
         double *totals = c->d_samp + nch;  // [world]
         double *g = totals + world;         // window {global total, own offset, next rank's offset}
         double *bscr = g + 3;               // [nb]
+        double *rowp = bscr + nb;           // [32 nch]
         uint64_t *dout = out;
         if (!out_on_device) {
             if (shots > c->shots_cap) {
@@ -1203,7 +1205,7 @@ sv_status sv_sample(sv_ctx *c, uint64_t shots, uint64_t seed, uint64_t *out, int
         }
         const uint64_t key = hash64(seed ^ 0x53414D5000000000ull);  // "SAMP" (G21)
         run(c, SV_K_READOUT, [&] {
-            launch_sample_prefix(c->dt, c->state, c->nres, c->d_samp, totals + rank, bscr, c->stream);
+            launch_sample_prefix(c->dt, c->state, c->nres, c->d_samp, totals + rank, bscr, rowp, c->stream);
         });
         if (c->comm) {  // every rank's total, in rank order
             run(c, SV_K_ALLREDUCE, [&] {
@@ -1212,7 +1214,7 @@ sv_status sv_sample(sv_ctx *c, uint64_t shots, uint64_t seed, uint64_t *out, int
         }
         const uint64_t base = c->comm ? (uint64_t)c->rank * c->nl_amps : 0;
         run(c, SV_K_READOUT, [&] {
-            launch_sample_draw(c->dt, c->state, c->nres, c->d_samp, totals, world, rank, g, key, shots, base, dout,
+            launch_sample_draw(c->dt, c->state, c->nres, c->d_samp, rowp, totals, world, rank, g, key, shots, base, dout,
                                c->stream);
         });
         if (c->comm && shots) {  // each shot is owned by one rank; the others wrote 0

@@ -314,8 +314,9 @@ void launch_marked_mass(sv_dtype dt, const void *a, const uint64_t *marked, uint
 uint64_t sample_chunks(uint64_t N);
 uint64_t sample_scan_blocks(uint64_t N);  // segments of the chunk-prefix scan (scratch doubles)
 void launch_sample_prefix(sv_dtype dt, const void *a, uint64_t N, double *scratch, double *rank_total,
-                          double *bscratch, cudaStream_t s);
-void launch_sample_draw(sv_dtype dt, const void *a, uint64_t N, const double *scratch, const double *totals,
+                          double *bscratch, double *rowp, cudaStream_t s);
+void launch_sample_draw(sv_dtype dt, const void *a, uint64_t N, const double *scratch, const double *rowp,
+                        const double *totals,
                         int world, int rank, double *g, uint64_t key, uint64_t shots, uint64_t index_base,
                         uint64_t *out, cudaStream_t s);
 
