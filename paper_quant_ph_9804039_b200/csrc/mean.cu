@@ -12,6 +12,8 @@
 // partials -> the last block to finish sums the partials in a fixed order
 // (deterministic: no floating-point atomics, G14).
 #include <cuda_runtime.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "reduce.cuh"
 #include "sv_internal.h"
@@ -145,7 +147,116 @@ __global__ void __launch_bounds__(kMeanThreads) mean_kernel(MeanArgs a) {
     finalize(sr, si, a.partials, a.counter, a.sum_out, red);
 }
 
-uint64_t mean_chunk_elems(sv_dtype dt) { return kChunkVec * (dt == SV_C64 ? 2 : 1); }
+// ------------------------------------------------------------------------- //
+// Tile-per-CTA form (round 2, default): one CTA = one 64 KiB tile, 16 x
+// 128-bit loads per thread issued at once, 2 CTAs per SM -- the access shape of
+// the contiguous WHT tile pass, which streams the same 2 S bytes ~15 % faster
+// than the persistent chunk sweep above (n = 34: 39.4 vs 46.3 ms).  Each CTA
+// writes its fp64 (re, im) partial to tilepart[tile]; sum_pairs_kernel then
+// sums the tile partials in tile order (contiguous segments per block, the
+// last block sums the segments in block order): fixed order, deterministic.
+// ------------------------------------------------------------------------- //
+constexpr int kTilePer = 16;
+constexpr int grid_cap_pairs = 4096;  // the partials capacity (sv_api.cu kMaxGrid)                                           // 16-byte vectors per thread
+constexpr unsigned long long kTileVec = (unsigned long long)kMeanThreads * kTilePer;  // 64 KiB
+
+bool mean_tile_mode() {
+    static const bool on = [] {
+        const char *e = getenv("SV_MEAN_TILE");
+        return !(e && strcmp(e, "0") == 0);
+    }();
+    return on;
+}
+
+template <typename E, bool WRITE>
+__global__ void __launch_bounds__(kMeanThreads, 2) mean_tile_kernel(MeanArgs a) {
+    using V = typename Vec<E>::T;
+    using R = decltype(E{}.x);
+    constexpr int VE = Vec<E>::VE;
+    __shared__ double red[2 * (kMeanThreads / 32)];
+    const unsigned long long nvec = a.N / VE;
+    const unsigned long long t = blockIdx.x;
+    const unsigned long long v0 = t * kTileVec + threadIdx.x;
+    V *p = reinterpret_cast<V *>(a.a);
+    V buf[kTilePer];
+#pragma unroll
+    for (int u = 0; u < kTilePer; ++u) {
+        const unsigned long long v = v0 + (unsigned long long)u * kMeanThreads;
+        if (v < nvec) buf[u] = __ldcg(p + v);
+    }
+    R two_mr = 0, two_mi = 0;
+    if (WRITE) {
+        const double mr = a.sum_in[0] * a.inv_total, mi = a.sum_in[1] * a.inv_total;
+        two_mr = (R)(2.0 * mr);
+        two_mi = (R)(2.0 * mi);
+    }
+    const auto *mk = reinterpret_cast<const unsigned long long *>(a.marked);
+    const bool any = a.n_marked != 0 && ((__ldg(&a.chunkmap[t >> 5]) >> (t & 31)) & 1u);
+    double sr = 0.0, si = 0.0;
+#pragma unroll
+    for (int u = 0; u < kTilePer; ++u) {
+        const unsigned long long v = v0 + (unsigned long long)u * kMeanThreads;
+        if (v >= nvec) continue;
+        E e[VE];
+        if constexpr (VE == 2) {
+            e[0].x = buf[u].x; e[0].y = buf[u].y;
+            e[1].x = buf[u].z; e[1].y = buf[u].w;
+        } else {
+            e[0].x = buf[u].x; e[0].y = buf[u].y;
+        }
+#pragma unroll
+        for (int q = 0; q < VE; ++q) {
+            const bool m = any && is_marked(v * VE + q, mk, a.n_marked);
+            if (m) { e[q].x = -e[q].x; e[q].y = -e[q].y; }   // O
+            if (WRITE) {
+                e[q].x = two_mr - e[q].x;                       // 2 mu - (O a)_i
+                e[q].y = two_mi - e[q].y;
+                sr += m ? -(double)e[q].x : (double)e[q].x;     // (O a')_i for the next sum
+                si += m ? -(double)e[q].y : (double)e[q].y;
+            } else {
+                sr += (double)e[q].x;
+                si += (double)e[q].y;
+            }
+        }
+        if (WRITE) {
+            if constexpr (VE == 2) {
+                buf[u].x = e[0].x; buf[u].y = e[0].y; buf[u].z = e[1].x; buf[u].w = e[1].y;
+            } else {
+                buf[u].x = e[0].x; buf[u].y = e[0].y;
+            }
+            p[v] = buf[u];
+        }
+    }
+    block_sum2(sr, si, red);
+    if (threadIdx.x == 0) {
+        a.tilepart[2 * t] = sr;
+        a.tilepart[2 * t + 1] = si;
+    }
+}
+
+// Fixed-order sum of `count` (re, im) pairs -> out[0..1].
+__global__ void __launch_bounds__(kMeanThreads) sum_pairs_kernel(const double *in, unsigned long long count,
+                                                                 double *partials, unsigned int *counter,
+                                                                 double *out) {
+    __shared__ double red[2 * (kMeanThreads / 32)];
+    const unsigned long long per = (count + gridDim.x - 1) / gridDim.x;
+    const unsigned long long lo = per * blockIdx.x, hi = lo + per < count ? lo + per : count;
+    double r = 0.0, m = 0.0;
+    for (unsigned long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        r += __ldcg(in + 2 * i);
+        m += __ldcg(in + 2 * i + 1);
+    }
+    block_sum2(r, m, red);
+    finalize(r, m, partials, counter, out, red);
+}
+
+uint64_t mean_tiles(uint64_t N, sv_dtype dt) {
+    const uint64_t nvec = N * elem_bytes(dt) / 16;
+    return (nvec + kTileVec - 1) / kTileVec;
+}
+
+uint64_t mean_chunk_elems(sv_dtype dt) { return (mean_tile_mode() ? kTileVec : kChunkVec) * (dt == SV_C64 ? 2 : 1); }
+
 
 int mean_grid(uint64_t N, sv_dtype dt) {
     int dev = 0, sms = 148, per = 1;
@@ -163,6 +274,25 @@ int mean_grid(uint64_t N, sv_dtype dt) {
 }
 
 void launch_mean_grid(sv_dtype dt, const MeanArgs &a, int grid, bool write, cudaStream_t s) {
+    if (mean_tile_mode()) {
+        const uint64_t nt = mean_tiles(a.N, dt);
+        SV_CHECK(a.tilepart != nullptr, SV_EINVAL, "internal: mean tile partials not allocated");
+        SV_CHECK(nt <= 0x7fffffffull, SV_EINVAL, "internal: too many mean tiles");
+        if (dt == SV_C64) {
+            if (write) mean_tile_kernel<float2, true><<<(unsigned)nt, kMeanThreads, 0, s>>>(a);
+            else mean_tile_kernel<float2, false><<<(unsigned)nt, kMeanThreads, 0, s>>>(a);
+        } else {
+            if (write) mean_tile_kernel<double2, true><<<(unsigned)nt, kMeanThreads, 0, s>>>(a);
+            else mean_tile_kernel<double2, false><<<(unsigned)nt, kMeanThreads, 0, s>>>(a);
+        }
+        SV_CUDA(cudaGetLastError());
+        unsigned int g = (unsigned int)((nt + 2047) / 2048);  // <= 2048 pairs per block
+        if (g < 1) g = 1;
+        if (g > (unsigned)grid_cap_pairs) g = (unsigned)grid_cap_pairs;
+        sum_pairs_kernel<<<g, kMeanThreads, 0, s>>>(a.tilepart, nt, a.partials, a.counter, a.sum_out);
+        SV_CUDA(cudaGetLastError());
+        return;
+    }
     if (dt == SV_C64) {
         if (write) mean_kernel<float2, true><<<grid, kMeanThreads, 0, s>>>(a);
         else mean_kernel<float2, false><<<grid, kMeanThreads, 0, s>>>(a);

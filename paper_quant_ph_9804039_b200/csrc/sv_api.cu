@@ -86,6 +86,7 @@ struct sv_ctx {
     uint64_t super_nseg = 0;
     int super_grid = 0;
     double *d_tilepart = nullptr;       // decoherence: per-tile sum |a|^2 of an iteration's last pass
+    double *d_meanpart = nullptr;       // mean kernel (tile form): per-tile (re, im) partials
     size_t tilepart_cap = 0;
     double *d_samp = nullptr;           // sampler: chunk prefixes + rank totals + window
     uint64_t *d_shots = nullptr;        // sampler: device output for host-returning calls
@@ -735,6 +736,11 @@ MeanArgs mean_args(sv_ctx *c, bool with_oracle) {
     m.chunkmap = c->d_chunkmap;
     m.partials = c->d_partials;
     m.counter = c->d_counter;
+    if (mean_tile_mode()) {
+        if (c->d_meanpart == nullptr)
+            dmalloc((void **)&c->d_meanpart, 2 * mean_tiles(c->nres, c->dt) * sizeof(double), "mean tile partials");
+        m.tilepart = c->d_meanpart;
+    }
     return m;
 }
 
@@ -941,6 +947,7 @@ void destroy(sv_ctx *c) {
     cudaFree(c->d_samp);
     cudaFree(c->d_deco);
     cudaFree(c->d_tilepart);
+    cudaFree(c->d_meanpart);
     cudaFree(c->d_superctr);
     cudaFree(c->d_superseg);
     for (auto &ge : c->graphs) cudaGraphExecDestroy(ge.exec);

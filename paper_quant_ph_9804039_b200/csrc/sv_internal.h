@@ -280,10 +280,13 @@ struct MeanArgs {
     double *sum_out = nullptr;         // local complex sum of (O a_new)
     double *partials = nullptr;        // 2 * grid doubles
     unsigned int *counter = nullptr;   // zero-initialised ticket
+    double *tilepart = nullptr;        // tile form: 2 * mean_tiles() doubles (per-tile partials)
 };
 // One wave of blocks (SM count x resident blocks), capped by the work.
 int mean_grid(uint64_t N, sv_dtype dt);
-uint64_t mean_chunk_elems(sv_dtype dt);  // amplitudes per chunk of the mean kernel
+uint64_t mean_chunk_elems(sv_dtype dt);  // amplitudes per chunk (tile) of the mean kernel
+bool mean_tile_mode();                   // SV_MEAN_TILE (default on): one CTA per 64 KiB tile
+uint64_t mean_tiles(uint64_t N, sv_dtype dt);
 // write = true: fused flip + invert-about-mean + next-sum; false: read-only
 // sum of (O a) (the first mu of an sv_iterate call).
 void launch_mean_grid(sv_dtype dt, const MeanArgs &a, int grid, bool write, cudaStream_t s);
