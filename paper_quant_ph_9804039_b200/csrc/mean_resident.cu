@@ -43,25 +43,23 @@ __device__ __forceinline__ void grid_barrier(unsigned int *count, unsigned int *
     __syncthreads();
 }
 
-// Block-wide fp64 (re, im) sum, result broadcast to every thread.
-__device__ __forceinline__ void block_sum_bcast(double &re, double &im, double *red) {
+// Block-wide fp64 (re, im) sum, result in thread 0 only (one barrier: the
+// next write of red[2 w] comes after the grid barrier's own __syncthreads,
+// which thread 0 reaches only after reading them).
+__device__ __forceinline__ void block_sum_t0(double &re, double &im, double *red) {
     for (int o = 16; o > 0; o >>= 1) {
         re += __shfl_xor_sync(0xffffffffu, re, o);
         im += __shfl_xor_sync(0xffffffffu, im, o);
     }
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
     if (l == 0) { red[2 * w] = re; red[2 * w + 1] = im; }
     __syncthreads();
     if (threadIdx.x == 0) {
         double r = 0.0, m = 0.0;
         for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { r += red[2 * i]; m += red[2 * i + 1]; }
-        red[64] = r;
-        red[65] = m;
+        re = r;
+        im = m;
     }
-    __syncthreads();
-    re = red[64];
-    im = red[65];
 }
 
 // One published block total: the fp64 (re, im) partial and the epoch it
@@ -135,7 +133,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
     // barrier, then warp 0 sums the partials in a fixed order (lane-strided,
     // then a fixed shuffle tree) -- the same total in every block.
     auto grid_total = [&](double r, double m, int parity, double &tr, double &ti) {
-        block_sum_bcast(r, m, red);
+        block_sum_t0(r, m, red);  // (thread 0 publishes it)
 #if SV_RES_SLOTS
         // all-gather instead of a counter barrier: every block publishes its
         // total with a release store of the round's epoch, and warp 0 of every
@@ -181,8 +179,8 @@ __global__ void __launch_bounds__(kResThreads, 1)
     // first sum: of O a
     double cr, ci, r = 0.0, m = 0.0;
     for (unsigned int i = threadIdx.x; i < len; i += blockDim.x) { r += (double)s[i].x; m += (double)s[i].y; }
+    __syncthreads();  // every element read before any is negated (another thread may own it)
     negate_marked(cr, ci);
-    __syncthreads();
     double tr, ti;
     grid_total(r - 2.0 * cr, m - 2.0 * ci, 0, tr, ti);
     // invariant at the top of an iteration: s holds O a and (tr, ti) = sum(O a)
@@ -201,7 +199,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
         if (it + 1 == k) break;
         __syncthreads();
         negate_marked(cr, ci);  // O of the next iteration: sum(O a') = sum(a') - 2 sum_marked(a')
-        __syncthreads();
+        // (the negated entries are next read after grid_total's barriers)
         grid_total(r - 2.0 * cr, m - 2.0 * ci, (it + 1) & 1, tr, ti);
     }
     __syncthreads();
