@@ -19,6 +19,8 @@
 // iterations, so they keep the launched path).
 #include <cuda_runtime.h>
 
+#include <cstdio>
+
 #include "sv_internal.h"
 
 namespace sv {
@@ -206,6 +208,206 @@ __global__ void __launch_bounds__(kResThreads, 1)
     for (unsigned int i = threadIdx.x; i < len; i += blockDim.x) a[lo + i] = s[i];
 }
 
+// Register-resident variant (round 2, the default where it fits: C <= NT x
+// NPT).  Same iteration, held differently:
+//   * thread tid keeps its NPT elements (block-local j * NT + tid) in
+//     registers for the whole call -- an iteration touches no memory but one
+//     partial per block (the shared-memory sweep above moved 226 KB of smem per
+//     SM per iteration at c2, ~0.9 us);
+//   * O is a per-thread sign mask built once (bit j: slot j is marked), so the
+//     registers hold b = O a between iterations and one pass per iteration
+//     computes a' = 2 mu - b, b' = O a' (a sign-bit flip) and the fp64 sums
+//     of b' -- exactly sum(O a'), the next mu, with no separate marked pass;
+//   * the block total is folded by warp 0 (a 5-level shuffle tree), published
+//     as one 16-B partial, counted in with ONE release-add on a monotonic
+//     64-bit counter (zeroed before the launch; round r is complete at
+//     (r + 1) x grid), and gathered with all of a lane's partials in flight.
+// Measured alternatives (tools/mean_resident_scan.py): flag-in-word
+// all-gather polling, counter + flag-in-word partials, and a last-arriver
+// broadcast into per-block lines were all slower (polling contention on L2).
+// Partials alternate by round parity: a block writes round r + 2's partial
+// only after round r + 1 completes, which every block reaches after gathering
+// round r.
+__device__ __forceinline__ void red_release_add_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+constexpr int kResRegMaxGrid = 160;  // blocks (one per SM; B200: 148)
+#ifndef SV_RESREG_TRACE
+#define SV_RESREG_TRACE 0  // 1: clock64 phase sums per round, printed by 3 blocks (A/B builds only)
+#endif
+
+// x with its sign flipped when s (0 or 1) is set: a sign-bit XOR, exact.
+__device__ __forceinline__ double flip_if(double x, unsigned int s) {
+    return __hiloint2double(__double2hiint(x) ^ (int)(s << 31), __double2loint(x));
+}
+__device__ __forceinline__ float flip_if(float x, unsigned int s) {
+    return __int_as_float(__float_as_int(x) ^ (int)(s << 31));
+}
+
+template <typename E, int NPT, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    mean_resreg_kernel(E *a, unsigned long long N, unsigned long long C, double inv_N,
+                       const unsigned long long *marked, unsigned long long n_marked, int k, double2 *partials,
+                       unsigned long long *ctr) {
+    using R = decltype(E{}.x);
+    __shared__ double red[66];
+    __shared__ unsigned long long s_mlo, s_mcnt;
+    __shared__ unsigned int s_mm[NT];  // per-thread marked-slot masks (built once)
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const unsigned long long lo = (unsigned long long)blockIdx.x * C;
+    const unsigned long long hi = lo + C < N ? lo + C : N;
+    const unsigned int len = (unsigned int)(hi > lo ? hi - lo : 0);
+    const unsigned int nb = gridDim.x;
+    if (tid == 0) {  // this block's marked entries: marked[s_mlo .. s_mlo + s_mcnt)
+        unsigned long long l = 0, h = n_marked;
+        while (l < h) { const unsigned long long md = (l + h) >> 1; if (marked[md] < lo) l = md + 1; else h = md; }
+        const unsigned long long first = l;
+        h = n_marked;
+        while (l < h) { const unsigned long long md = (l + h) >> 1; if (marked[md] < hi) l = md + 1; else h = md; }
+        s_mlo = first;
+        s_mcnt = l - first;
+    }
+    s_mm[tid] = 0u;
+    __syncthreads();
+    for (unsigned long long r = tid; r < s_mcnt; r += NT) {
+        const unsigned int off = (unsigned int)(marked[s_mlo + r] - lo);
+        atomicOr(&s_mm[off % NT], 1u << (off / NT));
+    }
+    __syncthreads();
+    const unsigned int mmask = s_mm[tid];
+    // slots j < nv hold elements (j * NT + tid < len); the rest are padding
+    const int nv = len > (unsigned int)tid ? (int)((len - (unsigned int)tid + NT - 1) / NT) : 0;
+    E v[NPT];
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+        if (j < nv) v[j] = __ldcg(a + lo + (unsigned int)j * NT + (unsigned int)tid);
+        else { v[j].x = (R)0; v[j].y = (R)0; }
+    }
+#if SV_RESREG_TRACE
+    long long tr_prev = clock64(), tr_sum[6] = {0, 0, 0, 0, 0, 0};
+#endif
+    // Grid total of the per-thread values: warp trees, warp 0 folds the warp
+    // sums, publishes the block partial, waits for the round, then sums all
+    // partials in block order (lane-strided + fixed tree): the same total in
+    // every block.
+    auto grid_total = [&](double r, double m, unsigned int round, double &tr, double &ti) {
+#if SV_RESREG_TRACE
+        const long long t_a = clock64();
+        tr_sum[0] += t_a - tr_prev;  // compute since the last broadcast
+#endif
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            r += __shfl_xor_sync(0xffffffffu, r, o);
+            m += __shfl_xor_sync(0xffffffffu, m, o);
+        }
+        if (lane == 0) { red[2 * w] = r; red[2 * w + 1] = m; }
+        __syncthreads();
+#if SV_RESREG_TRACE
+        const long long t_b = clock64();
+        tr_sum[1] += t_b - t_a;  // warp trees + block barrier
+#endif
+        if (w == 0) {
+            double R0 = lane < NT / 32 ? red[2 * lane] : 0.0, M0 = lane < NT / 32 ? red[2 * lane + 1] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                R0 += __shfl_xor_sync(0xffffffffu, R0, o);
+                M0 += __shfl_xor_sync(0xffffffffu, M0, o);
+            }
+            double2 *part = partials + (size_t)(round & 1u) * nb;
+            if (lane == 0) {
+                part[blockIdx.x] = make_double2(R0, M0);
+#if SV_RESREG_TRACE
+                const long long t_0 = clock64();
+#endif
+                red_release_add_u64(ctr, 1ull);
+#if SV_RESREG_TRACE
+                const long long t_1 = clock64();
+                tr_sum[3] += t_1 - t_0;  // fence + red issue
+#endif
+                const unsigned long long target = (unsigned long long)(round + 1u) * nb;
+                while (ld_acquire_u64(ctr) < target) {
+                }
+#if SV_RESREG_TRACE
+                tr_sum[4] += clock64() - t_1;  // wait until the round is complete
+#endif
+            }
+            __syncwarp();
+            // all of the lane's partials in flight at once (16-B loads, fixed order)
+            constexpr int kPer = kResRegMaxGrid / 32;
+            double2 q[kPer];
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) {
+                const unsigned int b = (unsigned int)lane + 32u * i;
+                q[i] = b < nb ? __ldcg(part + b) : make_double2(0.0, 0.0);
+            }
+            R0 = 0.0;
+            M0 = 0.0;
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) { R0 += q[i].x; M0 += q[i].y; }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                R0 += __shfl_xor_sync(0xffffffffu, R0, o);
+                M0 += __shfl_xor_sync(0xffffffffu, M0, o);
+            }
+            if (lane == 0) { red[64] = R0; red[65] = M0; }
+        }
+        __syncthreads();
+        tr = red[64];
+        ti = red[65];
+#if SV_RESREG_TRACE
+        tr_prev = clock64();
+        tr_sum[2] += tr_prev - t_b;  // publish + wait + gather + broadcast
+#endif
+    };
+    // b = O a and its sum (padding slots hold 0 and add nothing)
+    double r = 0.0, m = 0.0;
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+        const unsigned int sj = (mmask >> j) & 1u;
+        v[j].x = flip_if(v[j].x, sj);
+        v[j].y = flip_if(v[j].y, sj);
+        r += (double)v[j].x;
+        m += (double)v[j].y;
+    }
+    double tr, ti;
+    unsigned int round = 0;
+    grid_total(r, m, round++, tr, ti);
+    // invariant at the top of an iteration: v holds b = O a and (tr, ti) = sum(b)
+    for (int it = 0; it < k; ++it) {
+        const R two_mr = (R)(2.0 * tr * inv_N), two_mi = (R)(2.0 * ti * inv_N);
+        if (it + 1 == k) {  // the last a' = 2 mu - b is the result
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) {
+                v[j].x = two_mr - v[j].x;
+                v[j].y = two_mi - v[j].y;
+            }
+            break;
+        }
+        r = 0.0;
+        m = 0.0;
+#pragma unroll
+        for (int j = 0; j < NPT; ++j) {
+            const unsigned int sj = (mmask >> j) & 1u;
+            v[j].x = flip_if(two_mr - v[j].x, sj);  // b' = O a',  a' = 2 mu - b
+            v[j].y = flip_if(two_mi - v[j].y, sj);
+            if (j < nv) {
+                r += (double)v[j].x;
+                m += (double)v[j].y;
+            }
+        }
+        grid_total(r, m, round++, tr, ti);
+    }
+#pragma unroll
+    for (int j = 0; j < NPT; ++j)
+        if (j < nv) a[lo + (unsigned int)j * NT + (unsigned int)tid] = v[j];
+#if SV_RESREG_TRACE
+    if (tid == 0 && (blockIdx.x == 0 || blockIdx.x == nb / 2 || blockIdx.x + 1 == nb))
+        printf("resreg trace block %u rounds %u: cycles/round compute %.0f reduce %.0f grid %.0f (fence+red %.0f "
+               "wait %.0f)\n", blockIdx.x, round, (double)tr_sum[0] / round, (double)tr_sum[1] / round,
+               (double)tr_sum[2] / round, (double)tr_sum[3] / round, (double)tr_sum[4] / round);
+#endif
+}
+
 // Launch geometry: one wave of co-resident blocks, each holding C elements
 // in shared memory; grid = 0 if the state does not fit.
 static void resident_geometry(sv_dtype dt, uint64_t N, int &grid, uint64_t &C, int &smem, void *&fn) {
@@ -244,8 +446,34 @@ size_t mean_resident_slot_bytes(sv_dtype dt, uint64_t N) {
     return (size_t)2 * (size_t)(grid > 0 ? grid : 0) * sizeof(ResSlot);
 }
 
+// Register-resident configurations (threads NT, elements per thread NPT),
+// the first with NT x NPT >= C is used.  Registers per thread are capped at
+// 65536 / NT (ptxas -v: no spills in any of them).
+struct ResRegCfg {
+    int nt, npt;
+    void *fn;
+};
+static const ResRegCfg *resreg_cfg(sv_dtype dt, uint64_t C) {
+    static const ResRegCfg t64[] = {{512, 1, (void *)mean_resreg_kernel<float2, 1, 512>},
+                                    {512, 2, (void *)mean_resreg_kernel<float2, 2, 512>},
+                                    {512, 4, (void *)mean_resreg_kernel<float2, 4, 512>},
+                                    {512, 8, (void *)mean_resreg_kernel<float2, 8, 512>},
+                                    {512, 16, (void *)mean_resreg_kernel<float2, 16, 512>},
+                                    {512, 32, (void *)mean_resreg_kernel<float2, 32, 512>}};
+    static const ResRegCfg t128[] = {{512, 1, (void *)mean_resreg_kernel<double2, 1, 512>},
+                                     {512, 2, (void *)mean_resreg_kernel<double2, 2, 512>},
+                                     {512, 4, (void *)mean_resreg_kernel<double2, 4, 512>},
+                                     {512, 8, (void *)mean_resreg_kernel<double2, 8, 512>},
+                                     {512, 16, (void *)mean_resreg_kernel<double2, 16, 512>}};
+    const ResRegCfg *t = dt == SV_C64 ? t64 : t128;
+    for (int i = 0; i < (dt == SV_C64 ? 6 : 5); ++i)
+        if ((uint64_t)t[i].nt * t[i].npt >= C) return &t[i];
+    return nullptr;
+}
+
 void launch_mean_resident(sv_dtype dt, void *a, uint64_t N, double inv_N, const uint64_t *marked, uint64_t m, int k,
-                          double *partials, unsigned int *bar, void *slots, unsigned long long epoch0, cudaStream_t s) {
+                          double *partials, unsigned int *bar, void *slots, unsigned long long epoch0, bool regs,
+                          cudaStream_t s) {
     int grid, smem;
     uint64_t C;
     void *fn;
@@ -253,6 +481,22 @@ void launch_mean_resident(sv_dtype dt, void *a, uint64_t N, double inv_N, const 
     SV_CHECK(grid > 0 && k >= 1, SV_EINVAL, "internal: resident mean launch without a fitting geometry");
     unsigned long long Nl = N, Cl = C, ml = m;
     const unsigned long long *mk = reinterpret_cast<const unsigned long long *>(marked);
+    const ResRegCfg *rc = regs ? resreg_cfg(dt, C) : nullptr;
+    if (rc != nullptr) {
+        int per = 0, dev = 0, sms = 0;
+        SV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rc->fn, rc->nt, 0));
+        SV_CUDA(cudaGetDevice(&dev));
+        SV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        if (per >= 1 && grid <= per * sms && grid <= kResRegMaxGrid) {
+            // the monotonic 64-bit arrival counter lives after the {count, generation} pair
+            unsigned long long *ctr = reinterpret_cast<unsigned long long *>(bar + 2);
+            SV_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s));
+            double2 *part2 = reinterpret_cast<double2 *>(partials);
+            void *args[] = {&a, &Nl, &Cl, &inv_N, &mk, &ml, &k, &part2, &ctr};
+            SV_CUDA(cudaLaunchCooperativeKernel(rc->fn, dim3(grid), dim3(rc->nt), args, 0, s));
+            return;
+        }
+    }
     ResSlot *sl = reinterpret_cast<ResSlot *>(slots);
     void *args[] = {&a, &Nl, &Cl, &inv_N, &mk, &ml, &k, &partials, &bar, &sl, &epoch0};
     SV_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kResThreads), args, (size_t)smem, s));

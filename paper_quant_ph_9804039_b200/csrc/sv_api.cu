@@ -100,6 +100,7 @@ struct sv_ctx {
     void *d_res_slots = nullptr;     // resident mean kernel: per-block published totals (two rounds)
     unsigned long long res_epoch = 0;  // last epoch handed to the resident mean kernel
     bool mean_resident = true;       // SV_MEAN_RESIDENT=0 disables the one-launch path
+    bool mean_resreg = true;         // SV_MEAN_RESIDENT=smem: the shared-memory resident kernel (A/B)
     int mgrid = 1;
     Plan plan;
     bool broken = false;   // the communicator was aborted (sync_ctx): every call fails with SV_ENCCL
@@ -768,7 +769,7 @@ void run_mean(sv_ctx *c, int k, bool with_oracle) {
         run(c, SV_K_MEAN, [&] {
             launch_mean_resident(c->dt, c->state, c->nres, ldexp(1.0, -c->n), with_oracle ? c->d_marked : nullptr,
                                  with_oracle ? c->n_marked : 0, reps, c->d_partials, c->d_gbar, c->d_res_slots,
-                                 epoch0, c->stream);
+                                 epoch0, c->mean_resreg, c->stream);
         });
         return;
     }
@@ -1013,9 +1014,12 @@ sv_status sv_init(sv_ctx **out, int n, uint64_t seed, sv_dtype dtype, sv_init_ki
         dmalloc((void **)&c->d_partials, 2 * kMaxGrid * sizeof(double), "partials");
         dmalloc((void **)&c->d_sums, 8 * sizeof(double), "sums");
         dmalloc((void **)&c->d_counter, sizeof(unsigned int), "counter");
-        dmalloc((void **)&c->d_gbar, 2 * sizeof(unsigned int), "grid barrier");
-        SV_CUDA(cudaMemsetAsync(c->d_gbar, 0, 2 * sizeof(unsigned int), c->stream));
-        if (const char *e = getenv("SV_MEAN_RESIDENT")) c->mean_resident = strcmp(e, "0") != 0;
+        dmalloc((void **)&c->d_gbar, 4 * sizeof(unsigned int), "grid barrier");
+        SV_CUDA(cudaMemsetAsync(c->d_gbar, 0, 4 * sizeof(unsigned int), c->stream));
+        if (const char *e = getenv("SV_MEAN_RESIDENT")) {
+            c->mean_resident = strcmp(e, "0") != 0;
+            c->mean_resreg = strcmp(e, "smem") != 0;
+        }
         if (const char *e = getenv("SV_GRAPHS")) c->use_graphs = strcmp(e, "0") != 0;
         SV_CUDA(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned int), c->stream));
         SV_CUDA(cudaMemsetAsync(c->d_sums, 0, 8 * sizeof(double), c->stream));

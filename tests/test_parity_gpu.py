@@ -497,15 +497,17 @@ def test_profile_counts_launches():
 
 
 @pytest.mark.parametrize("dtype", DT, ids=DT_IDS)
-@pytest.mark.parametrize("n,m,k", [(14, 0, 3), (17, 5, 9), (20, 64, 6), (21, 300, 4)])
+@pytest.mark.parametrize("n,m,k", [(14, 0, 3), (16, 30000, 3), (17, 5, 9), (20, 64, 6), (21, 300, 4)])
 def test_mean_resident_and_launched_paths(dtype, n, m, k, monkeypatch):
-    """The one-launch shared-memory-resident mean path (mean_resident.cu,
-    states within the aggregate shared memory) and the launched per-iteration
-    path (SV_MEAN_RESIDENT=0) both equal the oracle; M = 0 (O = I) included."""
+    """The one-launch resident mean paths (mean_resident.cu, states within the
+    aggregate shared memory: the register-resident kernel by default, the
+    shared-memory one with SV_MEAN_RESIDENT=smem) and the launched
+    per-iteration path (SV_MEAN_RESIDENT=0) all equal the oracle; M = 0 (O = I)
+    included."""
     a0 = rand_state(n, dtype)
     marked = orc.marked_from_seed(n, m, 7) if m else np.zeros(0, np.uint64)
     ref = orc.iterate(a0.copy(), marked, k, orc.MEAN)
-    for env in ("1", "0"):
+    for env in ("1", "smem", "0"):
         monkeypatch.setenv("SV_MEAN_RESIDENT", env)
         with ctx_with(a0, dtype) as c:
             sv.sv_set_marked(c, marked)
@@ -516,7 +518,7 @@ def test_mean_resident_and_launched_paths(dtype, n, m, k, monkeypatch):
         sms = 148  # B200; the library asks the device
         chunk = -(-(1 << n) // sms) * (8 if dtype == sv.SV_C64 else 16)
         fits = chunk <= 232448 - 1024  # opt-in shared memory per block minus the kernel's reserve
-        assert launches == (1 if (env == "1" and fits) else k), (env, launches)
+        assert launches == (1 if (env != "0" and fits) else k), (env, launches)
         assert_close(got, ref, dtype, f"mean resident={env} n={n}", n=n, k=k)
 
 
