@@ -375,8 +375,8 @@ def run_ours(args):
     achieved = algo_bytes / avg_s / 1e9
     total_kernel_ms = sum(v[1] for name, v in prof.items() if name not in ("exchange", "allreduce", "init"))
     kdesc = {"wht_tile": "wht_tile_kernel / wht_tile2_kernel",
-             "mean": ("mean_resident_kernel (state held in shared memory for all k iterations; "
-                      "bytes = 2 S per iteration, served on-chip)") if resident else "mean_kernel",
+             "mean": "mean_resreg_kernel / mean_resident_kernel (state on-chip for all k iterations)"
+                     if resident else "mean_kernel",
              "wht_whole": "whole_reg_kernel (one CTA on one SM, state in the registers of 8 warps; "
                           "whole_state_kernel in shared memory below n = 9)"}[kname]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -384,20 +384,37 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": algo_bytes, "launches": launches, "avg_launch_ms": 1e3 * avg_s,
                 "share_of_step": kms / max(t_ms, 1e-9), "peak_source": peak_src}
     if resident:
-        # all k iterations in one launch with the state in shared memory: not an
-        # HBM measurement.  Each iteration reads and writes every amplitude once
-        # in shared memory, then crosses one grid-wide barrier; the bound is the
-        # aggregate shared-memory bandwidth plus that barrier's latency.
-        sms = torch.cuda.get_device_properties(local).multi_processor_count
-        smem_peak = sms * 128 * 1.965  # GB/s: 128 B/clk per SM at the 1965 MHz max SM clock
+        # all k iterations in one launch, the state held on-chip (registers;
+        # shared memory above the register kernel's size): not an HBM
+        # measurement.  An iteration is a few register ops per amplitude plus
+        # one grid-wide sum (block trees, one release-add arrival, a gather of
+        # every block's partial); its bound is that reduction's latency.  The
+        # floor is measured here: the same kernel at n = 14 (~110 amplitudes
+        # per block, no data work), k iterations, same dtype.
+        floor_ctx = sv.sv_init(14, seed, dtype)
+        try:
+            sv.sv_set_marked(floor_ctx, sv.sv_marked_from_seed(14, min(M, 16), seed))
+            sv.sv_iterate(floor_ctx, k, sv.SV_DIFFUSE_MEAN)
+            sv.sv_synchronize(floor_ctx)
+            sv.sv_profile(floor_ctx, True)
+            for _ in range(3):
+                sv.sv_iterate(floor_ctx, k, sv.SV_DIFFUSE_MEAN)
+            fl, fms = sv.sv_profile_read(floor_ctx, sv.SV_K_MEAN)
+        finally:
+            sv.sv_free(floor_ctx)
         per_it_us = 1e6 * avg_s / k
-        roofline = {"bound": "smem+barrier", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
-                    "frac": achieved / smem_peak, "traffic": None, "kernel": f"{kname} ({kdesc})",
-                    "algorithmic_bytes_per_launch": algo_bytes, "launches": launches, "avg_launch_ms": 1e3 * avg_s,
-                    "share_of_step": kms / max(t_ms, 1e-9), "us_per_iteration": per_it_us,
-                    "peak_source": (f"aggregate shared-memory bandwidth, {sms} SMs x 128 B/clk x 1.965 GHz; "
-                                    "each iteration also waits on one grid-wide barrier (latency-bound: "
-                                    "us_per_iteration)")}
+        floor_us = 1e3 * fms / max(fl, 1) / k
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        kdesc = ("mean_resreg_kernel (state in the registers of one 512-thread block per SM for all k "
+                 "iterations; O a per-thread sign mask; one grid-wide fp64 sum per iteration)")
+        roofline = {"bound": "latency", "achieved": 1e6 / per_it_us, "peak": 1e6 / floor_us, "unit": "iterations/s",
+                    "frac": floor_us / per_it_us, "traffic": None, "kernel": f"{kname} ({kdesc})",
+                    "floor_us_per_iteration": floor_us,
+                    "launches": launches, "avg_launch_ms": 1e3 * avg_s, "share_of_step": kms / max(t_ms, 1e-9),
+                    "us_per_iteration": per_it_us, "onchip_bytes_per_iteration": 2 * local_bytes,
+                    "peak_source": (f"measured floor: the same kernel at n = 14 (~110 amplitudes per block, "
+                                    f"{sms} blocks), i.e. one iteration's grid-wide sum + barrier with no data "
+                                    "work (achieved and peak as iteration rates)")}
     if kname == "wht_whole":
         # one CTA on one SM (state in registers / shared memory): the bound is
         # that SM's add rate -- k iterations x 2n stages x N/2 butterflies x 4 real adds
