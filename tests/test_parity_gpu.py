@@ -497,7 +497,8 @@ def test_profile_counts_launches():
 
 
 @pytest.mark.parametrize("dtype", DT, ids=DT_IDS)
-@pytest.mark.parametrize("n,m,k", [(14, 0, 3), (16, 30000, 3), (17, 5, 9), (20, 64, 6), (21, 300, 4)])
+@pytest.mark.parametrize("n,m,k", [(14, 0, 3), (16, 30000, 3), (17, 5, 9), (18, 1000, 1), (19, 7, 2), (20, 64, 6),
+                                   (21, 300, 4)])
 def test_mean_resident_and_launched_paths(dtype, n, m, k, monkeypatch):
     """The one-launch resident mean paths (mean_resident.cu, states within the
     aggregate shared memory: the register-resident kernel by default, the
