@@ -31,7 +31,7 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     # name: (n, dtype, M, k, diffusion, seed, init, description)
     "c1": (10, "c128", 1, 25, "wht", 1, "uniform", "c1: n=10 complex128, M=1, 25 WHT iterations (one-CTA kernel)"),
-    "c2": (20, "c128", 4, 402, "mean", 2, "uniform", "c2: n=20 complex128 (16 MiB, L2-resident), M=4, 402 mean iterations"),
+    "c2": (20, "c128", 4, 402, "mean", 2, "uniform", "c2: n=20 complex128 (16 MiB, held on-chip), M=4, 402 mean iterations"),
     "c3": (28, "c64", 1, 64, "wht", 3, "uniform", "c3: n=28 complex64 (2 GiB), M=1, 64 WHT iterations"),
     "c3m": (28, "c64", 1, 64, "mean", 3, "uniform", "c3 with the mean diffusion: n=28 complex64, M=1, 64 iterations"),
     "c4": (32, "c64", 256, 16, "wht", 4, "uniform",
