@@ -69,7 +69,7 @@ std::string u32(unsigned int v) { return std::to_string(v) + "u"; }
 // unrolled at code-generation time).  glb: the program is read from global
 // memory (else it is a __grid_constant__ parameter) -- only merged phase runs
 // read it, with the same GLB flavour as the interpreter would use.
-std::string generate(const GOp<float> *ops, uint64_t nops, bool lin, bool glb) {
+std::string generate(const GOp<float> *ops, uint64_t nops, bool lin, bool glb, bool l2) {
     std::string b;
     b += "#include \"gate_kernels.cuh\"\nusing namespace sv;\n";
     // co-resident CTAs per SM the kernel is compiled for (SV_GATE_JIT_MINB, A/B; default 2 -- the
@@ -82,7 +82,8 @@ std::string generate(const GOp<float> *ops, uint64_t nops, bool lin, bool glb) {
     if (lin && !glb) b += "const __grid_constant__ GProg<float> prog, int nops) {\n    const GOp<float> *ops = prog.op;\n";
     else b += "const GOp<float> *__restrict__ ops, int nops) {\n";
     b += "    (void)ops; (void)nops;\n"
-         "    using L = Layout<float2, " + std::to_string(kGateTileBitsC64) + ", " + std::to_string(kRegBitsC64) + ">;\n"
+         "    using L = " + (l2 ? "Layout2<" + std::to_string(kGateTileBitsC64) + ", " + std::to_string(kRegBitsC64) + ">"
+                          : "Layout<float2, " + std::to_string(kGateTileBitsC64) + ", " + std::to_string(kRegBitsC64) + ">") + ";\n"
          "    extern __shared__ __align__(16) unsigned char smem_raw[];\n"
          "    float2 *sm = reinterpret_cast<float2 *>(smem_raw);\n"
          "    const int tid = threadIdx.x;\n"
@@ -241,20 +242,20 @@ int gate_jit_mode() {
     return strcmp(e, "0") == 0 ? 0 : 1;
 }
 
-std::string gate_jit_source(const void *host_ops, uint64_t nops, bool lin, bool glb) {
-    return generate(reinterpret_cast<const GOp<float> *>(host_ops), nops, lin, glb);
+std::string gate_jit_source(const void *host_ops, uint64_t nops, bool lin, bool glb, bool l2) {
+    return generate(reinterpret_cast<const GOp<float> *>(host_ops), nops, lin, glb, l2);
 }
 
 // Before a run_gates call launches anything (host work only; module loads
 // stay out of the passes' profiling events): decide and, where due, compile
 // this pass's kernel.  Returns the kernel to launch, or nullptr for the
 // interpreter.  `call` numbers the run_gates calls (>= 1).
-void *gate_jit_prepare(const void *host_ops, uint64_t nops, bool lin, bool param, unsigned long long ntiles,
+void *gate_jit_prepare(const void *host_ops, uint64_t nops, bool lin, bool param, bool l2, unsigned long long ntiles,
                        uint64_t call) {
     const int mode = gate_jit_mode();
     if (mode == 0 || host_ops == nullptr) return nullptr;
     if (mode == 2 && ntiles < (1ull << 11)) return nullptr;
-    const std::string src = generate(reinterpret_cast<const GOp<float> *>(host_ops), nops, lin, !param);
+    const std::string src = generate(reinterpret_cast<const GOp<float> *>(host_ops), nops, lin, !param, l2);
     std::lock_guard<std::mutex> lk(J().mu);
     auto it = J().cache.find(src);
     if (it == J().cache.end()) {
@@ -301,8 +302,8 @@ void launch_gate_jit(void *kern, const KParams &kp, const void *dev_ops, const v
 }
 
 // NVRTC only (no device): the cubin size of the pass kernel, for host tests.
-size_t gate_jit_compile_only(const void *host_ops, uint64_t nops, bool lin, bool glb) {
-    return compile_cubin(generate(reinterpret_cast<const GOp<float> *>(host_ops), nops, lin, glb)).size();
+size_t gate_jit_compile_only(const void *host_ops, uint64_t nops, bool lin, bool glb, bool l2) {
+    return compile_cubin(generate(reinterpret_cast<const GOp<float> *>(host_ops), nops, lin, glb, l2)).size();
 }
 
 void gate_jit_stats(uint64_t *compiles, double *seconds) {

@@ -179,14 +179,20 @@ __device__ __forceinline__ void gate_dispatch(E (&x)[L::NR], const R (&m)[kNM<R>
 
 template <class L, typename E>
 __device__ __forceinline__ void relayout_dyn(E (&x)[L::NR], E *sm, int tid, unsigned int from, unsigned int to) {
-    switch (from * 3 + to) {
-        case 1: relayout<L, 0, 1>(x, sm, tid); break;
-        case 2: relayout<L, 0, 2>(x, sm, tid); break;
-        case 3: relayout<L, 1, 0>(x, sm, tid); break;
-        case 5: relayout<L, 1, 2>(x, sm, tid); break;
-        case 6: relayout<L, 2, 0>(x, sm, tid); break;
-        case 7: relayout<L, 2, 1>(x, sm, tid); break;
-        default: break;
+    if constexpr (L::kNPH == 2) {  // two-layout family: A <-> B only
+        if (from == 0 && to == 1) relayout<L, 0, 1>(x, sm, tid);
+        else if (from == 1 && to == 0) relayout<L, 1, 0>(x, sm, tid);
+        return;
+    } else {
+        switch (from * 3 + to) {
+            case 1: relayout<L, 0, 1>(x, sm, tid); break;
+            case 2: relayout<L, 0, 2>(x, sm, tid); break;
+            case 3: relayout<L, 1, 0>(x, sm, tid); break;
+            case 5: relayout<L, 1, 2>(x, sm, tid); break;
+            case 6: relayout<L, 2, 0>(x, sm, tid); break;
+            case 7: relayout<L, 2, 1>(x, sm, tid); break;
+            default: break;
+        }
     }
 }
 
@@ -351,8 +357,8 @@ __device__ __forceinline__ void gate_tile_store(const E (&x)[L::NR], unsigned in
                                                 unsigned long long base, int tid, E *const *s_dst) {
     E *gout = reinterpret_cast<E *>(p.out) + base;
     if (cur == 0) pass_store<L, 0, XCHG>(x, gout, base, p, tid, s_dst);
-    else if (cur == 1) pass_store<L, 1, XCHG>(x, gout, base, p, tid, s_dst);
-    else pass_store<L, 2, XCHG>(x, gout, base, p, tid, s_dst);
+    else if (cur == 1 || L::kNPH == 2) pass_store<L, 1, XCHG>(x, gout, base, p, tid, s_dst);
+    else pass_store<L, (L::kNPH > 2 ? 2 : 1), XCHG>(x, gout, base, p, tid, s_dst);
 }
 
 template <class L, bool XCHG, bool LIN, bool GLB, typename E, typename R>
@@ -369,11 +375,24 @@ __device__ __forceinline__ void gate_tile_body(const KParams &p, const GOp<R> *o
     gate_tile_store<L, XCHG>(x, cur, p, base, tid, s_dst);
 }
 
+// The register-layout family of a gate pass: the three-layout Layout (16-B
+// accesses) or, for complex64 strided passes whose non-diagonal targets start
+// at tile bit 3 or 4 (the WHT's rule), the two-layout Layout2 (one relayout per
+// A <-> B round trip, 8-B accesses; gates.cu gate_pass_l2).
+template <typename E, int TB, int RB, bool L2>
+struct GateLayout {
+    using T = Layout<E, TB, RB>;
+};
+template <int TB, int RB>
+struct GateLayout<float2, TB, RB, true> {
+    using T = Layout2<TB, RB>;
+};
+
 // One CTA per tile; the op program in global memory.
-template <typename E, int TB, int RB, bool XCHG, bool LIN>
+template <typename E, int TB, int RB, bool XCHG, bool LIN, bool L2 = false>
 __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB <= 7) ? 4 : 2)
     gate_tile_kernel(const KParams p, const GOp<typename RealOf<E>::T> *__restrict__ ops, int nops) {
-    gate_tile_body<Layout<E, TB, RB>, XCHG, LIN, true, E>(p, ops, nops);
+    gate_tile_body<typename GateLayout<E, TB, RB, L2>::T, XCHG, LIN, true, E>(p, ops, nops);
 }
 
 // The same with the op program as a kernel parameter (constant bank: uniform
@@ -383,10 +402,10 @@ template <typename R>
 struct GProg {
     GOp<R> op[kParamProgBytes / sizeof(GOp<R>)];
 };
-template <typename E, int TB, int RB, bool XCHG, bool LIN>
+template <typename E, int TB, int RB, bool XCHG, bool LIN, bool L2 = false>
 __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB <= 7) ? 4 : 2)
     gate_tile_kernel_p(const KParams p, const __grid_constant__ GProg<typename RealOf<E>::T> prog, int nops) {
-    gate_tile_body<Layout<E, TB, RB>, XCHG, LIN, false, E>(p, prog.op, nops);
+    gate_tile_body<typename GateLayout<E, TB, RB, L2>::T, XCHG, LIN, false, E>(p, prog.op, nops);
 }
 
 // Whole state (n <= T) in one CTA: every gate as a V/2-pair loop over shared

@@ -33,17 +33,54 @@
 namespace sv {
 
 // gate_jit.cu: pass-specialised kernels compiled at run time (complex64, no exchange store)
-void *gate_jit_prepare(const void *host_ops, uint64_t nops, bool lin, bool param, unsigned long long ntiles,
+void *gate_jit_prepare(const void *host_ops, uint64_t nops, bool lin, bool param, bool l2, unsigned long long ntiles,
                        uint64_t call);
 void launch_gate_jit(void *kern, const KParams &kp, const void *dev_ops, const void *host_ops, uint64_t nops,
                      bool lin, bool param, unsigned long long ntiles, cudaStream_t s);
-size_t gate_jit_compile_only(const void *host_ops, uint64_t nops, bool lin, bool glb);
+size_t gate_jit_compile_only(const void *host_ops, uint64_t nops, bool lin, bool glb, bool l2);
 void gate_jit_stats(uint64_t *compiles, double *seconds);
 
 // ------------------------------------------------------------------------- //
 // Host: op programs                                                          //
 // ------------------------------------------------------------------------- //
 namespace {
+
+// SV_GATE_L2=0: every tile pass on the three-layout family (A/B).
+bool gate_l2_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("SV_GATE_L2");
+        return !(e && strcmp(e, "0") == 0);
+    }();
+    return on;
+}
+
+// The two-layout family (Layout2, wht_kernels.cuh) for a complex64 tile pass
+// whose non-diagonal gate targets all lie on tile bits >= 3 with the lowest at
+// 3 or 4 -- a strided pass with 64-128 B runs, the WHT's rule for Layout2
+// (SV_2LAYOUT_MAX_U).  Diagonal gates and merged phase runs need no register
+// target.  A pure function of the pass, so the program builder, the launcher
+// and the relayout count agree.
+bool gate_pass_l2(sv_dtype dt, const GatePassArgs &a) {
+    if (dt != SV_C64 || !gate_l2_enabled()) return false;
+    int slot2bit[64];
+    for (int i = 0; i < 64; ++i) slot2bit[i] = -1;
+    int b = 0;
+    for (int sl = 0; sl < 64; ++sl)
+        if ((a.tile_mask >> sl) & 1) slot2bit[sl] = b++;
+    if (b != kGateTileBitsC64) return false;
+    int lo = 64;
+    for (uint64_t k = 0; k < a.count; ++k) {
+        const sv_gate &g = a.gates[a.order[k]];
+        if (gate_diag(g)) continue;
+        const int bt = slot2bit[gate_phys(g.target, a.nl, a.g, a.swapped)];
+        if (bt >= 0 && bt < lo) lo = bt;
+    }
+    static const int max_u = [] {  // SV_GATE_L2_MAXU: A/B of the upper bound
+        const char *e = getenv("SV_GATE_L2_MAXU");
+        return e ? atoi(e) : SV_2LAYOUT_MAX_U;
+    }();
+    return lo >= 3 && lo <= max_u && lo < 64;
+}
 
 unsigned int gate_kind(const sv_gate &g) {
     const double *m = g.m;
@@ -209,7 +246,7 @@ void build_tile_ops(const GatePassArgs &a, std::vector<GOp<R>> &out) {
         ready_in(cur, &take);
         if (take.empty()) {
             int best = -1, bc = -1;
-            for (int ph = 0; ph < 3; ++ph) {
+            for (int ph = 0; ph < L::kNPH; ++ph) {
                 if (ph == cur) continue;
                 const int c = ready_in(ph, nullptr);
                 if (c > bc) { bc = c; best = ph; }
@@ -352,6 +389,7 @@ void launch_tile_gates(const GatePassArgs &a, const void *dev_ops, const void *h
     const unsigned long long ntiles = 1ull << f;
     SV_CHECK(ntiles <= 0x7fffffffull, SV_EINVAL, "too many tiles for one launch");
     const int smem = (1 << TB) * (int)sizeof(E);
+    const bool l2 = gate_pass_l2(sizeof(E) == 8 ? SV_C64 : SV_C128, a);
     static bool attr = false;
     if (!attr) {
         for (auto f : {gate_tile_kernel<E, TB, RB, true, true>, gate_tile_kernel<E, TB, RB, false, true>,
@@ -360,6 +398,15 @@ void launch_tile_gates(const GatePassArgs &a, const void *dev_ops, const void *h
         for (auto f : {gate_tile_kernel_p<E, TB, RB, true, true>, gate_tile_kernel_p<E, TB, RB, false, true>,
                        gate_tile_kernel_p<E, TB, RB, true, false>, gate_tile_kernel_p<E, TB, RB, false, false>})
             SV_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        if constexpr (sizeof(E) == 8) {
+            for (auto f : {gate_tile_kernel<E, TB, RB, true, true, true>, gate_tile_kernel<E, TB, RB, false, true, true>,
+                           gate_tile_kernel<E, TB, RB, true, false, true>, gate_tile_kernel<E, TB, RB, false, false, true>})
+                SV_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            for (auto f : {gate_tile_kernel_p<E, TB, RB, true, true, true>, gate_tile_kernel_p<E, TB, RB, false, true, true>,
+                           gate_tile_kernel_p<E, TB, RB, true, false, true>,
+                           gate_tile_kernel_p<E, TB, RB, false, false, true>})
+                SV_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        }
         attr = true;
     }
     constexpr uint64_t cap = sizeof(GProg<R>) / sizeof(GOp<R>);
@@ -368,7 +415,8 @@ void launch_tile_gates(const GatePassArgs &a, const void *dev_ops, const void *h
         // interpreter's result; same program flavour for merged phase runs)
         const bool param = host_ops != nullptr && nops <= cap && gate_param_ops();
         if (a.jit_prepare) {
-            if (!kp.xchg && a.jit_kern) *a.jit_kern = gate_jit_prepare(host_ops, nops, lin, param, ntiles, a.jit_prepare);
+            if (!kp.xchg && a.jit_kern)
+                *a.jit_kern = gate_jit_prepare(host_ops, nops, lin, param, l2, ntiles, a.jit_prepare);
             return;
         }
         if (!kp.xchg && a.jit_kern && *a.jit_kern) {
@@ -377,15 +425,26 @@ void launch_tile_gates(const GatePassArgs &a, const void *dev_ops, const void *h
         }
     }
     if (a.jit_prepare) return;
-    if (host_ops != nullptr && nops <= cap && gate_param_ops()) {
+    const bool param = host_ops != nullptr && nops <= cap && gate_param_ops();
+    // (xchg, lin, l2) -> instantiation
+    auto pick = [&](auto k_ff, auto k_tf, auto k_ft, auto k_tt) { return kp.xchg ? (lin ? k_tt : k_tf) : (lin ? k_ft : k_ff); };
+    if (param) {
         auto prog = std::make_unique<GProg<R>>();
         memcpy(prog->op, host_ops, nops * sizeof(GOp<R>));
-        auto fn = lin ? (kp.xchg ? gate_tile_kernel_p<E, TB, RB, true, true> : gate_tile_kernel_p<E, TB, RB, false, true>)
-                      : (kp.xchg ? gate_tile_kernel_p<E, TB, RB, true, false> : gate_tile_kernel_p<E, TB, RB, false, false>);
+        auto fn = pick(gate_tile_kernel_p<E, TB, RB, false, false>, gate_tile_kernel_p<E, TB, RB, true, false>,
+                       gate_tile_kernel_p<E, TB, RB, false, true>, gate_tile_kernel_p<E, TB, RB, true, true>);
+        if constexpr (sizeof(E) == 8)
+            if (l2)
+                fn = pick(gate_tile_kernel_p<E, TB, RB, false, false, true>, gate_tile_kernel_p<E, TB, RB, true, false, true>,
+                          gate_tile_kernel_p<E, TB, RB, false, true, true>, gate_tile_kernel_p<E, TB, RB, true, true, true>);
         fn<<<(unsigned int)ntiles, L::NT, smem, s>>>(kp, *prog, (int)nops);
     } else {
-        auto fn = lin ? (kp.xchg ? gate_tile_kernel<E, TB, RB, true, true> : gate_tile_kernel<E, TB, RB, false, true>)
-                      : (kp.xchg ? gate_tile_kernel<E, TB, RB, true, false> : gate_tile_kernel<E, TB, RB, false, false>);
+        auto fn = pick(gate_tile_kernel<E, TB, RB, false, false>, gate_tile_kernel<E, TB, RB, true, false>,
+                       gate_tile_kernel<E, TB, RB, false, true>, gate_tile_kernel<E, TB, RB, true, true>);
+        if constexpr (sizeof(E) == 8)
+            if (l2)
+                fn = pick(gate_tile_kernel<E, TB, RB, false, false, true>, gate_tile_kernel<E, TB, RB, true, false, true>,
+                          gate_tile_kernel<E, TB, RB, false, true, true>, gate_tile_kernel<E, TB, RB, true, true, true>);
         fn<<<(unsigned int)ntiles, L::NT, smem, s>>>(kp, reinterpret_cast<const GOp<R> *>(dev_ops), (int)nops);
     }
     SV_CUDA(cudaGetLastError());
@@ -431,6 +490,7 @@ uint64_t build_gate_ops(sv_dtype dt, const GatePassArgs &a, bool whole, std::vec
     if (dt == SV_C64) {
         std::vector<GOp<float>> ops;
         if (whole) whole_ops<float2>(a, ops);
+        else if (gate_pass_l2(dt, a)) build_tile_ops<Layout2<kGateTileBitsC64, kRegBitsC64>, float>(a, ops);
         else build_tile_ops<Layout<float2, kGateTileBitsC64, kRegBitsC64>, float>(a, ops);
         if (has_lin) *has_lin = lin_in(ops);
         return append_ops(ops, prog);
@@ -460,7 +520,8 @@ static uint64_t relayouts_of(const std::vector<GOp<R>> &ops) {
 uint64_t count_gate_relayouts(sv_dtype dt, const GatePassArgs &a) {
     if (dt == SV_C64) {
         std::vector<GOp<float>> ops;
-        build_tile_ops<Layout<float2, kGateTileBitsC64, kRegBitsC64>, float>(a, ops);
+        if (gate_pass_l2(dt, a)) build_tile_ops<Layout2<kGateTileBitsC64, kRegBitsC64>, float>(a, ops);
+        else build_tile_ops<Layout<float2, kGateTileBitsC64, kRegBitsC64>, float>(a, ops);
         return relayouts_of(ops);
     }
     std::vector<GOp<double>> ops;
@@ -502,7 +563,9 @@ extern "C" sv_status sv_debug_gate_jit(int n, sv_dtype dtype, const sv_gate *gat
                 std::vector<unsigned char> prog;
                 bool lin = false;
                 const uint64_t nops = build_gate_ops(dtype, a, false, prog, &lin);
-                for (bool glb : {false, true}) SV_CHECK(gate_jit_compile_only(prog.data(), nops, lin, glb) > 0, SV_ECUDA, "empty cubin");
+                const bool l2 = gate_pass_l2(dtype, a);
+                for (bool glb : {false, true})
+                    SV_CHECK(gate_jit_compile_only(prog.data(), nops, lin, glb, l2) > 0, SV_ECUDA, "empty cubin");
                 ++np;
             }
             if (passes) *passes = np;

@@ -55,6 +55,7 @@ struct Layout {
     static constexpr int NT = 1 << (TB - RB);             // threads
     static constexpr int NR = 1 << RB;                    // amplitudes per thread
     static constexpr int kTB = TB, kRB = RB;
+    static constexpr int kNPH = 3;                        // register layouts A, B, C
     // complex64: tile bit 0 is a register bit in EVERY layout, so each thread
     // always holds adjacent pairs (e, e|1) = 16 bytes -> every shared and
     // global access is 128-bit; the other RB-1 register bits cover 3(RB-1)
@@ -121,6 +122,7 @@ struct Layout2 {
     static constexpr int NT = 1 << (TB - RB);
     static constexpr int NR = 1 << RB;
     static constexpr int kTB = TB, kRB = RB;
+    static constexpr int kNPH = 2;             // register layouts A, B
     static_assert(TB - 2 * RB >= 3, "carry bits 0..2 must stay outside both layouts");
     __host__ __device__ static constexpr int reg_bit(int ph, int i) {
         return ph == 0 ? TB - RB + i : TB - 2 * RB + i;
