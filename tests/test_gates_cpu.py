@@ -151,3 +151,22 @@ def test_gate_jit_sources_compile_with_nvrtc():
         assert r["passes"] == sum(1 for s in steps if s["kind"] == 0) > 0
     with pytest.raises(sv.SvError):
         sv.sv_debug_gate_jit(n, sv.SV_C128, C.qft_circuit(n), True)
+
+
+def test_strided_pass_takes_the_two_layout_family():
+    """A complex64 pass of general unitaries on qubits 3..12 (tile slots 0-12,
+    lowest target tile bit 3) runs on the two-layout family (gates.cu
+    gate_pass_l2): targets 8-12 in layout A, 3-7 in layout B -> ONE relayout.
+    The three-layout family would need two (A holds 9-12, B 3-4, C 5-8);
+    complex128 keeps it (its tiles are 12 bits)."""
+    import os
+    if os.environ.get("SV_GATE_L2") == "0":
+        pytest.skip("two-layout gate passes switched off in this process")
+    rng = np.random.default_rng(5)
+    g = C.circuit([C.record(q, C.random_unitary(rng)) for q in range(3, 13)])
+    steps, _ = sv.sv_plan_gates(16, 1, sv.SV_C64, g)
+    assert len(steps) == 1
+    assert list(sv.sv_debug_gate_relayouts(16, 1, sv.SV_C64, g)) == [1]
+    # a target on tile bit 2 keeps the three-layout family (16-B pairs, layout C)
+    g2 = C.circuit([C.record(q, C.random_unitary(rng)) for q in range(2, 13)])
+    assert list(sv.sv_debug_gate_relayouts(16, 1, sv.SV_C64, g2)) == [2]

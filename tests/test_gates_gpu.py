@@ -294,3 +294,43 @@ def test_phase_runs_global_program_path():
                        env=env, cwd=root, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-2000:]
+
+
+@pytest.mark.parametrize("n", [16, 22])
+def test_two_layout_strided_passes_match_oracle(n):
+    """Complex64 passes whose lowest non-diagonal target is tile bit 3 or 4 run
+    on the two-layout family (gates.cu gate_pass_l2): unitaries, controlled
+    gates (register / thread / tile-slot controls) and phase runs on qubits
+    >= 3, against the oracle; n = 22 puts the targets in strided tiles."""
+    rng = np.random.default_rng(n)
+    recs = []
+    for q in range(3, n):
+        recs.append(C.record(q, C.random_unitary(rng)))
+    for _ in range(60):
+        t, c1, c2 = (int(v) for v in rng.choice(np.arange(3, n), 3, replace=False))
+        recs.append(C.record(t, C.random_unitary(rng), controls=(c1,) if rng.random() < 0.5 else (c1, c2)))
+    for q in range(4, n):
+        recs.append(C.record(q, C.phase(0.1 * q), controls=(3,)))
+    gates = C.circuit(recs)
+    a = rand_state(n, sv.SV_C64, 17)
+    ref = orc.apply_gates(a.copy(), gates)
+    got = run_gpu(a, sv.SV_C64, gates)
+    assert_close(got, ref, sv.SV_C64, len(recs), f"two-layout n={n}")
+
+
+def test_three_layout_family_still_matches_oracle():
+    """SV_GATE_L2=0 (read once per process): the oracle tests of strided
+    circuits rerun in a subprocess on the three-layout family."""
+    import os
+    import subprocess
+    import sys
+    if os.environ.get("SV_GATE_L2") == "0":
+        pytest.skip("this is the subprocess")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SV_GATE_L2="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        "tests/test_gates_gpu.py", "-k",
+                        "random_circuit or structured or two_layout or qft or emulated_sharding"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-2000:]
