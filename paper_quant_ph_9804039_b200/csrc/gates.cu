@@ -54,33 +54,7 @@ bool gate_l2_enabled() {
     return on;
 }
 
-// The two-layout family (Layout2, wht_kernels.cuh) for a complex64 tile pass
-// whose non-diagonal gate targets all lie on tile bits >= 3 with the lowest at
-// 3 or 4 -- a strided pass with 64-128 B runs, the WHT's rule for Layout2
-// (SV_2LAYOUT_MAX_U).  Diagonal gates and merged phase runs need no register
-// target.  A pure function of the pass, so the program builder, the launcher
-// and the relayout count agree.
-bool gate_pass_l2(sv_dtype dt, const GatePassArgs &a) {
-    if (dt != SV_C64 || !gate_l2_enabled()) return false;
-    int slot2bit[64];
-    for (int i = 0; i < 64; ++i) slot2bit[i] = -1;
-    int b = 0;
-    for (int sl = 0; sl < 64; ++sl)
-        if ((a.tile_mask >> sl) & 1) slot2bit[sl] = b++;
-    if (b != kGateTileBitsC64) return false;
-    int lo = 64;
-    for (uint64_t k = 0; k < a.count; ++k) {
-        const sv_gate &g = a.gates[a.order[k]];
-        if (gate_diag(g)) continue;
-        const int bt = slot2bit[gate_phys(g.target, a.nl, a.g, a.swapped)];
-        if (bt >= 0 && bt < lo) lo = bt;
-    }
-    static const int max_u = [] {  // SV_GATE_L2_MAXU: A/B of the upper bound
-        const char *e = getenv("SV_GATE_L2_MAXU");
-        return e ? atoi(e) : SV_2LAYOUT_MAX_U;
-    }();
-    return lo >= 3 && lo <= max_u && lo < 64;
-}
+bool gate_pass_l2(sv_dtype dt, const GatePassArgs &a);
 
 unsigned int gate_kind(const sv_gate &g) {
     const double *m = g.m;
@@ -339,6 +313,55 @@ void build_tile_ops(const GatePassArgs &a, std::vector<GOp<R>> &out) {
 }
 
 template <typename R>
+uint64_t relayouts_of(const std::vector<GOp<R>> &ops) {
+    uint64_t r = 0;
+    unsigned int cur = 0;
+    for (size_t k = 0; k < ops.size(); ++k) {  // as the kernel's op loop walks the program
+        const unsigned int ph = ops[k].ph & 0xffu, kind = ops[k].ph >> 8;
+        if (ph != cur) {
+            ++r;
+            cur = ph;
+        }
+        if (kind == GK_LINPHASE) k += ops[k].tm;  // its entry records
+    }
+    return r;
+}
+
+// The two-layout family (Layout2, wht_kernels.cuh) for a complex64 tile pass
+// whose non-diagonal gate targets all lie on tile bits >= 3 with the lowest at
+// 3 or 4 -- a strided pass with 64-128 B runs, the WHT's rule for Layout2
+// (SV_2LAYOUT_MAX_U) -- unless its program needs more relayouts there than on
+// the three-layout family (gates alternating between A- and B-layout targets
+// without commuting).  Diagonal gates and merged phase runs need no register
+// target.  A pure function of the pass, so the program builder, the launcher
+// and the relayout count agree.
+bool gate_pass_l2(sv_dtype dt, const GatePassArgs &a) {
+    if (dt != SV_C64 || !gate_l2_enabled()) return false;
+    int slot2bit[64];
+    for (int i = 0; i < 64; ++i) slot2bit[i] = -1;
+    int b = 0;
+    for (int sl = 0; sl < 64; ++sl)
+        if ((a.tile_mask >> sl) & 1) slot2bit[sl] = b++;
+    if (b != kGateTileBitsC64) return false;
+    int lo = 64;
+    for (uint64_t k = 0; k < a.count; ++k) {
+        const sv_gate &g = a.gates[a.order[k]];
+        if (gate_diag(g)) continue;
+        const int bt = slot2bit[gate_phys(g.target, a.nl, a.g, a.swapped)];
+        if (bt >= 0 && bt < lo) lo = bt;
+    }
+    static const int max_u = [] {  // SV_GATE_L2_MAXU: A/B of the upper bound
+        const char *e = getenv("SV_GATE_L2_MAXU");
+        return e ? atoi(e) : SV_2LAYOUT_MAX_U;
+    }();
+    if (!(lo >= 3 && lo <= max_u && lo < 64)) return false;
+    std::vector<GOp<float>> o2, o3;
+    build_tile_ops<Layout2<kGateTileBitsC64, kRegBitsC64>, float>(a, o2);
+    build_tile_ops<Layout<float2, kGateTileBitsC64, kRegBitsC64>, float>(a, o3);
+    return relayouts_of(o2) <= relayouts_of(o3);
+}
+
+template <typename R>
 size_t append_ops(const std::vector<GOp<R>> &ops, std::vector<unsigned char> &prog) {
     const size_t off = prog.size();
     prog.resize(off + ops.size() * sizeof(GOp<R>));
@@ -500,21 +523,6 @@ uint64_t build_gate_ops(sv_dtype dt, const GatePassArgs &a, bool whole, std::vec
     else build_tile_ops<Layout<double2, kTileBitsC128, kRegBitsC128>, double>(a, ops);
     if (has_lin) *has_lin = lin_in(ops);
     return append_ops(ops, prog);
-}
-
-template <typename R>
-static uint64_t relayouts_of(const std::vector<GOp<R>> &ops) {
-    uint64_t r = 0;
-    unsigned int cur = 0;
-    for (size_t k = 0; k < ops.size(); ++k) {  // as the kernel's op loop walks the program
-        const unsigned int ph = ops[k].ph & 0xffu, kind = ops[k].ph >> 8;
-        if (ph != cur) {
-            ++r;
-            cur = ph;
-        }
-        if (kind == GK_LINPHASE) k += ops[k].tm;  // its entry records
-    }
-    return r;
 }
 
 uint64_t count_gate_relayouts(sv_dtype dt, const GatePassArgs &a) {
