@@ -25,7 +25,9 @@ KERNELS = [
     ("wht.cu.o", r"wht_tile2_kernel<13, 5, true, true, 4, 0, false>", "F0-fused strided pass (two-layout, U=4)"),
     ("wht.cu.o", r"wht_tile_kernel<float2, 13, 5, true, true, 5, 0, false>", "fused strided pass (U=5, c3)"),
     ("mean.cu.o", r"mean_kernel<float2, true>", "fused flip + invert-about-mean (complex64)"),
-    ("mean_resident.cu.o", r"mean_resident_kernel<double2>", "shared-memory-resident mean (c2)"),
+    ("mean_resident.cu.o", r"mean_resident_kernel<double2>", "shared-memory-resident mean (A/B, SV_MEAN_RESIDENT=smem)"),
+    ("mean_resident.cu.o", r"mean_resreg_kernel<double2, 16, 512>", "register-resident mean (c2)"),
+    ("gates.cu.o", r"gate_tile_kernel_p<float2, 13, 5, false, false, true>", "gate interpreter, two-layout family"),
 ]
 CLASSES = {
     "FADD2": r"^FADD2\b", "FFMA2": r"^FFMA2\b", "FMUL2": r"^FMUL2\b", "FADD": r"^FADD\b", "FFMA": r"^FFMA\b",
