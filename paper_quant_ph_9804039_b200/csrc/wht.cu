@@ -282,8 +282,12 @@ __device__ __forceinline__ void shfl_stage(E &x, int d, bool hi, const double *c
     y.x = __shfl_xor_sync(0xffffffffu, x.x, d);
     y.y = __shfl_xor_sync(0xffffffffu, x.y, d);
     if constexpr (!GEN) {  // ideal butterfly: (a_i, a_j) -> (a_i + a_j, a_i - a_j)
-        if (!hi) { x.x = x.x + y.x; x.y = x.y + y.y; }
-        else { x.x = y.x - x.x; x.y = y.y - x.y; }
+        // one FMA by +-1 per component: lo lanes x + y, hi lanes y - x -- the
+        // same single rounding as the add / subtract (bitwise identical), but
+        // without computing both and selecting (2 adds + 4 selects per element)
+        const R sg = hi ? (R)-1 : (R)1;
+        x.x = fma(sg, x.x, y.x);
+        x.y = fma(sg, x.y, y.y);
     } else {  // Fig. 3's [w x; y z]: a_i' = w a_i + x a_j, a_j' = y a_i + z a_j
         const R w = (R)c[0], xx = (R)c[1], yy = (R)c[2], z = (R)c[3];
         if (!hi) { x.x = w * x.x + xx * y.x; x.y = w * x.y + xx * y.y; }
