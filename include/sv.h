@@ -125,8 +125,9 @@ sv_status sv_diffuse(sv_ctx *ctx, sv_diffusion diffusion);
  * allreduce (Eq. 3's accumulate-and-redistribute).  On one GPU
  * a state of <= 16 (complex128) / 32 (complex64) amplitudes per thread of one
  * 512-thread block per SM (c2: n = 20) runs all k MEAN iterations in ONE
- * cooperative launch with the state in registers and one grid-wide fp64 sum
- * per iteration (SV_MEAN_RESIDENT=0 / smem: per-iteration launches / the
+ * cooperative launch with the state in registers and one grid-wide sum per
+ * iteration (exact fixed-point integer atomics, deterministic; SV_RESREG_FX=0:
+ * fp64 partials; SV_MEAN_RESIDENT=0 / smem: per-iteration launches / the
  * shared-memory resident kernel); the results agree within the dtype tolerance.
  * Errors: SV_EINVAL (k < 0), SV_ESTATE (no marked set was ever given). */
 sv_status sv_iterate(sv_ctx *ctx, int k, sv_diffusion diffusion);

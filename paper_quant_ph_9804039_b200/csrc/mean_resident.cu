@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "sv_internal.h"
 
@@ -218,10 +219,12 @@ __global__ void __launch_bounds__(kResThreads, 1)
 //     registers hold b = O a between iterations and one pass per iteration
 //     computes a' = 2 mu - b, b' = O a' (a sign-bit flip) and the fp64 sums
 //     of b' -- exactly sum(O a'), the next mu, with no separate marked pass;
-//   * the block total is folded by warp 0 (a 5-level shuffle tree), published
-//     as one 16-B partial, counted in with ONE release-add on a monotonic
+//   * the block total is folded by warp 0 (a 5-level shuffle tree); the
+//     per-iteration grid sums are exact fixed-point integer atomics (FX,
+//     the default; see fx_total), the first rounds (and FX = false) publish
+//     one 16-B fp64 partial, count in with ONE release-add on a monotonic
 //     64-bit counter (zeroed before the launch; round r is complete at
-//     (r + 1) x grid), and gathered with all of a lane's partials in flight.
+//     (r + 1) x grid) and gather with all of a lane's partials in flight.
 // Measured alternatives (tools/mean_resident_scan.py): flag-in-word
 // all-gather polling, counter + flag-in-word partials, and a last-arriver
 // broadcast into per-block lines were all slower (polling contention on L2).
@@ -232,6 +235,19 @@ __device__ __forceinline__ void red_release_add_u64(unsigned long long *p, unsig
     asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 constexpr int kResRegMaxGrid = 160;  // blocks (one per SM; B200: 148)
+__device__ __forceinline__ void red_relaxed_add_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+constexpr int kAccWords = 64;  // uint64 per iteration slot of the fixed-point sums: 4 words, 128 B apart
+__device__ __forceinline__ void ld_relaxed_v2_u64(const unsigned long long *p, unsigned long long &a,
+                                                  unsigned long long &b) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
 #ifndef SV_RESREG_TRACE
 #define SV_RESREG_TRACE 0  // 1: clock64 phase sums per round, printed by 3 blocks (A/B builds only)
 #endif
@@ -244,11 +260,13 @@ __device__ __forceinline__ float flip_if(float x, unsigned int s) {
     return __int_as_float(__float_as_int(x) ^ (int)(s << 31));
 }
 
-template <typename E, int NPT, int NT>
+// FX: the per-iteration grid sums as exact fixed-point integer adds (see
+// fx_total below); false: fp64 partials + gather for every round.
+template <typename E, int NPT, int NT, bool FX>
 __global__ void __launch_bounds__(NT, 1)
     mean_resreg_kernel(E *a, unsigned long long N, unsigned long long C, double inv_N,
                        const unsigned long long *marked, unsigned long long n_marked, int k, double2 *partials,
-                       unsigned long long *ctr) {
+                       unsigned long long *ctr, unsigned long long *acc) {
     using R = decltype(E{}.x);
     __shared__ double red[66];
     __shared__ unsigned long long s_mlo, s_mcnt;
@@ -372,6 +390,79 @@ __global__ void __launch_bounds__(NT, 1)
     double tr, ti;
     unsigned int round = 0;
     grid_total(r, m, round++, tr, ti);
+    // Fixed-point rounds (FX).  Every later sum is of b' = O a' over a subset
+    // of the state, so |sum| <= sqrt(N) ||a|| (Cauchy-Schwarz; D and O are
+    // unitary).  One more fp64 round gives ||a||^2; every block derives the
+    // same scale 2^sh with 2 sqrt(N) ||a|| 2^sh < 2^54 and, per iteration,
+    // adds its partial as two's-complement integers (a high word at 2^-sh and
+    // a low word at 2^-(sh+48)), each with an arrival count in its low 8 bits
+    // -- four relaxed 64-bit atomics into this iteration's own zeroed slot.
+    // Integer adds commute, so the total is the same bits in every block and
+    // run (deterministic, G14) and it is the EXACT sum of the partials to
+    // 2^-(sh+48) ~ 1e-29 of sqrt(N) ||a||, rounded to fp64 once (the fp64
+    // gather rounds 148 times); count and data share each word, so no fence
+    // and no gather: a block polls one 32-B slot until all four counts reach
+    // the grid size.
+    int sh = 0;
+    if constexpr (FX) {
+        double q = 0.0;
+#pragma unroll
+        for (int j = 0; j < NPT; ++j)
+            if (j < nv) q += (double)v[j].x * (double)v[j].x + (double)v[j].y * (double)v[j].y;
+        double tq, tdummy;
+        grid_total(q, 0.0, round++, tq, tdummy);
+        int e = 0;
+        frexp(2.0 * sqrt((double)N * tq) + 1e-300, &e);  // bound < 2^e
+        sh = 54 - e;
+        sh = sh > 1000 ? 1000 : sh;
+    }
+    auto fx_total = [&](double r, double m, unsigned int slot, double &tr, double &ti) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            r += __shfl_xor_sync(0xffffffffu, r, o);
+            m += __shfl_xor_sync(0xffffffffu, m, o);
+        }
+        if (lane == 0) { red[2 * w] = r; red[2 * w + 1] = m; }
+        __syncthreads();
+        if (w == 0) {
+            double R0 = lane < NT / 32 ? red[2 * lane] : 0.0, M0 = lane < NT / 32 ? red[2 * lane + 1] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                R0 += __shfl_xor_sync(0xffffffffu, R0, o);
+                M0 += __shfl_xor_sync(0xffffffffu, M0, o);
+            }
+            if (lane == 0) {
+                // each component as hi + lo * 2^-48 (a 101-bit fixed-point value, exact
+                // to far below the partial's own fp64 rounding); the four words of the
+                // slot -- re_hi, im_hi, re_lo, im_lo -- sit on their own 128-B lines
+                // (L2 atomics on one line serialise: 4 x 148 on one line measured slower)
+                unsigned long long *sl = acc + (size_t)kAccWords * slot;
+                const double xr = ldexp(R0, sh), xi = ldexp(M0, sh);
+                const long long hr = __double2ll_rn(xr), hi_ = __double2ll_rn(xi);
+                const long long lr = __double2ll_rn(ldexp(xr - (double)hr, 48));
+                const long long li = __double2ll_rn(ldexp(xi - (double)hi_, 48));
+                red_relaxed_add_u64(sl, ((unsigned long long)hr << 8) + 1ull);
+                red_relaxed_add_u64(sl + 16, ((unsigned long long)hi_ << 8) + 1ull);
+                red_relaxed_add_u64(sl + 32, ((unsigned long long)lr << 8) + 1ull);
+                red_relaxed_add_u64(sl + 48, ((unsigned long long)li << 8) + 1ull);
+                unsigned long long w0, w1, w2, w3;
+                do {
+                    w0 = ld_relaxed_u64(sl);
+                    w1 = ld_relaxed_u64(sl + 16);
+                    w2 = ld_relaxed_u64(sl + 32);
+                    w3 = ld_relaxed_u64(sl + 48);
+                } while ((w0 & 0xffull) != nb || (w1 & 0xffull) != nb || (w2 & 0xffull) != nb ||
+                         (w3 & 0xffull) != nb);
+                // wrapped intermediate sums are harmless: the final integer fits
+                red[64] = ldexp((double)((long long)w0 >> 8) + ldexp((double)((long long)w2 >> 8), -48), -sh);
+                red[65] = ldexp((double)((long long)w1 >> 8) + ldexp((double)((long long)w3 >> 8), -48), -sh);
+            }
+        }
+        __syncthreads();
+        tr = red[64];
+        ti = red[65];
+    };
+    (void)fx_total;
     // invariant at the top of an iteration: v holds b = O a and (tr, ti) = sum(b)
     for (int it = 0; it < k; ++it) {
         const R two_mr = (R)(2.0 * tr * inv_N), two_mi = (R)(2.0 * ti * inv_N);
@@ -395,7 +486,8 @@ __global__ void __launch_bounds__(NT, 1)
                 m += (double)v[j].y;
             }
         }
-        grid_total(r, m, round++, tr, ti);
+        if constexpr (FX) fx_total(r, m, (unsigned int)it, tr, ti);
+        else grid_total(r, m, round++, tr, ti);
     }
 #pragma unroll
     for (int j = 0; j < NPT; ++j)
@@ -451,20 +543,20 @@ size_t mean_resident_slot_bytes(sv_dtype dt, uint64_t N) {
 // 65536 / NT (ptxas -v: no spills in any of them).
 struct ResRegCfg {
     int nt, npt;
-    void *fn;
+    void *fn[2];  // [FX]
 };
 static const ResRegCfg *resreg_cfg(sv_dtype dt, uint64_t C) {
-    static const ResRegCfg t64[] = {{512, 1, (void *)mean_resreg_kernel<float2, 1, 512>},
-                                    {512, 2, (void *)mean_resreg_kernel<float2, 2, 512>},
-                                    {512, 4, (void *)mean_resreg_kernel<float2, 4, 512>},
-                                    {512, 8, (void *)mean_resreg_kernel<float2, 8, 512>},
-                                    {512, 16, (void *)mean_resreg_kernel<float2, 16, 512>},
-                                    {512, 32, (void *)mean_resreg_kernel<float2, 32, 512>}};
-    static const ResRegCfg t128[] = {{512, 1, (void *)mean_resreg_kernel<double2, 1, 512>},
-                                     {512, 2, (void *)mean_resreg_kernel<double2, 2, 512>},
-                                     {512, 4, (void *)mean_resreg_kernel<double2, 4, 512>},
-                                     {512, 8, (void *)mean_resreg_kernel<double2, 8, 512>},
-                                     {512, 16, (void *)mean_resreg_kernel<double2, 16, 512>}};
+    static const ResRegCfg t64[] = {{512, 1, {(void *)mean_resreg_kernel<float2, 1, 512, false>, (void *)mean_resreg_kernel<float2, 1, 512, true>}},
+                                    {512, 2, {(void *)mean_resreg_kernel<float2, 2, 512, false>, (void *)mean_resreg_kernel<float2, 2, 512, true>}},
+                                    {512, 4, {(void *)mean_resreg_kernel<float2, 4, 512, false>, (void *)mean_resreg_kernel<float2, 4, 512, true>}},
+                                    {512, 8, {(void *)mean_resreg_kernel<float2, 8, 512, false>, (void *)mean_resreg_kernel<float2, 8, 512, true>}},
+                                    {512, 16, {(void *)mean_resreg_kernel<float2, 16, 512, false>, (void *)mean_resreg_kernel<float2, 16, 512, true>}},
+                                    {512, 32, {(void *)mean_resreg_kernel<float2, 32, 512, false>, (void *)mean_resreg_kernel<float2, 32, 512, true>}}};
+    static const ResRegCfg t128[] = {{512, 1, {(void *)mean_resreg_kernel<double2, 1, 512, false>, (void *)mean_resreg_kernel<double2, 1, 512, true>}},
+                                     {512, 2, {(void *)mean_resreg_kernel<double2, 2, 512, false>, (void *)mean_resreg_kernel<double2, 2, 512, true>}},
+                                     {512, 4, {(void *)mean_resreg_kernel<double2, 4, 512, false>, (void *)mean_resreg_kernel<double2, 4, 512, true>}},
+                                     {512, 8, {(void *)mean_resreg_kernel<double2, 8, 512, false>, (void *)mean_resreg_kernel<double2, 8, 512, true>}},
+                                     {512, 16, {(void *)mean_resreg_kernel<double2, 16, 512, false>, (void *)mean_resreg_kernel<double2, 16, 512, true>}}};
     const ResRegCfg *t = dt == SV_C64 ? t64 : t128;
     for (int i = 0; i < (dt == SV_C64 ? 6 : 5); ++i)
         if ((uint64_t)t[i].nt * t[i].npt >= C) return &t[i];
@@ -473,7 +565,7 @@ static const ResRegCfg *resreg_cfg(sv_dtype dt, uint64_t C) {
 
 void launch_mean_resident(sv_dtype dt, void *a, uint64_t N, double inv_N, const uint64_t *marked, uint64_t m, int k,
                           double *partials, unsigned int *bar, void *slots, unsigned long long epoch0, bool regs,
-                          cudaStream_t s) {
+                          void *acc, cudaStream_t s) {
     int grid, smem;
     uint64_t C;
     void *fn;
@@ -484,7 +576,13 @@ void launch_mean_resident(sv_dtype dt, void *a, uint64_t N, double inv_N, const 
     const ResRegCfg *rc = regs ? resreg_cfg(dt, C) : nullptr;
     if (rc != nullptr) {
         int per = 0, dev = 0, sms = 0;
-        SV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rc->fn, rc->nt, 0));
+        static const int fx_env = [] {  // SV_RESREG_FX=0: fp64 partials + gather every round (A/B)
+            const char *e = getenv("SV_RESREG_FX");
+            return e ? atoi(e) : 1;
+        }();
+        const bool fx = fx_env != 0 && acc != nullptr;
+        void *rfn = rc->fn[fx ? 1 : 0];
+        SV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rfn, rc->nt, 0));
         SV_CUDA(cudaGetDevice(&dev));
         SV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         if (per >= 1 && grid <= per * sms && grid <= kResRegMaxGrid) {
@@ -492,8 +590,10 @@ void launch_mean_resident(sv_dtype dt, void *a, uint64_t N, double inv_N, const 
             unsigned long long *ctr = reinterpret_cast<unsigned long long *>(bar + 2);
             SV_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s));
             double2 *part2 = reinterpret_cast<double2 *>(partials);
-            void *args[] = {&a, &Nl, &Cl, &inv_N, &mk, &ml, &k, &part2, &ctr};
-            SV_CUDA(cudaLaunchCooperativeKernel(rc->fn, dim3(grid), dim3(rc->nt), args, 0, s));
+            unsigned long long *acc64 = reinterpret_cast<unsigned long long *>(acc);
+            if (fx) SV_CUDA(cudaMemsetAsync(acc64, 0, kAccWords * sizeof(unsigned long long) * (size_t)k, s));
+            void *args[] = {&a, &Nl, &Cl, &inv_N, &mk, &ml, &k, &part2, &ctr, &acc64};
+            SV_CUDA(cudaLaunchCooperativeKernel(rfn, dim3(grid), dim3(rc->nt), args, 0, s));
             return;
         }
     }

@@ -99,6 +99,8 @@ struct sv_ctx {
     unsigned int *d_gbar = nullptr;  // grid barrier of the persistent mean kernel {count, generation}
     void *d_res_slots = nullptr;     // resident mean kernel: per-block published totals (two rounds)
     unsigned long long res_epoch = 0;  // last epoch handed to the resident mean kernel
+    void *d_res_acc = nullptr;       // resident mean kernel: fixed-point per-iteration sums (512 B each)
+    size_t res_acc_cap = 0;          // iterations d_res_acc holds
     bool mean_resident = true;       // SV_MEAN_RESIDENT=0 disables the one-launch path
     bool mean_resreg = true;         // SV_MEAN_RESIDENT=smem: the shared-memory resident kernel (A/B)
     int mgrid = 1;
@@ -764,12 +766,20 @@ void run_mean(sv_ctx *c, int k, bool with_oracle) {
             dmalloc(&c->d_res_slots, b, "resident mean slots");
             SV_CUDA(cudaMemsetAsync(c->d_res_slots, 0, b, c->stream));
         }
+        if (c->res_acc_cap < (size_t)reps) {  // grown, never shrunk
+            if (c->d_res_acc) SV_CUDA(cudaFree(c->d_res_acc));
+            c->d_res_acc = nullptr;
+            c->res_acc_cap = 0;
+            const size_t cap = std::max<size_t>((size_t)reps, 512);
+            dmalloc(&c->d_res_acc, cap * 64 * sizeof(unsigned long long), "resident mean sums");
+            c->res_acc_cap = cap;
+        }
         const unsigned long long epoch0 = c->res_epoch + 1;
         c->res_epoch += (unsigned long long)reps + 1;  // rounds of this launch: reps (+1 spare)
         run(c, SV_K_MEAN, [&] {
             launch_mean_resident(c->dt, c->state, c->nres, ldexp(1.0, -c->n), with_oracle ? c->d_marked : nullptr,
                                  with_oracle ? c->n_marked : 0, reps, c->d_partials, c->d_gbar, c->d_res_slots,
-                                 epoch0, c->mean_resreg, c->stream);
+                                 epoch0, c->mean_resreg, c->d_res_acc, c->stream);
         });
         return;
     }
@@ -967,6 +977,7 @@ void destroy(sv_ctx *c) {
     cudaFree(c->d_sums);
     cudaFree(c->d_counter);
     cudaFree(c->d_gbar);
+    cudaFree(c->d_res_acc);
     cudaFree(c->d_res_slots);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;

@@ -298,11 +298,13 @@ bool mean_resident_fits(sv_dtype dt, uint64_t N, size_t partials_cap);
 // kernel's all-gather; epoch0: launch-unique, advanced by >= k + 1 per launch.
 // bar: 4 unsigned ints (the shared-memory kernel's {count, generation}, then
 // the register kernel's 64-bit arrival counter).  regs: the register-resident
-// kernel where its slice fits (else the shared-memory one).
+// kernel where its slice fits (else the shared-memory one).  acc: 64 k uint64
+// of device memory for the register kernel's fixed-point per-iteration sums
+// (zeroed here before the launch), or nullptr (fp64 gather every round).
 size_t mean_resident_slot_bytes(sv_dtype dt, uint64_t N);
 void launch_mean_resident(sv_dtype dt, void *a, uint64_t N, double inv_N, const uint64_t *marked, uint64_t m, int k,
                           double *partials, unsigned int *bar, void *slots, unsigned long long epoch0, bool regs,
-                          cudaStream_t s);
+                          void *acc, cudaStream_t s);
 
 void launch_init_uniform(sv_dtype dt, void *a, uint64_t N, int n, cudaStream_t s);
 void launch_init_zero(sv_dtype dt, void *a, uint64_t N, int has_origin, cudaStream_t s);

@@ -559,3 +559,21 @@ def test_graph_replay_long_k_is_chunked():
         sv.sv_iterate(c, k, sv.SV_DIFFUSE_WHT)
         got = sv.sv_get_amplitudes(c)
     assert_close(got, orc.iterate(a0.copy(), mk, k, orc.WHT), sv.SV_C128, "chunked graphs", n=n, k=k)
+
+
+def test_resident_mean_fp64_gather_variant():
+    """SV_RESREG_FX=0 (read once per process): the register-resident mean
+    kernel with fp64 partials + gather in every round instead of the
+    fixed-point integer sums -- the resident-path tests rerun in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    if os.environ.get("SV_RESREG_FX") == "0":
+        pytest.skip("this is the subprocess")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SV_RESREG_FX="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        "tests/test_parity_gpu.py", "-k", "mean_resident_and_launched or c2_n20 or bitwise"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-2000:]
