@@ -105,6 +105,14 @@ int pack_tile_params(sv_dtype dt, const PassArgs &a, bool check_lookup, KParams 
     for (int h = 0; h < 2; ++h)
         for (int bb = 0; bb < 16; ++bb) ka.coef[h][bb][0] = kc.coef[h][bb][0] != 0.0 ? kc.coef[h][bb][1] / kc.coef[h][bb][0] : 0.0;
     ka.pass_scale = pass_scale;
+    for (int h = 0; h < 2; ++h)
+        for (int bb = 0; bb < 16; ++bb)
+            for (int e = 0; e < 4; ++e) {
+                kc.coeff[h][bb][e] = (float)kc.coef[h][bb][e];
+                ka.coeff[h][bb][e] = (float)ka.coef[h][bb][e];
+            }
+    kc.pass_scalef = 1.0f;  // (the general flavour carries no pass factor)
+    ka.pass_scalef = (float)ka.pass_scale;
     return tan_form ? 2 : 1;
 }
 

@@ -194,6 +194,11 @@ template <int NOISY>
 struct KParamsT : KParams {
     double coef[2][16][4];
     double pass_scale;
+    // the same, rounded to fp32 on the host (complex64 kernels: the device
+    // conversions were ~90-150 F2F per thread per tile on the conversion pipe;
+    // host rounding is the same round-to-nearest, so results are unchanged)
+    float coeff[2][16][4];
+    float pass_scalef;
 };
 template <>
 struct KParamsT<0> : KParams {};
@@ -265,6 +270,26 @@ __device__ __forceinline__ void bfly_gen<float2>(float2 &x, float2 &y, const dou
     y = *reinterpret_cast<float2 *>(&u);
 }
 
+// complex64 with fp32 coefficients (KParamsT::coeff)
+__device__ __forceinline__ void bfly_gen(float2 &x, float2 &y, const float *m) {
+    const float2 W = make_float2(m[0], m[0]), X = make_float2(m[1], m[1]), Y = make_float2(m[2], m[2]),
+                 Z = make_float2(m[3], m[3]);
+    const unsigned long long a = *reinterpret_cast<unsigned long long *>(&x);
+    const unsigned long long b = *reinterpret_cast<unsigned long long *>(&y);
+    const unsigned long long w2 = *reinterpret_cast<const unsigned long long *>(&W);
+    const unsigned long long x2 = *reinterpret_cast<const unsigned long long *>(&X);
+    const unsigned long long y2 = *reinterpret_cast<const unsigned long long *>(&Y);
+    const unsigned long long z2 = *reinterpret_cast<const unsigned long long *>(&Z);
+    unsigned long long t, u;
+    asm("mul.rn.f32x2 %0, %2, %4;\n\t"
+        "fma.rn.f32x2 %0, %3, %5, %0;\n\t"
+        "mul.rn.f32x2 %1, %2, %6;\n\t"
+        "fma.rn.f32x2 %1, %3, %7, %1;"
+        : "=&l"(t), "=&l"(u) : "l"(a), "l"(b), "l"(w2), "l"(x2), "l"(y2), "l"(z2));
+    x = *reinterpret_cast<float2 *>(&t);
+    y = *reinterpret_cast<float2 *>(&u);
+}
+
 // Angle-error butterfly without its factor c: (u, v) -> (u + t v, t u - v).
 template <typename E>
 __device__ __forceinline__ void bfly_tan(E &x, E &y, double td) {
@@ -275,6 +300,12 @@ __device__ __forceinline__ void bfly_tan(E &x, E &y, double td) {
     x.y = a.y + t * y.y;
     y.x = t * a.x - y.x;
     y.y = t * a.y - y.y;
+}
+
+__device__ __forceinline__ void bfly_tan(float2 &x, float2 &y, float t) {
+    const float2 T = make_float2(t, t), a = x, b = y;
+    x = __ffma2_rn(T, b, a);                          // u = t b + a
+    y = __ffma2_rn(T, a, make_float2(-b.x, -b.y));    // v = t a - b
 }
 
 template <>
@@ -315,8 +346,13 @@ __device__ __forceinline__ void run_stages(E (&x)[L::NR], const KParamsT<NOISY> 
 #pragma unroll
                 for (int j = 0; j < L::NR; ++j)
                     if (!(j & (1 << i))) {
-                        if constexpr (NOISY == 2)
+                        constexpr bool F32 = sizeof(E) == 8;  // complex64: the host-rounded fp32 coefficients
+                        if constexpr (NOISY == 2 && F32)
+                            bfly_tan(x[j], x[j | (1 << i)], p.coeff[HALF][b][0]);
+                        else if constexpr (NOISY == 2)
                             bfly_tan(x[j], x[j | (1 << i)], p.coef[HALF][b][0]);
+                        else if constexpr (NOISY == 1 && F32)
+                            bfly_gen(x[j], x[j | (1 << i)], p.coeff[HALF][b]);
                         else if constexpr (NOISY == 1)
                             bfly_gen(x[j], x[j | (1 << i)], p.coef[HALF][b]);
                         else
@@ -564,6 +600,13 @@ __device__ __forceinline__ void apply_scale(E (&x)[NR], double s) {
     for (int j = 0; j < NR; ++j) scale(x[j], (R)s);
 }
 
+// x *= s with an fp32 factor (complex64, host-rounded pass_scalef)
+template <int NR>
+__device__ __forceinline__ void apply_scalef(float2 (&x)[NR], float s) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) scale(x[j], s);
+}
+
 // Decoherence (G22): the fp64 sum |a|^2 of the tile as stored, in a fixed
 // order (per thread in register order, warp xor tree, warps in order), into
 // out[tile] -- the global sum of Eq. 3 then needs no extra read
@@ -786,7 +829,7 @@ __global__ void __launch_bounds__(1 << (TB - RB), SV_TILE_MIN_BLOCKS) wht_tile2_
     if constexpr (NOISY) {  // renormalisation (decoherence) rides only on the general-2x2 flavours
         if (p.scale_in) apply_scale(x, *p.scale_in);
     }
-    if constexpr (NOISY == 2) apply_scale(x, p.pass_scale);  // the product of the pass's factors c
+    if constexpr (NOISY == 2) apply_scalef(x, p.pass_scalef);  // the product of the pass's factors c
     const bool has_marked = (p.mid == MID_ORACLE) && oracle_lookup(p, blockIdx.x, tid, &s_mlo, &s_mcnt);
     tile_body2<L, PRE, POST, U, NOISY, XCHG>(x, sm, p, base, reinterpret_cast<float2 *>(p.out) + base, tid, s_dst, has_marked, &s_mlo,
                                 &s_mcnt);
@@ -813,7 +856,10 @@ __global__ void __launch_bounds__(1 << (TB - RB), (TB - RB >= 9) ? 1 : SV_TILE_M
     if constexpr (NOISY) {  // renormalisation (decoherence) rides only on the general-2x2 flavours
         if (p.scale_in) apply_scale(x, *p.scale_in);
     }
-    if constexpr (NOISY == 2) apply_scale(x, p.pass_scale);  // the product of the pass's factors c
+    if constexpr (NOISY == 2) {  // the product of the pass's factors c
+        if constexpr (sizeof(E) == 8) apply_scalef(x, p.pass_scalef);
+        else apply_scale(x, p.pass_scale);
+    }
     const bool has_marked = (p.mid == MID_ORACLE) && oracle_lookup(p, blockIdx.x, tid, &s_mlo, &s_mcnt);
     tile_body<L, PRE, POST, U, NOISY, XCHG>(x, sm, p, base, reinterpret_cast<E *>(p.out) + base, tid, s_dst, has_marked, &s_mlo, &s_mcnt);
     if constexpr (NOISY) {

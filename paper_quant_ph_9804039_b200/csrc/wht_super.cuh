@@ -84,13 +84,13 @@ __device__ __forceinline__ void super_tile(const KParamsT<NOISY> &p, unsigned lo
     if constexpr (U >= 3 && U <= SV_2LAYOUT_MAX_U) {
         using L = Layout2<kTileBitsC64, kRegBitsC64>;
         global_load<L, 0>(x, reinterpret_cast<const float2 *>(p.in) + base, p, tid);
-        if constexpr (NOISY == 2) apply_scale(x, p.pass_scale);
+        if constexpr (NOISY == 2) apply_scalef(x, p.pass_scalef);
         tile_body2<L, PRE, POST, U, NOISY, false>(x, sm, p, base, reinterpret_cast<float2 *>(p.out) + base, tid,
                                                   static_cast<float2 *const *>(nullptr), false, &s_dummy, &s_dummy);
     } else {
         using L = Layout<float2, kTileBitsC64, kRegBitsC64>;
         global_load<L, 0>(x, reinterpret_cast<const float2 *>(p.in) + base, p, tid);
-        if constexpr (NOISY == 2) apply_scale(x, p.pass_scale);
+        if constexpr (NOISY == 2) apply_scalef(x, p.pass_scalef);
         tile_body<L, PRE, POST, U, NOISY, false>(x, sm, p, base, reinterpret_cast<float2 *>(p.out) + base, tid,
                                                  static_cast<float2 *const *>(nullptr), false, &s_dummy, &s_dummy);
     }
