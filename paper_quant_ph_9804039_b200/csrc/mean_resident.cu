@@ -416,28 +416,69 @@ __global__ void __launch_bounds__(NT, 1)
         sh = 54 - e;
         sh = sh > 1000 ? 1000 : sh;
     }
-    auto fx_total = [&](double r, double m, unsigned int slot, double &tr, double &ti) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            r += __shfl_xor_sync(0xffffffffu, r, o);
-            m += __shfl_xor_sync(0xffffffffu, m, o);
-        }
-        if (lane == 0) { red[2 * w] = r; red[2 * w + 1] = m; }
-        __syncthreads();
-        if (w == 0) {
-            double R0 = lane < NT / 32 ? red[2 * lane] : 0.0, M0 = lane < NT / 32 ? red[2 * lane + 1] : 0.0;
+    // invariant at the top of an iteration: v holds b = O a and (tr, ti) = sum(b)
+    if constexpr (FX) {
+        // Pipelined: sum(b') = sum_j s_j (2 mu - b_j) = 2 mu S - P with S = sum_j s_j
+        // (s_j = -1 on marked slots, a block constant) and P = sum_j s_j b_j, which
+        // is known BEFORE mu arrives -- so a block publishes its next partial the
+        // moment it reads mu, and the element update plus the next P overlap the
+        // round in flight.  (Exact algebra; the stored b' differ from the summed
+        // values by their own rounding only.)
+        // fold: warp trees -> smem -> warp 0 (valid in warp 0 only)
+        auto fold = [&](double r, double m, double &R, double &M) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
-                R0 += __shfl_xor_sync(0xffffffffu, R0, o);
-                M0 += __shfl_xor_sync(0xffffffffu, M0, o);
+                r += __shfl_xor_sync(0xffffffffu, r, o);
+                m += __shfl_xor_sync(0xffffffffu, m, o);
             }
-            if (lane == 0) {
-                // each component as hi + lo * 2^-48 (a 101-bit fixed-point value, exact
-                // to far below the partial's own fp64 rounding); the four words of the
-                // slot -- re_hi, im_hi, re_lo, im_lo -- sit on their own 128-B lines
-                // (L2 atomics on one line serialise: 4 x 148 on one line measured slower)
-                unsigned long long *sl = acc + (size_t)kAccWords * slot;
-                const double xr = ldexp(R0, sh), xi = ldexp(M0, sh);
+            if (lane == 0) { red[2 * w] = r; red[2 * w + 1] = m; }
+            __syncthreads();
+            R = 0.0;
+            M = 0.0;
+            if (w == 0) {
+                R = lane < NT / 32 ? red[2 * lane] : 0.0;
+                M = lane < NT / 32 ? red[2 * lane + 1] : 0.0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    R += __shfl_xor_sync(0xffffffffu, R, o);
+                    M += __shfl_xor_sync(0xffffffffu, M, o);
+                }
+            }
+        };
+        auto signed_sum = [&](double &pr, double &pi) {  // this thread's sum_j s_j v_j
+            pr = 0.0;
+            pi = 0.0;
+#pragma unroll
+            for (int j = 0; j < NPT; ++j)
+                if (j < nv) {
+                    const unsigned int sj = (mmask >> j) & 1u;
+                    pr += (double)flip_if(v[j].x, sj);
+                    pi += (double)flip_if(v[j].y, sj);
+                }
+        };
+        double sc = 0.0;
+#pragma unroll
+        for (int j = 0; j < NPT; ++j)
+            if (j < nv) sc += ((mmask >> j) & 1u) ? -1.0 : 1.0;
+        double S_blk, dummy, P_r, P_i, pr, pi;
+        fold(sc, 0.0, S_blk, dummy);
+        __syncthreads();  // red[] reused by the next fold
+        signed_sum(pr, pi);
+        fold(pr, pi, P_r, P_i);
+        for (int it = 0; it < k; ++it) {
+            const R two_mr = (R)(2.0 * tr * inv_N), two_mi = (R)(2.0 * ti * inv_N);
+            if (it + 1 == k) {  // the last a' = 2 mu - b is the result
+#pragma unroll
+                for (int j = 0; j < NPT; ++j) {
+                    v[j].x = two_mr - v[j].x;
+                    v[j].y = two_mi - v[j].y;
+                }
+                break;
+            }
+            unsigned long long *sl = acc + (size_t)kAccWords * (unsigned int)it;
+            if (w == 0 && lane == 0) {
+                // this block's sum of b' = O a', as the elements will hold it (2 mu in R)
+                const double xr = ldexp((double)two_mr * S_blk - P_r, sh), xi = ldexp((double)two_mi * S_blk - P_i, sh);
                 const long long hr = __double2ll_rn(xr), hi_ = __double2ll_rn(xi);
                 const long long lr = __double2ll_rn(ldexp(xr - (double)hr, 48));
                 const long long li = __double2ll_rn(ldexp(xi - (double)hi_, 48));
@@ -445,6 +486,23 @@ __global__ void __launch_bounds__(NT, 1)
                 red_relaxed_add_u64(sl + 16, ((unsigned long long)hi_ << 8) + 1ull);
                 red_relaxed_add_u64(sl + 32, ((unsigned long long)lr << 8) + 1ull);
                 red_relaxed_add_u64(sl + 48, ((unsigned long long)li << 8) + 1ull);
+            }
+            // b' = O a',  a' = 2 mu - b; the next P = sum_j s_j b'_j = sum_j a'_j
+            pr = 0.0;
+            pi = 0.0;
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) {
+                const unsigned int sj = (mmask >> j) & 1u;
+                const R ar = two_mr - v[j].x, ai = two_mi - v[j].y;
+                if (j < nv) {
+                    pr += (double)ar;
+                    pi += (double)ai;
+                }
+                v[j].x = flip_if(ar, sj);
+                v[j].y = flip_if(ai, sj);
+            }
+            fold(pr, pi, P_r, P_i);  // P of the new b, for the next publication
+            if (w == 0 && lane == 0) {
                 unsigned long long w0, w1, w2, w3;
                 do {
                     w0 = ld_relaxed_u64(sl);
@@ -457,37 +515,35 @@ __global__ void __launch_bounds__(NT, 1)
                 red[64] = ldexp((double)((long long)w0 >> 8) + ldexp((double)((long long)w2 >> 8), -48), -sh);
                 red[65] = ldexp((double)((long long)w1 >> 8) + ldexp((double)((long long)w3 >> 8), -48), -sh);
             }
+            __syncthreads();
+            tr = red[64];
+            ti = red[65];
         }
-        __syncthreads();
-        tr = red[64];
-        ti = red[65];
-    };
-    (void)fx_total;
-    // invariant at the top of an iteration: v holds b = O a and (tr, ti) = sum(b)
-    for (int it = 0; it < k; ++it) {
-        const R two_mr = (R)(2.0 * tr * inv_N), two_mi = (R)(2.0 * ti * inv_N);
-        if (it + 1 == k) {  // the last a' = 2 mu - b is the result
+    } else {
+        for (int it = 0; it < k; ++it) {
+            const R two_mr = (R)(2.0 * tr * inv_N), two_mi = (R)(2.0 * ti * inv_N);
+            if (it + 1 == k) {  // the last a' = 2 mu - b is the result
+#pragma unroll
+                for (int j = 0; j < NPT; ++j) {
+                    v[j].x = two_mr - v[j].x;
+                    v[j].y = two_mi - v[j].y;
+                }
+                break;
+            }
+            r = 0.0;
+            m = 0.0;
 #pragma unroll
             for (int j = 0; j < NPT; ++j) {
-                v[j].x = two_mr - v[j].x;
-                v[j].y = two_mi - v[j].y;
+                const unsigned int sj = (mmask >> j) & 1u;
+                v[j].x = flip_if(two_mr - v[j].x, sj);  // b' = O a',  a' = 2 mu - b
+                v[j].y = flip_if(two_mi - v[j].y, sj);
+                if (j < nv) {
+                    r += (double)v[j].x;
+                    m += (double)v[j].y;
+                }
             }
-            break;
+            grid_total(r, m, round++, tr, ti);
         }
-        r = 0.0;
-        m = 0.0;
-#pragma unroll
-        for (int j = 0; j < NPT; ++j) {
-            const unsigned int sj = (mmask >> j) & 1u;
-            v[j].x = flip_if(two_mr - v[j].x, sj);  // b' = O a',  a' = 2 mu - b
-            v[j].y = flip_if(two_mi - v[j].y, sj);
-            if (j < nv) {
-                r += (double)v[j].x;
-                m += (double)v[j].y;
-            }
-        }
-        if constexpr (FX) fx_total(r, m, (unsigned int)it, tr, ti);
-        else grid_total(r, m, round++, tr, ti);
     }
 #pragma unroll
     for (int j = 0; j < NPT; ++j)
