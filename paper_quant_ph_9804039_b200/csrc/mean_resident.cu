@@ -243,6 +243,17 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+// Round-to-nearest-even of |x| < 2^51 to an integer with one fp64 add (the
+// 1.5 * 2^52 magic number), and back: exact, no F2I / I2F.
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+__device__ __forceinline__ long long round_i64(double x, double &xd) {
+    const double t = x + kMagic;
+    xd = t - kMagic;  // the rounded value as a double (exact)
+    return __double_as_longlong(t) - __double_as_longlong(kMagic);
+}
+__device__ __forceinline__ double i64_to_double(long long i) {  // |i| < 2^51
+    return __longlong_as_double(i + __double_as_longlong(kMagic)) - kMagic;
+}
 constexpr int kAccWords = 64;  // uint64 per iteration slot of the fixed-point sums: 4 words, 128 B apart
 __device__ __forceinline__ void ld_relaxed_v2_u64(const unsigned long long *p, unsigned long long &a,
                                                   unsigned long long &b) {
@@ -393,16 +404,16 @@ __global__ void __launch_bounds__(NT, 1)
     // Fixed-point rounds (FX).  Every later sum is of b' = O a' over a subset
     // of the state, so |sum| <= sqrt(N) ||a|| (Cauchy-Schwarz; D and O are
     // unitary).  One more fp64 round gives ||a||^2; every block derives the
-    // same scale 2^sh with 2 sqrt(N) ||a|| 2^sh < 2^54 and, per iteration,
+    // same scale 2^sh with 2 sqrt(N) ||a|| 2^sh < 2^51 and, per iteration,
     // adds its partial as two's-complement integers (a high word at 2^-sh and
-    // a low word at 2^-(sh+48)), each with an arrival count in its low 8 bits
-    // -- four relaxed 64-bit atomics into this iteration's own zeroed slot.
-    // Integer adds commute, so the total is the same bits in every block and
-    // run (deterministic, G14) and it is the EXACT sum of the partials to
-    // 2^-(sh+48) ~ 1e-29 of sqrt(N) ||a||, rounded to fp64 once (the fp64
-    // gather rounds 148 times); count and data share each word, so no fence
-    // and no gather: a block polls one 32-B slot until all four counts reach
-    // the grid size.
+    // a low word at 2^-(sh+44)), each with an arrival count in its low 8 bits
+    // -- four relaxed 64-bit atomics into this iteration's own zeroed slot,
+    // each word on its own 128-B line.  Integer adds commute, so the total is
+    // the same bits in every block and run (deterministic, G14) and it is the
+    // EXACT sum of the partials to 2^-(sh+44) ~ 1e-28 of sqrt(N) ||a||,
+    // rounded to fp64 once (the fp64 gather rounds 148 times); count and data
+    // share each word, so no fence and no gather: a block polls the four
+    // words until every count reaches the grid size.
     int sh = 0;
     if constexpr (FX) {
         double q = 0.0;
@@ -413,7 +424,7 @@ __global__ void __launch_bounds__(NT, 1)
         grid_total(q, 0.0, round++, tq, tdummy);
         int e = 0;
         frexp(2.0 * sqrt((double)N * tq) + 1e-300, &e);  // bound < 2^e
-        sh = 54 - e;
+        sh = 51 - e;  // |partials|, |total| < 2^50: inside the magic-number rounding range
         sh = sh > 1000 ? 1000 : sh;
     }
     // invariant at the top of an iteration: v holds b = O a and (tr, ti) = sum(b)
@@ -460,11 +471,15 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int j = 0; j < NPT; ++j)
             if (j < nv) sc += ((mmask >> j) & 1u) ? -1.0 : 1.0;
+        const double up = ldexp(1.0, sh), dn = ldexp(1.0, -sh);  // exact powers of two (|sh| <= 1000)
         double S_blk, dummy, P_r, P_i, pr, pi;
         fold(sc, 0.0, S_blk, dummy);
         __syncthreads();  // red[] reused by the next fold
         signed_sum(pr, pi);
         fold(pr, pi, P_r, P_i);
+#if SV_RESREG_TRACE
+        long long tp[5] = {0, 0, 0, 0, 0}, tprev = clock64();
+#endif
         for (int it = 0; it < k; ++it) {
             const R two_mr = (R)(2.0 * tr * inv_N), two_mi = (R)(2.0 * ti * inv_N);
             if (it + 1 == k) {  // the last a' = 2 mu - b is the result
@@ -476,17 +491,31 @@ __global__ void __launch_bounds__(NT, 1)
                 break;
             }
             unsigned long long *sl = acc + (size_t)kAccWords * (unsigned int)it;
+#if SV_RESREG_TRACE
+            long long tc = clock64();
+            tp[0] += tc - tprev;  // barrier -> top
+            tprev = tc;
+#endif
             if (w == 0 && lane == 0) {
                 // this block's sum of b' = O a', as the elements will hold it (2 mu in R)
-                const double xr = ldexp((double)two_mr * S_blk - P_r, sh), xi = ldexp((double)two_mi * S_blk - P_i, sh);
-                const long long hr = __double2ll_rn(xr), hi_ = __double2ll_rn(xi);
-                const long long lr = __double2ll_rn(ldexp(xr - (double)hr, 48));
-                const long long li = __double2ll_rn(ldexp(xi - (double)hi_, 48));
+                // (scalings by exact powers of two and magic-number roundings: ldexp and
+                // F2I / I2F were ~800 cycles on this, the iteration's critical path)
+                const double xr = ((double)two_mr * S_blk - P_r) * up, xi = ((double)two_mi * S_blk - P_i) * up;
+                double hrd, hid;
+                const long long hr = round_i64(xr, hrd), hi_ = round_i64(xi, hid);
+                double unused;
+                const long long lr = round_i64((xr - hrd) * 0x1p44, unused);
+                const long long li = round_i64((xi - hid) * 0x1p44, unused);
                 red_relaxed_add_u64(sl, ((unsigned long long)hr << 8) + 1ull);
                 red_relaxed_add_u64(sl + 16, ((unsigned long long)hi_ << 8) + 1ull);
                 red_relaxed_add_u64(sl + 32, ((unsigned long long)lr << 8) + 1ull);
                 red_relaxed_add_u64(sl + 48, ((unsigned long long)li << 8) + 1ull);
             }
+#if SV_RESREG_TRACE
+            tc = clock64();
+            tp[1] += tc - tprev;  // publish
+            tprev = tc;
+#endif
             // b' = O a',  a' = 2 mu - b; the next P = sum_j s_j b'_j = sum_j a'_j
             pr = 0.0;
             pi = 0.0;
@@ -501,7 +530,17 @@ __global__ void __launch_bounds__(NT, 1)
                 v[j].x = flip_if(ar, sj);
                 v[j].y = flip_if(ai, sj);
             }
+#if SV_RESREG_TRACE
+            tc = clock64();
+            tp[2] += tc - tprev;  // update
+            tprev = tc;
+#endif
             fold(pr, pi, P_r, P_i);  // P of the new b, for the next publication
+#if SV_RESREG_TRACE
+            tc = clock64();
+            tp[3] += tc - tprev;  // fold
+            tprev = tc;
+#endif
             if (w == 0 && lane == 0) {
                 unsigned long long w0, w1, w2, w3;
                 do {
@@ -512,13 +551,24 @@ __global__ void __launch_bounds__(NT, 1)
                 } while ((w0 & 0xffull) != nb || (w1 & 0xffull) != nb || (w2 & 0xffull) != nb ||
                          (w3 & 0xffull) != nb);
                 // wrapped intermediate sums are harmless: the final integer fits
-                red[64] = ldexp((double)((long long)w0 >> 8) + ldexp((double)((long long)w2 >> 8), -48), -sh);
-                red[65] = ldexp((double)((long long)w1 >> 8) + ldexp((double)((long long)w3 >> 8), -48), -sh);
+                red[64] = (i64_to_double((long long)w0 >> 8) + i64_to_double((long long)w2 >> 8) * 0x1p-44) * dn;
+                red[65] = (i64_to_double((long long)w1 >> 8) + i64_to_double((long long)w3 >> 8) * 0x1p-44) * dn;
             }
             __syncthreads();
             tr = red[64];
             ti = red[65];
+#if SV_RESREG_TRACE
+            tc = clock64();
+            tp[4] += tc - tprev;  // wait + barrier
+            tprev = tc;
+#endif
         }
+#if SV_RESREG_TRACE
+        if (tid == 0 && (blockIdx.x == 0 || blockIdx.x == nb / 2 || blockIdx.x + 1 == nb))
+            printf("resreg FX trace block %u iters %d: cycles/iter top %.0f publish %.0f update %.0f fold %.0f wait %.0f\n",
+                   blockIdx.x, k - 1, (double)tp[0] / (k - 1), (double)tp[1] / (k - 1), (double)tp[2] / (k - 1),
+                   (double)tp[3] / (k - 1), (double)tp[4] / (k - 1));
+#endif
     } else {
         for (int it = 0; it < k; ++it) {
             const R two_mr = (R)(2.0 * tr * inv_N), two_mi = (R)(2.0 * ti * inv_N);
