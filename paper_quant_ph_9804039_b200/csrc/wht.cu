@@ -510,10 +510,11 @@ void launch_whole_state(sv_dtype dt, void *state, int n, int k, int with_oracle,
         if (dt == SV_C64) {
             SV_WR(float2, 2, 2); SV_WR(float2, 3, 2); SV_WR(float2, 2, 3); SV_WR(float2, 4, 2); SV_WR(float2, 3, 3);
             SV_WR(float2, 2, 4); SV_WR(float2, 5, 2); SV_WR(float2, 4, 3); SV_WR(float2, 3, 4); SV_WR(float2, 6, 2);
-            SV_WR(float2, 5, 3); SV_WR(float2, 4, 4);
+            SV_WR(float2, 5, 3); SV_WR(float2, 4, 4); SV_WR(float2, 0, 5);
         } else {
             SV_WR(double2, 2, 2); SV_WR(double2, 3, 2); SV_WR(double2, 2, 3); SV_WR(double2, 4, 2); SV_WR(double2, 3, 3);
-            SV_WR(double2, 2, 4); SV_WR(double2, 4, 3); SV_WR(double2, 3, 4);
+            SV_WR(double2, 2, 4); SV_WR(double2, 4, 3); SV_WR(double2, 3, 4); SV_WR(double2, 1, 4);
+            SV_WR(double2, 0, 5);
         }
 #undef SV_WR
     }

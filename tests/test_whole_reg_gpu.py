@@ -23,7 +23,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SPLITS = {
     2: [("c64", n) for n in (9, 10, 11, 12, 13)] + [("c128", n) for n in (9, 10, 11)],
     3: [("c64", n) for n in (10, 11, 12, 13)] + [("c128", n) for n in (10, 11, 12)],
-    4: [("c64", n) for n in (11, 12, 13)] + [("c128", n) for n in (11, 12)],
+    4: [("c64", n) for n in (11, 12, 13)] + [("c128", n) for n in (10, 11, 12)],
+    5: [("c64", 10), ("c128", 10)],
 }
 DTS = {"c64": sv.SV_C64, "c128": sv.SV_C128}
 K, M, SIGMA, RATE = 3, 3, 0.07, 0.02
